@@ -1,0 +1,209 @@
+"""fp64 CPU oracle for arXiv cs/0103001 -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference``) may import this package.  The
+product library (``paper_cs_0103001_b200``) never imports, links or calls it
+and shares no code with it.
+
+Thin ctypes wrapper over ``oracle.c``; every function there cites the PAPER.md
+passage it follows.  Arrays are numpy complex128 (interleaved re/im doubles).
+All functions are pinned by ``tests/test_oracle.py`` (nothing here is "parity
+unpinned").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c (gcc -O2 -fopenmp, no fast-math)."""
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=gnu11", "-fopenmp", "-fPIC", "-shared", "-fno-fast-math",
+             "-o", _SO, src, "-lm"]
+        )
+    return _SO
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        i64, vp, ci, cd = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+        sig = {
+            "oracle_bitrev_order": [i64, vp],
+            "oracle_fft": [vp, vp, i64],
+            "oracle_ifft": [vp, vp, i64],
+            "oracle_ifft_plus_tree": [vp, vp, i64],
+            "oracle_dft_bruteforce": [vp, vp, i64, ci],
+            "oracle_eval_exp_poly": [vp, i64, cd, vp],
+            "oracle_fft_batch": [vp, vp, i64, i64, ci],
+            "oracle_fft2d": [vp, vp, i64, i64],
+            "oracle_ifft2d": [vp, vp, i64, i64],
+            "oracle_dft2d_bruteforce": [vp, vp, i64, i64, ci],
+            "oracle_gauss_filter": [i64, i64, cd, vp],
+            "oracle_filter_pipeline": [vp, vp, i64, i64, vp],
+            "oracle_gauss_pipeline": [vp, vp, i64, i64, cd],
+            "oracle_dft_bins": [vp, i64, vp, i64, ci, vp],
+        }
+        for name, args in sig.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = ci
+        lib.oracle_num_threads.restype = ci
+        lib.oracle_set_num_threads.argtypes = [ci]
+        _lib = lib
+    return _lib
+
+
+def _c128(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise OracleError(f"{what}: oracle status {rc}")
+
+
+def num_threads() -> int:
+    return _load().oracle_num_threads()
+
+
+def set_num_threads(t: int) -> None:
+    _load().oracle_set_num_threads(int(t))
+
+
+def bitrev_order(n: int) -> np.ndarray:
+    out = np.empty(n, dtype=np.int64)
+    _check(_load().oracle_bitrev_order(n, out.ctypes.data), "bitrev_order")
+    return out
+
+
+def fft(x) -> np.ndarray:
+    """Eq. E2: (1/N) sum_j x_j e^{-2 pi i jk/N} via the paper's tree (O2)."""
+    x = _c128(x)
+    out = np.empty_like(x)
+    _check(_load().oracle_fft(x.ctypes.data, out.ctypes.data, x.size), "fft")
+    return out
+
+
+def ifft(c) -> np.ndarray:
+    """Sec. 3 inverse: N * FFT(c)[(N-k) mod N], unscaled +sign sum (O3)."""
+    c = _c128(c)
+    out = np.empty_like(c)
+    _check(_load().oracle_ifft(c.ctypes.data, out.ctypes.data, c.size), "ifft")
+    return out
+
+
+def ifft_plus_tree(c) -> np.ndarray:
+    c = _c128(c)
+    out = np.empty_like(c)
+    _check(_load().oracle_ifft_plus_tree(c.ctypes.data, out.ctypes.data, c.size), "ifft_plus")
+    return out
+
+
+def dft_bruteforce(x, inverse: bool = False) -> np.ndarray:
+    x = _c128(x)
+    out = np.empty_like(x)
+    _check(_load().oracle_dft_bruteforce(x.ctypes.data, out.ctypes.data, x.size, int(inverse)),
+           "dft_bruteforce")
+    return out
+
+
+def eval_exp_poly(c, x: float) -> complex:
+    c = _c128(c)
+    out = np.empty(1, dtype=np.complex128)
+    _check(_load().oracle_eval_exp_poly(c.ctypes.data, c.size, float(x), out.ctypes.data),
+           "eval_exp_poly")
+    return complex(out[0])
+
+
+def fft_batch(x, inverse: bool = False) -> np.ndarray:
+    """Rows of a 2D array transformed independently (OpenMP over rows)."""
+    x = _c128(x)
+    assert x.ndim == 2
+    out = np.empty_like(x)
+    _check(_load().oracle_fft_batch(x.ctypes.data, out.ctypes.data, x.shape[1], x.shape[0],
+                                    int(inverse)), "fft_batch")
+    return out
+
+
+def fft2d(f) -> np.ndarray:
+    """eq5 (1/N, N = rows) via rows -> x M -> columns (O4)."""
+    f = _c128(f)
+    out = np.empty_like(f)
+    _check(_load().oracle_fft2d(f.ctypes.data, out.ctypes.data, *f.shape), "fft2d")
+    return out
+
+
+def ifft2d(F) -> np.ndarray:
+    """2D-IDFT (1/M, M = columns) (O4)."""
+    F = _c128(F)
+    out = np.empty_like(F)
+    _check(_load().oracle_ifft2d(F.ctypes.data, out.ctypes.data, *F.shape), "ifft2d")
+    return out
+
+
+def dft2d_bruteforce(f, inverse: bool = False) -> np.ndarray:
+    f = _c128(f)
+    out = np.empty_like(f)
+    _check(_load().oracle_dft2d_bruteforce(f.ctypes.data, out.ctypes.data, f.shape[0],
+                                           f.shape[1], int(inverse)), "dft2d_bruteforce")
+    return out
+
+
+def gauss_filter(N: int, M: int, param: float = 0.1) -> np.ndarray:
+    H = np.empty((N, M), dtype=np.float64)
+    _check(_load().oracle_gauss_filter(N, M, float(param), H.ctypes.data), "gauss_filter")
+    return H
+
+
+def filter_pipeline(f, H) -> np.ndarray:
+    f = _c128(f)
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    out = np.empty_like(f)
+    _check(_load().oracle_filter_pipeline(f.ctypes.data, out.ctypes.data, f.shape[0], f.shape[1],
+                                          H.ctypes.data), "filter_pipeline")
+    return out
+
+
+def gauss_pipeline(f, param: float = 0.1) -> np.ndarray:
+    f = _c128(f)
+    out = np.empty_like(f)
+    _check(_load().oracle_gauss_pipeline(f.ctypes.data, out.ctypes.data, f.shape[0], f.shape[1],
+                                         float(param)), "gauss_pipeline")
+    return out
+
+
+def dft_bins(x, bins, inverse: bool = False) -> np.ndarray:
+    """Selected bins of one transform by compensated direct sums (O7)."""
+    x = _c128(x)
+    bins = np.ascontiguousarray(bins, dtype=np.int64)
+    out = np.empty(bins.size, dtype=np.complex128)
+    _check(_load().oracle_dft_bins(x.ctypes.data, x.size, bins.ctypes.data, bins.size,
+                                   int(inverse), out.ctypes.data), "dft_bins")
+    return out
+
+
+def rel_l2(a, ref) -> float:
+    """O8: sqrt(sum |a-ref|^2) / sqrt(sum |ref|^2), fp64 (numpy pairwise sums)."""
+    a = np.asarray(a).astype(np.complex128, copy=False).ravel()
+    ref = np.asarray(ref).astype(np.complex128, copy=False).ravel()
+    d = a - ref
+    num = np.sum(d.real * d.real + d.imag * d.imag)
+    den = np.sum(ref.real * ref.real + ref.imag * ref.imag)
+    return float(np.sqrt(num / den)) if den > 0 else float(np.sqrt(num))
