@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the paper's FFT hot path on B200 (see DESIGN.md
+"Measurement").
+
+Default workload (BASELINE.json configs[1], the metric's config, "C2"):
+4096 independent complex64 transforms of N = 65536 (N(0,1) parts, seed 2).
+One step = forward (1/N) + inverse over the whole batch.  Metric: GFLOP/s in
+the 5 N log2 N convention (2 transforms per row per step), whole job.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C2|C3|C4|C5|C1] [--extra]
+
+Multi-GPU (torchrun, one process per GPU): the C2 batch is sharded with no
+collective (weak scaling: every rank transforms its own 4096 rows of the
+global seeded input stream).  Timing: CUDA events on the plan stream,
+barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import fixtures  # noqa: E402  (seeded inputs; no method arithmetic)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- distributed
+def dist_init(n_gpus):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if _cuda_ok() else "gloo")
+    return ws, rank, local
+
+
+def _cuda_ok():
+    import torch
+
+    return torch.cuda.is_available()
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(ws, v: float) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if _cuda_ok() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------- C2
+def flops_1d(n, batch, transforms_per_row=2):
+    return 5.0 * n * math.log2(n) * batch * transforms_per_row
+
+
+def cpu_baseline_c2(n=65536, target_s=12.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of
+    the C2 workload (forward + inverse of the first rows)."""
+    import oracle
+
+    cores = oracle.num_threads()
+    rows = 16
+    while True:
+        x = fixtures.complex_input(rows * n, fixtures.NORMAL, seed=2).reshape(rows, n)
+        t0 = time.perf_counter()
+        y = oracle.fft_batch(x)
+        oracle.fft_batch(y, inverse=True)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 4 or rows >= 4096:
+            break
+        rows = min(4096, int(rows * max(2.0, (target_s / 4) / max(dt, 1e-3))))
+    gf = flops_1d(n, rows) / dt / 1e9
+    return {"value": round(gf, 4), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"{rows} of 4096 rows of C2 (N=65536), forward+inverse, fp64, {dt:.1f} s"}
+
+
+def bench_c2(args, ws, rank, local):
+    import torch
+
+    import paper_cs_0103001_b200 as b
+
+    n, batch = 65536, 4096
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    # rank r owns global rows [r*batch, (r+1)*batch) of the seeded stream (weak scaling)
+    x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=2, offset=rank * batch * n)
+    xh = torch.from_numpy(x.reshape(batch, n)).pin_memory()
+    xd = xh.to(dev, non_blocking=True)
+    yd = torch.empty_like(xd)
+    zd = torch.empty_like(xd)
+    plan = b.Plan((n,), batch=batch, precision=b.C64, stream=stream)
+    ws_t = torch.empty(max(plan.workspace_bytes(), 1), dtype=torch.uint8, device=dev)
+    if plan.workspace_bytes():
+        plan.set_workspace(ws_t)
+    torch.cuda.synchronize()
+
+    def step():
+        plan.forward(xd, yd)
+        l1 = plan.last_launch_count()
+        plan.inverse(yd, zd)
+        return l1 + plan.last_launch_count()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            plan.forward(xd, yd)
+            launches += plan.last_launch_count()
+            ev[i][1].record(stream)
+            plan.inverse(yd, zd)
+            launches += plan.last_launch_count()
+            ev[i][2].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    ms = allreduce_max(ws, ms)
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    inv_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    ms_step = ms / args.steps
+    value = flops_1d(n, batch * ws) / (ms_step / 1e3) / 1e9
+
+    # roofline of the dominant call (the forward transform: its launches)
+    peak, peak_kind = hbm_peak()
+    alg_bytes = 16.0 * n * batch
+    fwd_avg = statistics.mean(fwd_ms)
+    achieved = alg_bytes / (fwd_avg / 1e3) / 1e9
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "c2_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # end to end through the public API on host buffers (pinned), H2D + D2H inside
+    e2e = None
+    if not args.no_e2e:
+        out_h = torch.empty_like(xh).pin_memory()
+        back_h = torch.empty_like(xh).pin_memory()
+        plan.execute_host(+1, xh, out_h)
+        torch.cuda.synchronize()
+        barrier(ws)
+        e2e_steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            plan.execute_host(+1, xh, out_h)
+            plan.execute_host(-1, out_h, back_h)
+        dt = time.perf_counter() - t0
+        dt = allreduce_max(ws, dt)
+        e2e = {"value": round(flops_1d(n, batch * ws) * e2e_steps / dt / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": 2 * 8 * n * batch, "d2h_bytes_per_step": 2 * 8 * n * batch,
+               "steps": e2e_steps, "timer": "host wall clock around synchronous execute_host"}
+        # parity spot check of the timed buffers (first row) on the device
+    err = float(torch.linalg.vector_norm(zd[:64] - xd[:64]) / torch.linalg.vector_norm(xd[:64]))
+    res = {
+        "metric": "FFT GFLOP/s (5N*log2N), forward(1/N)+inverse",
+        "value": round(value, 3),
+        "unit": "GFLOP/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32 arithmetic)",
+        "data": "synthetic (counter-based seeded N(0,1), fixtures/gen.c)",
+        "config": {"workload": "C2: BASELINE configs[1], 4096 x N=65536 complex64 per GPU, forward(1/N)+inverse",
+                   "n": n, "batch_per_gpu": batch, "global_batch": batch * ws,
+                   "parallelism": f"batch-sharded x{ws}, no collective",
+                   "l2": "inputs 2 GiB per buffer >> 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "forward transform (all its launches)", "peak_source": peak_kind,
+                     "alg_bytes_per_launch": alg_bytes,
+                     "fwd_ms_avg": round(fwd_avg, 4), "inv_ms_avg": round(statistics.mean(inv_ms), 4)},
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "roundtrip_rel_l2_first64rows": err,
+        "clocks": clk.summary(),
+    }
+    plan.destroy()
+    return res
+
+
+# ---------------------------------------------------------- extra configs
+def bench_c3(args, local):
+    import torch
+
+    import paper_cs_0103001_b200 as b
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    img = fixtures.sky_image(2048, 2048, seed=3)
+    idev = torch.from_numpy(img).to(dev)
+    out = torch.empty((2048, 2048), dtype=torch.complex64, device=dev)
+    plan = b.Plan((2048, 2048), batch=1, precision=b.C64, flags=b.IN_REAL_F32, stream=stream)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        plan.filter_pipeline(idev, out, b.FILTER_GAUSS, 0.1)
+    times = []
+    for _ in range(max(args.steps, 20)):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            flush.zero_()  # cold L2: write 512 MiB (> 126 MB L2) on the plan stream, before the timed region
+            s.record(stream)
+            plan.filter_pipeline(idev, out, b.FILTER_GAUSS, 0.1)
+            e.record(stream)
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    med = statistics.median(times)
+    n = 2048 * 2048
+    gf = 2 * 5 * n * math.log2(n) / (med / 1e3) / 1e9
+    peak, _ = hbm_peak()
+    alg = 32.0 * n
+    plan.destroy()
+    return {"workload": "C3: 2048^2 sky image Gaussian pipeline (cold L2)", "ms_median": round(med, 4),
+            "ms_min": round(min(times), 4), "GFLOP/s": round(gf, 1),
+            "hbm_frac": round(alg / (med / 1e3) / 1e9 / peak, 4)}
+
+
+def bench_c1(args, local):
+    import torch
+
+    import paper_cs_0103001_b200 as b
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    x = fixtures.complex_input(1024, fixtures.UNIFORM, seed=1, dtype=np.complex128)
+    xd = torch.from_numpy(x).to(dev)
+    yd = torch.empty_like(xd)
+    plan = b.Plan((1024,), batch=1, precision=b.C128, stream=stream)
+    for _ in range(5):
+        plan.forward(xd, yd)
+        plan.inverse(yd, yd)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(50):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        plan.forward(xd, yd)
+        plan.inverse(yd, yd)
+        e.record(stream)
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e) * 1e3)
+    plan.destroy()
+    return {"workload": "C1: N=1024 complex128 forward+inverse (latency)",
+            "us_median": round(statistics.median(times), 2), "us_min": round(min(times), 2)}
+
+
+def reference_arm(args, ws, rank):
+    """--impl reference: the fp64 oracle (the paper's plain radix-2 tree) as it
+    stands, on this host's cores, on a bounded sample of the C2 workload."""
+    if rank != 0:
+        return None
+    import oracle
+
+    n = 65536
+    rows = 32
+    cores = oracle.num_threads()
+    x = fixtures.complex_input(rows * n, fixtures.NORMAL, seed=2).reshape(rows, n)
+    for _ in range(args.warmup):
+        oracle.fft_batch(x[:2])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        y = oracle.fft_batch(x)
+        oracle.fft_batch(y, inverse=True)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = flops_1d(n, rows) / dt / 1e9
+    return {
+        "impl": "reference",
+        "metric": "FFT GFLOP/s (5N*log2N), forward(1/N)+inverse",
+        "value": round(val, 4), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2: BASELINE configs[1] (bounded sample: 32 of 4096 rows per step)",
+                   "n": n, "rows_per_step": rows},
+        "cpu_baseline": {"value": round(val, 4), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{rows} rows x N=65536 forward+inverse per step"},
+        "e2e": {"value": round(val, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--extra", action="store_true", help="also time C1 and C3 (rank 0)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        res = reference_arm(args, ws, rank)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    res = bench_c2(args, ws, rank, local)
+    if rank == 0:
+        if ws == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline_c2()
+        if args.extra:
+            res["extra"] = {"C1": bench_c1(args, local), "C3": bench_c3(args, local)}
+        print(json.dumps(res), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

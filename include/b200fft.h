@@ -1,0 +1,158 @@
+/*
+ * b200fft.h -- C ABI of the B200-native FFT library for the computation of
+ * arXiv cs/0103001 (Higuera, Sarria, Fonseca, Idarraga, "Construction of an
+ * algorithm in parallel for the Fast Fourier Transform").
+ *
+ * Citations "P:a-b" are line ranges of the paper's text, with the
+ * section / equation they fall in.
+ *
+ * Operations (what is computed)
+ * -----------------------------
+ *  forward 1D  (Eq. E2 / Eq. coefFourier, Sec. 2):
+ *      X[k] = (1/N) * sum_{j<N} x[j] * exp(-2 pi i j k / N)
+ *  inverse 1D  (Eq. E3 at x_k = 2 pi k / N; Sec. 3):
+ *      f[j] = sum_{k<N} c[k] * exp(+2 pi i j k / N)          (no 1/N)
+ *  forward 2D  (eq5, Sec. 5), f is N x M row-major, N = rows:
+ *      F(u,v) = (1/N) sum_x sum_y f(x,y) exp(-2 pi i (ux/N + vy/M))
+ *  inverse 2D  (2D-IDFT):
+ *      f(x,y) = (1/M) sum_u sum_v F(u,v) exp(+2 pi i (ux/N + vy/M))
+ *  filter pipeline (Sec. 6): out = IDFT2( H .* DFT2(in) ), H real,
+ *      multiplied into the real and imaginary parts.
+ *
+ * Conventions
+ * -----------
+ *  - Data are interleaved complex: complex64 = {float re, im} (8 B),
+ *    complex128 = {double re, im} (16 B), batch-major, contiguous, in DEVICE
+ *    memory owned by the caller (e.g. torch tensors).  Pointers must be
+ *    aligned to the element size (8 / 16 B); otherwise FFT_E_INVALID_ARG.
+ *  - Sizes are powers of two (the paper pads to the next power of two,
+ *    P:366-367); anything else is FFT_E_INVALID_SIZE (see per-call limits).
+ *  - Calls are asynchronous on the plan's stream (default: the legacy
+ *    default stream; set it with fft_plan_set_stream).  Argument errors are
+ *    returned synchronously; asynchronous CUDA faults surface on a later
+ *    call.  After an error the output is undefined ("no partial result").
+ *  - A plan is not thread-safe; distinct plans may be used concurrently.
+ *  - Nothing throws across this ABI; every call returns an fft_status, and
+ *    fft_last_error() gives a thread-local detail string for the last
+ *    failure.
+ *  - There is no CPU fallback: every transform runs in the library's sm_100a
+ *    kernels.
+ */
+#ifndef B200FFT_H
+#define B200FFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fft_plan_s* fft_plan; /* opaque, library-owned */
+
+typedef enum {
+    FFT_OK = 0,
+    FFT_E_INVALID_SIZE = 1, /* n not a power of two, < 1, or over the limit */
+    FFT_E_INVALID_ARG = 2,  /* null / misaligned pointer, bad rank, bad flag */
+    FFT_E_UNSUPPORTED = 3,  /* valid request this build does not implement */
+    FFT_E_CUDA = 4,         /* a CUDA runtime error (detail in fft_last_error) */
+    FFT_E_NCCL = 5,         /* an NCCL error */
+    FFT_E_ALLOC = 6,        /* device / host allocation failed */
+    FFT_E_STATE = 7         /* call not valid in the plan's current state */
+} fft_status;
+
+typedef enum { FFT_C64 = 0, FFT_C128 = 1 } fft_precision;
+
+typedef enum {
+    FFT_FILTER_NONE = 0,  /* H = 1 */
+    /* Gaussian low-pass of BASELINE configs[2]/[3]:
+     *   H(u,v) = exp(-(k_u^2 / (2 s_N^2) + k_v^2 / (2 s_M^2))),
+     *   k_u = u (u < N/2) else u - N (signed index), s_N = param * N / 2
+     *   ("param * Nyquist"; param = 0.1 in the configs).  Square: the usual
+     *   exp(-(kx^2+ky^2)/(2 (param Nyq)^2)). */
+    FFT_FILTER_GAUSS = 1,
+    /* Eq. (filtro), read literally on the unshifted spectrum:
+     *   H = 0 if sqrt((u - N/2)^2 + (v - M/2)^2) <= b, else 1;  b = param. */
+    FFT_FILTER_IDEAL_LITERAL = 2,
+    /* The centred low-pass reading of Eq. (filtro):
+     *   H = 1 if sqrt(k_u^2 + k_v^2) <= b, else 0 (signed k);  b = param. */
+    FFT_FILTER_IDEAL_LOWPASS = 3
+} fft_filter;
+
+/* plan flags (fft_plan_create_ex) */
+enum {
+    FFT_FLAG_NONE = 0,
+    /* fft2d_filter_pipeline input is float32 real [N][M] (promoted to complex
+     * in the first pass's load, BASELINE configs[2]); output stays complex. */
+    FFT_IN_REAL_F32 = 1u << 1,
+    /* distributed 1D: leave the output in the four-step transposed order
+     * X[k1 + N1 k2] stored at [k1][k2] (one all-to-all less).  */
+    FFT_OUT_TRANSPOSED = 1u << 0
+};
+
+/* Short form from BASELINE.json's north_star: rank = transform
+ * dimensionality (1: `batch` transforms of length n; 2: `batch` n x n grids),
+ * complex64.  Limits: 1D n in [1, 2^30]; 2D n in [1, 8192] per side. */
+fft_status fft_plan_create(fft_plan* out, int64_t n, int64_t batch, int rank);
+
+/* dims[0..rank-1]: rank 1 -> {n}; rank 2 -> {N rows, M cols}.  flags: the
+ * FFT_* flags above.  complex128 limits: 1D n <= 2^28, 2D sides <= 4096. */
+fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int64_t batch,
+                              fft_precision prec, unsigned flags);
+
+/* cudaStream_t as void* (e.g. torch.cuda.current_stream().cuda_stream). */
+fft_status fft_plan_set_stream(fft_plan plan, void* cuda_stream);
+
+/* Scratch the plan needs for multi-pass transforms (0 if none).  If the
+ * caller never calls fft_plan_set_workspace the library allocates it itself
+ * on first use.  The caller keeps ownership of memory it passes in. */
+size_t fft_plan_workspace_bytes(fft_plan plan);
+fft_status fft_plan_set_workspace(fft_plan plan, void* dev_ptr, size_t bytes);
+
+/* Forward (1/N, or eq5's 1/N for rank 2) and inverse (unscaled, or the
+ * 2D-IDFT's 1/M) transforms.  in/out: device pointers to the local data
+ * (batch * prod(dims) elements); out may equal in. */
+fft_status fft_forward(fft_plan plan, const void* in, void* out);
+fft_status fft_inverse(fft_plan plan, const void* in, void* out);
+
+/* Rank-2 plans only: out = 2D-IDFT( H .* 2D-DFT(in) ) (Sec. 6).
+ * The net scale of the round trip is 1/(N M) (eq5's 1/N times the
+ * 2D-IDFT's 1/M), so H = 1 reproduces the input.  in is complex, or float32
+ * real when the plan has FFT_IN_REAL_F32.  out may equal in only for
+ * complex input. */
+fft_status fft2d_filter_pipeline(fft_plan plan, const void* in, void* out, fft_filter filter,
+                                 double param);
+
+/* End-to-end call on HOST buffers (pageable or pinned): copies the input
+ * host->device, transforms, copies the result device->host, pipelined over
+ * batch chunks on the plan's streams; returns after the result is in
+ * host_out.  direction: +1 forward, -1 inverse, 0 filter pipeline with
+ * (filter, param). */
+fft_status fft_execute_host(fft_plan plan, int direction, const void* host_in, void* host_out,
+                            fft_filter filter, double param);
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) ----------------
+ * Distributed plans shard the leading dimension across `nranks` processes:
+ *  rank 1: the batch (independent transforms, no collective), or for
+ *          batch == 1 the four-step view of one large transform (n/nranks
+ *          contiguous elements per rank, all-to-all transposes);
+ *  rank 2: row slabs of N/nranks rows per rank (all-to-all transposes).
+ * Every rank calls every distributed entry point with identical plan
+ * parameters (collective semantics, NCCL-style). */
+fft_status fft_nccl_unique_id(unsigned char id[128]); /* on one rank; broadcast it */
+fft_status fft_plan_set_comm(fft_plan plan, const unsigned char id[128], int nranks, int my_rank);
+
+fft_status fft_plan_destroy(fft_plan plan);
+
+const char* fft_status_string(fft_status s);
+const char* fft_last_error(void); /* thread-local detail of the last failure */
+
+/* Introspection for tests/benchmarks: number of kernel launches the plan's
+ * last call issued, and the library build string. */
+int fft_plan_last_launch_count(fft_plan plan);
+const char* fft_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200FFT_H */

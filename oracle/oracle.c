@@ -438,10 +438,10 @@ static double pairwise(double* a, int64_t n) {
     int64_t h = n / 2;
     return pairwise(a, h) + pairwise(a + h, n - h);
 }
-int oracle_dft_bins(const double* in, int64_t N, const int64_t* bins, int64_t nbins, int inverse,
-                    double* out) {
+static int dft_bins_impl(const double* in, const float* in32, int64_t N, const int64_t* bins,
+                         int64_t nbins, int inverse, double* out) {
     if (!is_pow2(N)) return ORACLE_E_SIZE;
-    if (!in || !bins || !out) return ORACLE_E_ARG;
+    if ((!in && !in32) || !bins || !out) return ORACLE_E_ARG;
     const int m = ilog2(N);
     const int h = (m + 1) / 2;
     const int64_t nb = (int64_t)1 << h, na = (int64_t)1 << (m - h);
@@ -478,8 +478,11 @@ int oracle_dft_bins(const double* in, int64_t N, const int64_t* bins, int64_t nb
                 const double* b = B + 2 * (t & (uint64_t)(nb - 1));
                 double wr = a[0] * b[0] - a[1] * b[1];
                 double wi = a[0] * b[1] + a[1] * b[0];
-                kahan_add(&sr, &cr, in[2 * j] * wr - in[2 * j + 1] * wi);
-                kahan_add(&si, &ci, in[2 * j] * wi + in[2 * j + 1] * wr);
+                /* complex64 inputs are promoted exactly to fp64 (O1) */
+                const double xr = in ? in[2 * j] : (double)in32[2 * j];
+                const double xi = in ? in[2 * j + 1] : (double)in32[2 * j + 1];
+                kahan_add(&sr, &cr, xr * wr - xi * wi);
+                kahan_add(&si, &ci, xr * wi + xi * wr);
             }
             pr[blk] = sr;
             pi[blk] = si;
@@ -490,4 +493,17 @@ int oracle_dft_bins(const double* in, int64_t N, const int64_t* bins, int64_t nb
     }
     free(A); free(B); free(pr); free(pi);
     return ORACLE_OK;
+}
+
+int oracle_dft_bins(const double* in, int64_t N, const int64_t* bins, int64_t nbins, int inverse,
+                    double* out) {
+    if (!in) return ORACLE_E_ARG;
+    return dft_bins_impl(in, NULL, N, bins, nbins, inverse, out);
+}
+
+/* Same sums on a complex64 input (each value promoted exactly to fp64). */
+int oracle_dft_bins_c64(const float* in, int64_t N, const int64_t* bins, int64_t nbins, int inverse,
+                        double* out) {
+    if (!in) return ORACLE_E_ARG;
+    return dft_bins_impl(NULL, in, N, bins, nbins, inverse, out);
 }

@@ -1,0 +1,159 @@
+// fft_common.cuh -- complex arithmetic and in-register DFT butterflies for the
+// sm_100a kernels of libb200fft.
+//
+// The transforms computed are the paper's DFT (Eq. E2) and
+// its unscaled inverse (Eq. E3 / Sec. 3).  Here only the
+// building blocks live: a radix-rho DFT on values held in registers,
+//     V[q] = sum_{r<rho} v[r] * w^(r q),  w = exp(-+2 pi i / rho),
+// with compile-time constant twiddles.  The minus sign is the forward
+// transform (INV = false), the plus sign the inverse (INV = true).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace b200fft {
+
+template <typename T> struct cpx_t;
+template <> struct cpx_t<float> { using type = float2; };
+template <> struct cpx_t<double> { using type = double2; };
+template <typename T> using cpx = typename cpx_t<T>::type;
+
+__device__ __forceinline__ float2 mk(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ double2 mk(double x, double y) { return make_double2(x, y); }
+
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return mk(a.x + b.x, a.y + b.y); }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { return mk(a.x - b.x, a.y - b.y); }
+// a * b
+template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
+    return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename C> __device__ __forceinline__ C cmulc(C a, C b) {
+    return mk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <bool CONJ, typename C> __device__ __forceinline__ C cmul_dir(C a, C b) {
+    if constexpr (CONJ) return cmulc(a, b);
+    else return cmul(a, b);
+}
+template <typename C, typename S> __device__ __forceinline__ C cscale(C a, S s) {
+    return mk(a.x * s, a.y * s);
+}
+// -i * a (forward quarter turn) / +i * a (inverse)
+template <bool INV, typename C> __device__ __forceinline__ C rot_quarter(C a) {
+    if constexpr (INV) return mk(-a.y, a.x);
+    else return mk(a.y, -a.x);
+}
+
+// cos / sin of 2 pi e / 16 (exact decimal expansions, 20 digits)
+__host__ __device__ constexpr double cos16(int e) {
+    switch (e & 15) {
+        case 0: return 1.0;
+        case 1: return 0.92387953251128675613;
+        case 2: return 0.70710678118654752440;
+        case 3: return 0.38268343236508977173;
+        case 4: return 0.0;
+        case 5: return -0.38268343236508977173;
+        case 6: return -0.70710678118654752440;
+        case 7: return -0.92387953251128675613;
+        case 8: return -1.0;
+        case 9: return -0.92387953251128675613;
+        case 10: return -0.70710678118654752440;
+        case 11: return -0.38268343236508977173;
+        case 12: return 0.0;
+        case 13: return 0.38268343236508977173;
+        case 14: return 0.70710678118654752440;
+        default: return 0.92387953251128675613;
+    }
+}
+__host__ __device__ constexpr double sin16(int e) { return cos16(e - 4); }  // sin x = cos(x - pi/2)
+
+// a * W_N^e with W_N = exp(-2 pi i / N) (forward) or exp(+2 pi i / N) (INV),
+// N in {1, 2, 4, 8, 16}; e is a compile-time constant after unrolling.
+template <int N, bool INV, typename C>
+__device__ __forceinline__ C mulw(C a, int e) {
+    const int e16 = (e * (16 / N)) & 15;
+    using T = decltype(a.x);
+    if (e16 == 0) return a;
+    if (e16 == 8) return mk(-a.x, -a.y);
+    if (e16 == 4) return rot_quarter<INV>(a);
+    if (e16 == 12) return rot_quarter<!INV>(a);
+    const T c = (T)cos16(e16);
+    const T s = INV ? (T)sin16(e16) : (T)(-sin16(e16));
+    return mk(a.x * c - a.y * s, a.x * s + a.y * c);
+}
+
+// In-place DFT of N values v[0..N-1] (natural order in and out), N in
+// {1,2,4,8,16}.  Two-factor decomposition N = A * B:
+//   Y[n1][k2] = sum_{n2<B} v[n1 + A n2] W_B^{n2 k2}
+//   Y[n1][k2] *= W_N^{n1 k2}
+//   V[k2 + B k1] = sum_{n1<A} Y[n1][k2] W_A^{n1 k1}
+template <int N, bool INV, typename C>
+__device__ __forceinline__ void dft(C* v) {
+    if constexpr (N == 1) {
+        return;
+    } else if constexpr (N == 2) {
+        C a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    } else if constexpr (N == 4) {
+        C s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+        C s13 = cadd(v[1], v[3]), d13 = rot_quarter<INV>(csub(v[1], v[3]));
+        v[0] = cadd(s02, s13);
+        v[2] = csub(s02, s13);
+        v[1] = cadd(d02, d13);
+        v[3] = csub(d02, d13);
+    } else {
+        constexpr int A = (N == 8) ? 2 : 4;
+        constexpr int B = N / A;
+        C y[A][B];
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) {
+#pragma unroll
+            for (int n2 = 0; n2 < B; ++n2) y[n1][n2] = v[n1 + A * n2];
+            dft<B, INV>(y[n1]);
+#pragma unroll
+            for (int k2 = 0; k2 < B; ++k2) y[n1][k2] = mulw<N, INV>(y[n1][k2], n1 * k2);
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < B; ++k2) {
+            C t[A];
+#pragma unroll
+            for (int n1 = 0; n1 < A; ++n1) t[n1] = y[n1][k2];
+            dft<A, INV>(t);
+#pragma unroll
+            for (int k1 = 0; k1 < A; ++k1) v[k2 + B * k1] = t[k1];
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// Radix schedule of an R-point DFT done inside one CTA (R = 2^m <= 8192):
+// sub-passes of radix 16, then one remainder radix (2, 4 or 8) last.
+// --------------------------------------------------------------------------
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
+__host__ __device__ constexpr int n_steps(int R) {
+    return R <= 16 ? 1 : (ilog2c(R) / 4 + ((ilog2c(R) % 4) ? 1 : 0));
+}
+__host__ __device__ constexpr int radix_at(int R, int s) {
+    return R <= 16 ? R : ((s < ilog2c(R) / 4) ? 16 : (1 << (ilog2c(R) % 4)));
+}
+__host__ __device__ constexpr int span_at(int R, int s) {  // product of radices before step s
+    return s == 0 ? 1 : span_at(R, s - 1) * radix_at(R, s - 1);
+}
+
+// offset of step s's twiddles in the step-major table of an R-point DFT:
+// step s (s >= 1) owns (rho_s - 1) * Ns_s entries laid out [r - 1][k],
+// value W_{Ns rho}^{k r}; consecutive k (consecutive threads) are adjacent.
+__host__ __device__ constexpr int tw_off(int R, int s) {
+    return s <= 1 ? 0 : tw_off(R, s - 1) + (radix_at(R, s - 1) - 1) * span_at(R, s - 1);
+}
+__host__ __device__ constexpr int tw_size(int R) { return tw_off(R, n_steps(R)); }
+// all R = 2, 4, ..., 8192 tables concatenated: base offset of R's table
+__host__ __device__ constexpr int tw_base(int R) { return R <= 2 ? 0 : tw_base(R / 2) + tw_size(R / 2); }
+
+// padded shared-memory index: one spare slot every 16 elements (breaks the
+// stride-16 bank pattern of the first Stockham write)
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int pad16c(int i) { return i + (i >> 4); }
+
+}  // namespace b200fft

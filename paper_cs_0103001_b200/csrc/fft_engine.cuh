@@ -1,0 +1,312 @@
+// fft_engine.cuh -- the CTA-level Stockham engine and the three kernel
+// families of libb200fft (sm_100a).
+//
+// What is computed: the DFT of Eq. E2 (Sec. 2) and the
+// unscaled inverse of Eq. E3 / Sec. 3, by a radix-16
+// Stockham autosort (natural order out, no bit-reversal pass) instead of the
+// paper's in-place radix-2 tree: the same sums, reassociated.
+//
+// One "line" = one R-point DFT held by TPL = R/E threads, E values per thread
+// in registers.  A step of radix rho with span Ns (product of the radices
+// before it) is, for every butterfly j < R/rho with k = j mod Ns:
+//     v[r]  = a[j + r R/rho] * W_{Ns rho}^{k r}          (r < rho)
+//     b[(j - k) rho + k + q Ns] = sum_r v[r] W_rho^{r q}  (q < rho)
+// Steps exchange through shared memory (one padded buffer per line).  At the
+// boundary of the engine every thread holds the elements lt + TPL*m, m < E,
+// of its line (lt = lane within the line), which is what makes global loads
+// and stores coalesced and lets a forward and an inverse transform chain in
+// registers (the fused filter pipeline).
+#pragma once
+#include "fft_common.cuh"
+
+namespace b200fft {
+
+constexpr int RMAX = 8192;  // largest in-CTA DFT
+// Twiddles of the in-CTA steps come from the step-major tables of
+// fft_common.cuh (tw_base / tw_off), fp64-generated on the host and rounded
+// once; kernels receive the pointer to their R's table.
+
+template <typename T, int R, int E, bool INV>
+struct LineFFT {
+    using C = cpx<T>;
+    static constexpr int TPL = R / E;
+    static constexpr int S = n_steps(R);
+    static constexpr int LS = pad16c(R) + 1;  // odd line stride in smem (slots)
+    static constexpr int RHO0 = radix_at(R, 0);
+    static constexpr int RHOL = radix_at(R, S - 1);
+    static_assert(E % RHO0 == 0 && E % RHOL == 0, "E must be a multiple of every radix");
+
+    // register slot of boundary element m (element index lt + TPL m)
+    __device__ static constexpr int pos_in(int m) {
+        return (m % (E / RHO0)) * RHO0 + m / (E / RHO0);
+    }
+    __device__ static constexpr int pos_out(int m) {
+        return (m % (E / RHOL)) * RHOL + m / (E / RHOL);
+    }
+
+    template <int s>
+    __device__ __forceinline__ static void compute(C* v, int lt, const C* __restrict__ tw) {
+        constexpr int rho = radix_at(R, s), Ns = span_at(R, s), nb = E / rho;
+#pragma unroll
+        for (int b = 0; b < nb; ++b) {
+            if constexpr (Ns > 1) {
+                const int j = lt + b * TPL;
+                const int k = j & (Ns - 1);
+                const C* __restrict__ ts = tw + tw_off(R, s) + k;
+#pragma unroll
+                for (int r = 1; r < rho; ++r) {
+                    const C w = __ldg(ts + (r - 1) * Ns);
+                    v[b * rho + r] = cmul_dir<INV>(v[b * rho + r], w);
+                }
+            }
+            dft<rho, INV>(v + b * rho);
+        }
+    }
+
+    template <int s>
+    __device__ __forceinline__ static void write_out(C* line, const C* v, int lt) {
+        constexpr int rho = radix_at(R, s), Ns = span_at(R, s), nb = E / rho;
+#pragma unroll
+        for (int b = 0; b < nb; ++b) {
+            const int j = lt + b * TPL;
+            const int k = j & (Ns - 1);
+            const int base = (j - k) * rho + k;
+#pragma unroll
+            for (int q = 0; q < rho; ++q) line[pad16(base + q * Ns)] = v[b * rho + q];
+        }
+    }
+
+    template <int s>
+    __device__ __forceinline__ static void read_in(const C* line, C* v, int lt) {
+        constexpr int rho = radix_at(R, s), nb = E / rho;
+#pragma unroll
+        for (int b = 0; b < nb; ++b) {
+            const int j = lt + b * TPL;
+#pragma unroll
+            for (int r = 0; r < rho; ++r) v[b * rho + r] = line[pad16(j + r * (R / rho))];
+        }
+    }
+
+    template <int s>
+    __device__ __forceinline__ static void run_from(C* v, C* line, int lt, const C* __restrict__ tw) {
+        if constexpr (s < S) {
+            __syncthreads();
+            write_out<s - 1>(line, v, lt);
+            __syncthreads();
+            read_in<s>(line, v, lt);
+            compute<s>(v, lt, tw);
+            run_from<s + 1>(v, line, lt, tw);
+        }
+    }
+
+    // v holds the step-0 inputs (pos_in layout) -> v holds the outputs (pos_out layout)
+    __device__ __forceinline__ static void run(C* v, C* line, int lt, const C* __restrict__ tw) {
+        compute<0>(v, lt, tw);
+        run_from<1>(v, line, lt, tw);
+    }
+};
+
+// --------------------------------------------------------------------------
+// Kernel family A: contiguous rows, one whole transform per line.
+//   out[row][i] = scale * sum_j in[row][j] W_R^{+-ij},  rows < batch.
+// W lines (rows) per CTA.  REAL_IN: input rows are float32 real values
+// (promotion to complex fused into the load, BASELINE configs[2]).
+// --------------------------------------------------------------------------
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN>
+__global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_, cpx<T>* __restrict__ out,
+                                                    int64_t batch, T scale, const cpx<T>* __restrict__ tw) {
+    using C = cpx<T>;
+    using F = LineFFT<T, R, E, INV>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* smem = reinterpret_cast<C*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int t = tid / F::TPL, lt = tid % F::TPL;
+    const int64_t row = (int64_t)blockIdx.x * W + t;
+    const bool valid = row < batch;
+    C v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int64_t idx = row * R + lt + F::TPL * m;
+        if constexpr (REAL_IN) {
+            const float* in = reinterpret_cast<const float*>(in_);
+            v[F::pos_in(m)] = valid ? mk((T)__ldg(in + idx), (T)0) : mk((T)0, (T)0);
+        } else {
+            const C* in = reinterpret_cast<const C*>(in_);
+            v[F::pos_in(m)] = valid ? in[idx] : mk((T)0, (T)0);
+        }
+    }
+    F::run(v, smem + t * F::LS, lt, tw);
+    if (valid) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) out[row * R + lt + F::TPL * m] = cscale(v[F::pos_out(m)], scale);
+    }
+}
+
+// --------------------------------------------------------------------------
+// Filters of the 2D pipeline (Sec. 6), evaluated per (u, v):
+//   GAUSS: g_u[u] * g_v[v] (separable fp64-generated 1D tables, b200fft.h)
+//   IDEAL_LITERAL: 0 if (u-N/2)^2 + (v-M/2)^2 <= b^2 else 1   (Eq. filtro)
+//   IDEAL_LOWPASS: 1 if k_u^2 + k_v^2 <= b^2 else 0 (signed k)
+// --------------------------------------------------------------------------
+struct FilterArgs {
+    int kind;           // fft_filter
+    double b2;          // radius^2 for the ideal filters
+    const void* gu;     // T[N] (GAUSS)
+    const void* gv;     // T[M] (GAUSS)
+    int64_t N, M;
+};
+
+template <typename T>
+__device__ __forceinline__ T filter_value(const FilterArgs& f, int64_t u, int64_t v) {
+    if (f.kind == 1) {
+        return __ldg(reinterpret_cast<const T*>(f.gu) + u) * __ldg(reinterpret_cast<const T*>(f.gv) + v);
+    } else if (f.kind == 2) {
+        const double du = (double)(u - f.N / 2), dv = (double)(v - f.M / 2);
+        return (du * du + dv * dv <= f.b2) ? (T)0 : (T)1;
+    } else if (f.kind == 3) {
+        const double ku = (double)(u < f.N / 2 ? u : u - f.N), kv = (double)(v < f.M / 2 ? v : v - f.M);
+        return (ku * ku + kv * kv <= f.b2) ? (T)1 : (T)0;
+    }
+    return (T)1;
+}
+
+// --------------------------------------------------------------------------
+// Kernel family B: columns of [img][R][S] (R rows of S complex), W adjacent
+// columns per CTA (coalesced W-element row segments, staged through smem).
+//   MODE 0: forward column DFT, times scale
+//   MODE 1: inverse column DFT, times scale
+//   MODE 2: forward -> * H(u, v) * scale -> inverse (the fused middle of the
+//           2D filter pipeline; scale = 1/(N M))
+// --------------------------------------------------------------------------
+// smem line stride of the column tiles: a multiple of the 128-B bank row plus
+// 128 B / (W * elem) so that the W-wide staging rows hit distinct banks
+template <typename T, int R, int W>
+__host__ __device__ constexpr int cols_ls() {
+    constexpr int SL = 128 / (int)sizeof(cpx<T>);
+    return ((pad16c(R) + SL - 1) / SL) * SL + (W >= SL ? 1 : SL / W);
+}
+
+template <typename T, int R, int E, int W, int MODE>
+__global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out,
+                                                    int64_t S, T scale, const cpx<T>* __restrict__ tw,
+                                                    FilterArgs filt) {
+    using C = cpx<T>;
+    constexpr bool INV0 = (MODE == 1);
+    using F = LineFFT<T, R, E, INV0>;
+    using FI = LineFFT<T, R, E, true>;
+    constexpr int NT = W * F::TPL;
+    constexpr int LSC = cols_ls<T, R, W>();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* smem = reinterpret_cast<C*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int t = tid / F::TPL, lt = tid % F::TPL;
+    const int64_t s0 = (int64_t)blockIdx.x * W;
+    const int64_t img = blockIdx.y;
+    const C* src = in + img * (int64_t)R * S + s0;
+    C* dst = out + img * (int64_t)R * S + s0;
+    const int wv = (int)((S - s0) < W ? (S - s0) : W);  // ragged last tile
+
+    for (int idx = tid; idx < W * R; idx += NT) {
+        const int tt = idx % W, r = idx / W;
+        smem[tt * LSC + pad16(r)] = (tt < wv) ? src[(int64_t)r * S + tt] : mk((T)0, (T)0);
+    }
+    __syncthreads();
+    C* line = smem + t * LSC;
+    C v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[pad16(lt + F::TPL * m)];
+    F::run(v, line, lt, tw);
+    if constexpr (MODE == 2) {
+        C w[E];
+        const int64_t col = s0 + t;
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int64_t u = lt + F::TPL * m;
+            const T h = (col < S) ? filter_value<T>(filt, u, col) * scale : (T)0;
+            w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], h);
+        }
+        FI::run(w, line, lt, tw);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < E; ++m) line[pad16(lt + F::TPL * m)] = w[FI::pos_out(m)];
+    } else {
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < E; ++m) line[pad16(lt + F::TPL * m)] = cscale(v[F::pos_out(m)], scale);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < W * R; idx += NT) {
+        const int tt = idx % W, r = idx / W;
+        if (tt < wv) dst[(int64_t)r * S + tt] = smem[tt * LSC + pad16(r)];
+    }
+}
+
+// --------------------------------------------------------------------------
+// Kernel family C: one global Stockham pass of radix R over rows of length L
+// (multi-pass transforms, L > RMAX), W adjacent butterflies j per CTA:
+//   v[r] = a[j + r L/R] * W_{Ns R}^{k r},  k = j mod Ns
+//   b[(j - k) R + k + q Ns] = scale * sum_r v[r] W_R^{r q}
+// The pass twiddle W_{Ns R}^{k r} comes from two fp64-generated tables laid
+// out [r][k] so that adjacent lines (adjacent k) read adjacent entries:
+//   pa[r KLO + (k mod KLO)] * pb[r (Ns/KLO) + k / KLO]   (pb only if Ns > KLO)
+// --------------------------------------------------------------------------
+template <typename T, int R, int E, int W, bool INV>
+__global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out,
+                                                    int64_t L, int64_t Ns, int64_t nlines, T scale,
+                                                    const cpx<T>* __restrict__ tw,
+                                                    const cpx<T>* __restrict__ pa,
+                                                    const cpx<T>* __restrict__ pb, int klo_sh) {
+    using C = cpx<T>;
+    using F = LineFFT<T, R, E, INV>;
+    constexpr int NT = W * F::TPL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* smem = reinterpret_cast<C*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int t = tid / F::TPL, lt = tid % F::TPL;
+    const int64_t LR = L / R;                     // butterflies per transform
+    const int64_t gl0 = (int64_t)blockIdx.x * W;  // first line of the tile (W | LR)
+    const int64_t bidx = gl0 / LR;
+    const int64_t j0 = gl0 - bidx * LR;
+    const C* src = in + bidx * L;
+    C* dst = out + bidx * L;
+    const int64_t KLO = (int64_t)1 << klo_sh;
+    const int64_t nhi = Ns >> klo_sh;
+
+    for (int idx = tid; idx < W * R; idx += NT) {
+        const int tt = idx % W, r = idx / W;
+        const int64_t j = j0 + tt;
+        C a = src[j + (int64_t)r * LR];
+        if (Ns > 1) {
+            const int64_t k = j & (Ns - 1);
+            C w = __ldg(pa + (int64_t)r * KLO + (k & (KLO - 1)));
+            if (nhi > 1) w = cmul(w, __ldg(pb + (int64_t)r * nhi + (k >> klo_sh)));
+            a = cmul_dir<INV>(a, w);
+        }
+        smem[tt * F::LS + pad16(r)] = a;
+    }
+    __syncthreads();
+    C* line = smem + t * F::LS;
+    C v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[pad16(lt + F::TPL * m)];
+    F::run(v, line, lt, tw);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) line[pad16(lt + F::TPL * m)] = cscale(v[F::pos_out(m)], scale);
+    __syncthreads();
+    if (Ns >= W) {
+        for (int idx = tid; idx < W * R; idx += NT) {
+            const int tt = idx % W, q = idx / W;
+            const int64_t j = j0 + tt, k = j & (Ns - 1);
+            dst[(j - k) * R + k + (int64_t)q * Ns] = smem[tt * F::LS + pad16(q)];
+        }
+    } else {
+        for (int idx = tid; idx < W * R; idx += NT) {
+            const int q = idx % R, tt = idx / R;
+            const int64_t j = j0 + tt, k = j & (Ns - 1);
+            dst[(j - k) * R + k + (int64_t)q * Ns] = smem[tt * F::LS + pad16(q)];
+        }
+    }
+}
+
+}  // namespace b200fft

@@ -1,0 +1,74 @@
+// kernels_cols.cu -- instantiations and launcher of kernel family B (columns,
+// and the fused column forward -> filter -> column inverse of the pipeline).
+#include "fft_engine.cuh"
+#include "launch.h"
+
+namespace b200fft {
+
+namespace {
+
+template <typename T> constexpr int cols_budget() { return sizeof(T) == 4 ? 16384 : 8192; }
+
+template <typename T, int R, int MODE>
+cudaError_t cols_t(const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
+                   const FilterArgs& f, cudaStream_t st) {
+    constexpr int E = R < 32 ? (R < 16 ? R : 16) : 32;
+    constexpr int TPL = R / E;
+    constexpr int W0 = cols_budget<T>() / R;
+    constexpr int W = W0 > 16 ? 16 : (W0 < 2 ? 2 : W0);
+    using F = LineFFT<T, R, E, MODE == 1>;
+    constexpr size_t smem = sizeof(cpx<T>) * W * cols_ls<T, R, W>();
+    static_assert(smem <= 227 * 1024, "column tile exceeds shared memory");
+    auto kern = k_cols<T, R, E, W, MODE>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    if (S <= 0 || nimg <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((S + W - 1) / W), (unsigned)nimg);
+    kern<<<grid, W * TPL, smem, st>>>(reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<cpx<T>*>(out), S,
+                                      (T)scale, reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), f);
+    return cudaGetLastError();
+}
+
+template <typename T, int MODE>
+cudaError_t cols_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg, double scale,
+                   const void* tw, const FilterArgs& f, cudaStream_t st) {
+    switch (R) {
+#define B200_COLS_CASE(r) \
+    case r: return cols_t<T, r, MODE>(in, out, S, nimg, scale, tw, f, st);
+        B200_COLS_CASE(1) B200_COLS_CASE(2) B200_COLS_CASE(4) B200_COLS_CASE(8) B200_COLS_CASE(16)
+        B200_COLS_CASE(32) B200_COLS_CASE(64) B200_COLS_CASE(128) B200_COLS_CASE(256)
+        B200_COLS_CASE(512) B200_COLS_CASE(1024) B200_COLS_CASE(2048) B200_COLS_CASE(4096)
+#undef B200_COLS_CASE
+        case 8192:
+            if constexpr (sizeof(T) == 4) return cols_t<T, 8192, MODE>(in, out, S, nimg, scale, tw, f, st);
+            return cudaErrorInvalidValue;
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_cols(int prec, int mode, int64_t R, const void* in, void* out, int64_t S,
+                        int64_t nimg, double scale, const void* tw, const FilterArgs& f,
+                        cudaStream_t st) {
+    if (prec == 0) {
+        switch (mode) {
+            case 0: return cols_r<float, 0>(R, in, out, S, nimg, scale, tw, f, st);
+            case 1: return cols_r<float, 1>(R, in, out, S, nimg, scale, tw, f, st);
+            case 2: return cols_r<float, 2>(R, in, out, S, nimg, scale, tw, f, st);
+        }
+    } else {
+        switch (mode) {
+            case 0: return cols_r<double, 0>(R, in, out, S, nimg, scale, tw, f, st);
+            case 1: return cols_r<double, 1>(R, in, out, S, nimg, scale, tw, f, st);
+            case 2: return cols_r<double, 2>(R, in, out, S, nimg, scale, tw, f, st);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace b200fft

@@ -1,0 +1,31 @@
+// launch.h -- internal launchers of libb200fft (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace b200fft {
+
+struct FilterArgs;
+
+// Largest transform length handled by one CTA, per precision (0 = c64, 1 = c128).
+constexpr int64_t kRowsMax = 8192;
+constexpr int64_t kColsMax[2] = {8192, 4096};
+
+// Kernel family A: batch contiguous rows of length R (power of two <= 8192).
+cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void* in, void* out,
+                        int64_t batch, double scale, const void* tw, cudaStream_t st);
+
+// Kernel family B: column transforms of nimg grids [R][S]; mode 0 fwd, 1 inv,
+// 2 fwd -> filter*scale -> inv.
+cudaError_t launch_cols(int prec, int mode, int64_t R, const void* in, void* out, int64_t S,
+                        int64_t nimg, double scale, const void* tw, const FilterArgs& f,
+                        cudaStream_t st);
+
+// Kernel family C: one global Stockham pass of radix R (128..1024) over
+// `batch` rows of length L with span Ns; pa/pb: the pass twiddle tables
+// (pa[r][k mod 2^klo_sh], pb[r][k >> klo_sh]).
+cudaError_t launch_pass(int prec, bool inv, int64_t R, const void* in, void* out, int64_t L,
+                        int64_t Ns, int64_t batch, double scale, const void* tw, const void* pa,
+                        const void* pb, int klo_sh, cudaStream_t st);
+
+}  // namespace b200fft

@@ -1,0 +1,597 @@
+// plan.cu -- host side of libb200fft: plans, twiddle/filter tables, the
+// C ABI of include/b200fft.h, and the execution schedules.
+//
+// Schedules:
+//   1D, n <= 8192     : one launch of k_rows (whole transform per CTA line),
+//                       1/N fused into the store (exact: a power of two).
+//   1D, n > 8192      : 2 or 3 global Stockham passes (k_pass, radix
+//                       128..1024), 1/N fused into the last pass.
+//   2D (eq5)          : k_rows over the N rows (unnormalised: the paper's
+//                       "FFT on rows -> multiplication for M"),
+//                       then k_cols over the M columns with 1/N.
+//   2D-IDFT           : k_cols inverse (unscaled), then k_rows inverse * 1/M.
+//   filter pipeline   : k_rows fwd -> k_cols(fwd, * H/(N M), inv) -> k_rows inv
+//                       (three launches; the column forward, the filter and
+//                       the column inverse are one kernel).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/b200fft.h"
+#include "fft_engine.cuh"
+#include "launch.h"
+
+using namespace b200fft;
+
+#define B200FFT_STR2(x) #x
+#define B200FFT_STR(x) B200FFT_STR2(x)
+
+namespace {
+
+thread_local std::string g_last_error;
+
+fft_status fail(fft_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+fft_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(FFT_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+int ilog2(int64_t n) {
+    int m = 0;
+    while (((int64_t)1 << m) < n) ++m;
+    return m;
+}
+
+// ---- twiddle tables -----------------------------------------------------
+// All tables are computed in fp64 from cos/sin of the exactly reduced angle
+// and rounded once to the plan's precision.
+cudaError_t upload(const std::vector<double>& v, int prec, void** dptr) {
+    size_t n = v.size();
+    cudaError_t e;
+    if (prec == 0) {
+        std::vector<float> f(n);
+        for (size_t i = 0; i < n; ++i) f[i] = (float)v[i];
+        e = cudaMalloc(dptr, n * sizeof(float));
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(*dptr, f.data(), n * sizeof(float), cudaMemcpyHostToDevice);
+    }
+    e = cudaMalloc(dptr, n * sizeof(double));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(*dptr, v.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+}
+
+struct DeviceTables {
+    void* tw[2] = {nullptr, nullptr};  // step-major in-CTA twiddles for c64 / c128
+};
+
+// The step-major twiddle tables of every in-CTA DFT size R = 2 .. 8192
+// (fft_common.cuh tw_base / tw_off): entry [r - 1][k] of step s is
+// W_{Ns rho}^{k r} = exp(-2 pi i k r / (Ns rho)).
+void fill_step_tables(std::vector<double>& v) {
+    const int total = tw_base(2 * RMAX);
+    v.assign(2 * (size_t)total, 0.0);
+    for (int R = 2; R <= RMAX; R *= 2) {
+        for (int s = 1; s < n_steps(R); ++s) {
+            const int rho = radix_at(R, s), Ns = span_at(R, s);
+            const int64_t n = (int64_t)Ns * rho;
+            for (int r = 1; r < rho; ++r)
+                for (int k = 0; k < Ns; ++k) {
+                    const int64_t idx = (int64_t)tw_base(R) + tw_off(R, s) + (int64_t)(r - 1) * Ns + k;
+                    const int64_t x = ((int64_t)k * r) % n;
+                    const double ang = -2.0 * M_PI * (double)x / (double)n;
+                    v[2 * idx] = std::cos(ang);
+                    v[2 * idx + 1] = std::sin(ang);
+                }
+        }
+    }
+}
+std::mutex g_tab_mu;
+std::map<int, DeviceTables> g_tables;
+
+cudaError_t device_twiddles(int dev, int prec, const void** out) {
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    DeviceTables& t = g_tables[dev];
+    if (!t.tw[prec]) {
+        std::vector<double> v;
+        fill_step_tables(v);
+        cudaError_t e = upload(v, prec, &t.tw[prec]);
+        if (e != cudaSuccess) {
+            t.tw[prec] = nullptr;
+            return e;
+        }
+    }
+    *out = t.tw[prec];
+    return cudaSuccess;
+}
+
+}  // namespace
+
+struct fft_plan_s {
+    int rank = 1;
+    int64_t n0 = 1, n1 = 1;  // 1D: n0 = length; 2D: n0 = N rows, n1 = M cols
+    int64_t batch = 1;
+    int prec = 0;
+    unsigned flags = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    const void* tw = nullptr;
+    // multi-pass 1D
+    std::vector<int64_t> radices;
+    std::vector<void*> pa, pb;  // per pass twiddle tables [r][k_lo], [r][k_hi]
+    std::vector<int> klo_sh;
+    // filter tables (Gaussian)
+    void* gu = nullptr;
+    void* gv = nullptr;
+    double g_param = -1.0;
+    // workspace
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    bool ws_owned = false;
+    // host-execution staging buffers
+    void* hbuf[2] = {nullptr, nullptr};   // device output staging per stream
+    void* hbin[2] = {nullptr, nullptr};   // device input staging per stream
+    size_t hbuf_bytes = 0;
+    cudaStream_t hstream[2] = {nullptr, nullptr};
+    cudaEvent_t hev = nullptr;
+    int last_launches = 0;
+    // distributed
+    int nranks = 1, my_rank = 0;
+    void* comm = nullptr;
+
+    size_t elem_bytes() const { return prec == 0 ? 8 : 16; }
+    int64_t elems() const { return batch * n0 * (rank == 2 ? n1 : 1); }
+};
+
+namespace {
+
+size_t workspace_need(const fft_plan_s* p) {
+    if (p->rank == 1 && !p->radices.empty()) {
+        size_t one = (size_t)p->elems() * p->elem_bytes();
+        return p->radices.size() >= 3 ? 2 * one : one;
+    }
+    return 0;
+}
+
+fft_status ensure_workspace(fft_plan_s* p) {
+    size_t need = workspace_need(p);
+    if (need == 0 || (p->ws && p->ws_bytes >= need)) return FFT_OK;
+    if (p->ws && !p->ws_owned) return fail(FFT_E_STATE, "caller workspace smaller than fft_plan_workspace_bytes()");
+    if (p->ws_owned && p->ws) cudaFree(p->ws);
+    p->ws = nullptr;
+    cudaError_t e = cudaMalloc(&p->ws, need);
+    if (e != cudaSuccess) {
+        p->ws = nullptr;
+        return fail(FFT_E_ALLOC, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    p->ws_bytes = need;
+    p->ws_owned = true;
+    return FFT_OK;
+}
+
+bool aligned(const void* ptr, size_t a) { return ((uintptr_t)ptr % a) == 0; }
+
+// radix split of a multi-pass length L = 2^m (m >= 14): 2 or 3 passes of
+// radix 2^7 .. 2^10, as even as possible (largest first).
+std::vector<int64_t> split_radices(int64_t L) {
+    int m = ilog2(L);
+    int P = (m + 9) / 10;
+    std::vector<int64_t> r;
+    for (int i = 0; i < P; ++i) {
+        int mi = m / P + (i < m % P ? 1 : 0);
+        r.push_back((int64_t)1 << mi);
+    }
+    return r;
+}
+
+fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
+    const int64_t L = p->n0;
+    const double scale = inv ? 1.0 : 1.0 / (double)L;
+    cudaError_t e;
+    if (p->radices.empty()) {
+        e = launch_rows(p->prec, inv, false, L, in, out, p->batch, scale, p->tw, st);
+        p->last_launches = 1;
+        if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
+        return FFT_OK;
+    }
+    fft_status s = ensure_workspace(p);
+    if (s != FFT_OK) return s;
+    const int P = (int)p->radices.size();
+    const size_t one = (size_t)p->elems() * p->elem_bytes();
+    char* ws0 = (char*)p->ws;
+    char* ws1 = ws0 + one;
+    std::vector<const void*> src(P);
+    std::vector<void*> dst(P);
+    dst[P - 1] = out;
+    if (P == 2) {
+        dst[0] = ws0;
+    } else {  // P == 3
+        dst[1] = ws0;
+        dst[0] = (in == out) ? (void*)ws1 : out;
+    }
+    src[0] = in;
+    for (int i = 1; i < P; ++i) src[i] = dst[i - 1];
+    int64_t Ns = 1;
+    p->last_launches = 0;
+    for (int i = 0; i < P; ++i) {
+        const int64_t R = p->radices[i];
+        e = launch_pass(p->prec, inv, R, src[i], dst[i], L, Ns, p->batch, (i == P - 1) ? scale : 1.0, p->tw,
+                        p->pa[i], p->pb[i], p->klo_sh[i], st);
+        p->last_launches++;
+        if (e != cudaSuccess) return cuda_fail(e, "k_pass launch");
+        Ns *= R;
+    }
+    return FFT_OK;
+}
+
+fft_status run_2d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
+    const int64_t N = p->n0, M = p->n1;
+    FilterArgs f{};
+    cudaError_t e;
+    if (!inv) {
+        // rows: unnormalised (FFT_M * M)
+        e = launch_rows(p->prec, false, false, M, in, out, p->batch * N, 1.0, p->tw, st);
+        if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
+        // columns: eq5's 1/N
+        e = launch_cols(p->prec, 0, N, out, out, M, p->batch, 1.0 / (double)N, p->tw, f, st);
+        if (e != cudaSuccess) return cuda_fail(e, "k_cols launch");
+    } else {
+        e = launch_cols(p->prec, 1, N, in, out, M, p->batch, 1.0, p->tw, f, st);
+        if (e != cudaSuccess) return cuda_fail(e, "k_cols launch");
+        e = launch_rows(p->prec, true, false, M, out, out, p->batch * N, 1.0 / (double)M, p->tw, st);
+        if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
+    }
+    p->last_launches = 2;
+    return FFT_OK;
+}
+
+fft_status gauss_tables(fft_plan_s* p, double param) {
+    if (p->gu && p->g_param == param) return FFT_OK;
+    if (p->gu) cudaFree(p->gu);
+    if (p->gv) cudaFree(p->gv);
+    p->gu = p->gv = nullptr;
+    auto make = [&](int64_t n, void** d) -> cudaError_t {
+        std::vector<double> g(n);
+        const double s = param * (double)n / 2.0;
+        for (int64_t u = 0; u < n; ++u) {
+            const double k = (double)(u < n / 2 ? u : u - n);
+            g[u] = (n == 1) ? 1.0 : std::exp(-k * k / (2.0 * s * s));
+        }
+        if (p->prec == 0) {
+            std::vector<float> f(g.begin(), g.end());
+            cudaError_t e = cudaMalloc(d, n * sizeof(float));
+            if (e != cudaSuccess) return e;
+            return cudaMemcpy(*d, f.data(), n * sizeof(float), cudaMemcpyHostToDevice);
+        }
+        cudaError_t e = cudaMalloc(d, n * sizeof(double));
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(*d, g.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+    };
+    cudaError_t e = make(p->n0, &p->gu);
+    if (e == cudaSuccess) e = make(p->n1, &p->gv);
+    if (e != cudaSuccess) return cuda_fail(e, "filter table upload");
+    p->g_param = param;
+    return FFT_OK;
+}
+
+fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter filter, double param,
+                        cudaStream_t st) {
+    const int64_t N = p->n0, M = p->n1;
+    FilterArgs f{};
+    f.kind = (int)filter;
+    f.N = N;
+    f.M = M;
+    if (filter == FFT_FILTER_GAUSS) {
+        fft_status s = gauss_tables(p, param);
+        if (s != FFT_OK) return s;
+        f.gu = p->gu;
+        f.gv = p->gv;
+    } else if (filter == FFT_FILTER_IDEAL_LITERAL || filter == FFT_FILTER_IDEAL_LOWPASS) {
+        f.b2 = param * param;
+    }
+    const bool real_in = (p->flags & FFT_IN_REAL_F32) != 0;
+    cudaError_t e = launch_rows(p->prec, false, real_in, M, in, out, p->batch * N, 1.0, p->tw, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
+    e = launch_cols(p->prec, 2, N, out, out, M, p->batch, 1.0 / ((double)N * (double)M), p->tw, f, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_cols launch");
+    e = launch_rows(p->prec, true, false, M, out, out, p->batch * N, 1.0, p->tw, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
+    p->last_launches = 3;
+    return FFT_OK;
+}
+
+fft_status check_ptrs(fft_plan_s* p, const void* in, void* out, bool real_in) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (!in || !out) return fail(FFT_E_INVALID_ARG, "null data pointer");
+    if (!aligned(in, real_in ? 4 : p->elem_bytes()) || !aligned(out, p->elem_bytes()))
+        return fail(FFT_E_INVALID_ARG, "data pointer not aligned to the element size");
+    return FFT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fft_status_string(fft_status s) {
+    switch (s) {
+        case FFT_OK: return "FFT_OK";
+        case FFT_E_INVALID_SIZE: return "FFT_E_INVALID_SIZE";
+        case FFT_E_INVALID_ARG: return "FFT_E_INVALID_ARG";
+        case FFT_E_UNSUPPORTED: return "FFT_E_UNSUPPORTED";
+        case FFT_E_CUDA: return "FFT_E_CUDA";
+        case FFT_E_NCCL: return "FFT_E_NCCL";
+        case FFT_E_ALLOC: return "FFT_E_ALLOC";
+        case FFT_E_STATE: return "FFT_E_STATE";
+    }
+    return "FFT_E_UNKNOWN";
+}
+
+const char* fft_last_error(void) { return g_last_error.c_str(); }
+
+const char* fft_build_info(void) {
+    return "libb200fft sm_100a (nvcc " B200FFT_STR(__CUDACC_VER_MAJOR__) "." B200FFT_STR(__CUDACC_VER_MINOR__) ")";
+}
+
+fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int64_t batch,
+                              fft_precision prec, unsigned flags) {
+    if (!out) return fail(FFT_E_INVALID_ARG, "null plan output pointer");
+    *out = nullptr;
+    if (!dims) return fail(FFT_E_INVALID_ARG, "null dims");
+    if (rank != 1 && rank != 2) return fail(FFT_E_INVALID_ARG, "rank must be 1 or 2");
+    if (prec != FFT_C64 && prec != FFT_C128) return fail(FFT_E_INVALID_ARG, "bad precision");
+    if (batch < 0) return fail(FFT_E_INVALID_SIZE, "negative batch");
+    if (flags & ~(unsigned)(FFT_IN_REAL_F32 | FFT_OUT_TRANSPOSED)) return fail(FFT_E_INVALID_ARG, "unknown flag");
+    const int ip = (int)prec;
+    for (int d = 0; d < rank; ++d)
+        if (!is_pow2(dims[d])) return fail(FFT_E_INVALID_SIZE, "transform sizes must be powers of two >= 1");
+    if (rank == 1) {
+        const int64_t lim = ip == 0 ? ((int64_t)1 << 30) : ((int64_t)1 << 28);
+        if (dims[0] > lim) return fail(FFT_E_INVALID_SIZE, "1D length over the limit");
+        if (flags & FFT_IN_REAL_F32) return fail(FFT_E_INVALID_ARG, "FFT_IN_REAL_F32 applies to rank-2 plans");
+    } else {
+        if (dims[0] > kColsMax[ip] || dims[1] > kRowsMax)
+            return fail(FFT_E_INVALID_SIZE, "2D side over the limit");
+        if ((flags & FFT_IN_REAL_F32) && ip != 0) return fail(FFT_E_INVALID_ARG, "FFT_IN_REAL_F32 needs complex64");
+    }
+    fft_plan_s* p = new fft_plan_s();
+    p->rank = rank;
+    p->n0 = dims[0];
+    p->n1 = rank == 2 ? dims[1] : 1;
+    p->batch = batch;
+    p->prec = ip;
+    p->flags = flags;
+    cudaError_t e = cudaGetDevice(&p->device);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "cudaGetDevice");
+    }
+    e = device_twiddles(p->device, ip, &p->tw);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "twiddle table upload");
+    }
+    if (rank == 1 && p->n0 > kRowsMax) {
+        p->radices = split_radices(p->n0);
+        // pass i (span Ns, radix R): W_{Ns R}^{k r} = pa[r][k mod KLO] * pb[r][k / KLO]
+        int64_t Ns = 1;
+        for (size_t i = 0; i < p->radices.size(); ++i) {
+            const int64_t R = p->radices[i];
+            const int64_t klo = Ns < 1024 ? Ns : 1024, nhi = Ns / klo;
+            p->klo_sh.push_back(ilog2(klo));
+            void* da = nullptr;
+            void* db = nullptr;
+            if (Ns > 1) {
+                std::vector<double> a(2 * (size_t)(R * klo)), bt(2 * (size_t)(R * nhi));
+                const int64_t n = Ns * R;
+                for (int64_t r = 0; r < R; ++r) {
+                    for (int64_t k = 0; k < klo; ++k) {
+                        const double ang = -2.0 * M_PI * (double)((r * k) % n) / (double)n;
+                        a[2 * (r * klo + k)] = std::cos(ang);
+                        a[2 * (r * klo + k) + 1] = std::sin(ang);
+                    }
+                    for (int64_t h = 0; h < nhi; ++h) {
+                        const double ang = -2.0 * M_PI * (double)((r * h * klo) % n) / (double)n;
+                        bt[2 * (r * nhi + h)] = std::cos(ang);
+                        bt[2 * (r * nhi + h) + 1] = std::sin(ang);
+                    }
+                }
+                e = upload(a, ip, &da);
+                if (e == cudaSuccess && nhi > 1) e = upload(bt, ip, &db);
+                if (e != cudaSuccess) {
+                    p->pa.push_back(da);
+                    p->pb.push_back(db);
+                    fft_plan_destroy(p);
+                    return cuda_fail(e, "pass twiddle upload");
+                }
+            }
+            p->pa.push_back(da);
+            p->pb.push_back(db);
+            Ns *= R;
+        }
+    }
+    *out = p;
+    return FFT_OK;
+}
+
+fft_status fft_plan_create(fft_plan* out, int64_t n, int64_t batch, int rank) {
+    int64_t dims[2] = {n, n};
+    return fft_plan_create_ex(out, dims, rank, batch, FFT_C64, 0);
+}
+
+fft_status fft_plan_set_stream(fft_plan p, void* s) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    p->stream = (cudaStream_t)s;
+    return FFT_OK;
+}
+
+size_t fft_plan_workspace_bytes(fft_plan p) { return p ? workspace_need(p) : 0; }
+
+fft_status fft_plan_set_workspace(fft_plan p, void* ptr, size_t bytes) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (bytes < workspace_need(p)) return fail(FFT_E_INVALID_ARG, "workspace too small");
+    if (!ptr && bytes) return fail(FFT_E_INVALID_ARG, "null workspace");
+    if (p->ws_owned && p->ws) cudaFree(p->ws);
+    p->ws = ptr;
+    p->ws_bytes = bytes;
+    p->ws_owned = false;
+    return FFT_OK;
+}
+
+static fft_status exec(fft_plan p, const void* in, void* out, bool inv) {
+    fft_status s = check_ptrs(p, in, out, false);
+    if (s != FFT_OK) return s;
+    if (p->nranks > 1) return fail(FFT_E_UNSUPPORTED, "distributed execution not built in this library");
+    if (p->elems() == 0) return FFT_OK;
+    return p->rank == 1 ? run_1d(p, in, out, inv, p->stream) : run_2d(p, in, out, inv, p->stream);
+}
+
+fft_status fft_forward(fft_plan p, const void* in, void* out) { return exec(p, in, out, false); }
+fft_status fft_inverse(fft_plan p, const void* in, void* out) { return exec(p, in, out, true); }
+
+fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filter filter, double param) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (p->rank != 2) return fail(FFT_E_INVALID_ARG, "fft2d_filter_pipeline needs a rank-2 plan");
+    const bool real_in = (p->flags & FFT_IN_REAL_F32) != 0;
+    fft_status s = check_ptrs(p, in, out, real_in);
+    if (s != FFT_OK) return s;
+    if (filter < FFT_FILTER_NONE || filter > FFT_FILTER_IDEAL_LOWPASS) return fail(FFT_E_INVALID_ARG, "unknown filter");
+    if (filter == FFT_FILTER_GAUSS && !(param > 0.0)) return fail(FFT_E_INVALID_ARG, "Gaussian needs param > 0");
+    if ((filter == FFT_FILTER_IDEAL_LITERAL || filter == FFT_FILTER_IDEAL_LOWPASS) && !(param >= 0.0))
+        return fail(FFT_E_INVALID_ARG, "ideal filter needs radius >= 0");
+    if (real_in && in == out) return fail(FFT_E_INVALID_ARG, "real input cannot alias the complex output");
+    if (p->nranks > 1) return fail(FFT_E_UNSUPPORTED, "distributed execution not built in this library");
+    if (p->elems() == 0) return FFT_OK;
+    return run_pipeline(p, in, out, filter, param, p->stream);
+}
+
+fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void* host_out, fft_filter filter,
+                            double param) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (!host_in || !host_out) return fail(FFT_E_INVALID_ARG, "null host pointer");
+    if (direction == 0 && p->rank != 2) return fail(FFT_E_INVALID_ARG, "pipeline needs a rank-2 plan");
+    if (direction < -1 || direction > 1) return fail(FFT_E_INVALID_ARG, "direction must be -1, 0 or +1");
+    if (p->nranks > 1) return fail(FFT_E_UNSUPPORTED, "host execution of a distributed plan");
+    const int64_t total = p->elems();
+    if (total == 0) return FFT_OK;
+    const bool real_in = direction == 0 && (p->flags & FFT_IN_REAL_F32);
+    const size_t eb = p->elem_bytes();
+    const size_t in_eb = real_in ? 4 : eb;
+    // rows per chunk: 1D plans are split over the batch (independent
+    // transforms); 2D plans over the batch of grids.
+    const int64_t unit = p->rank == 1 ? p->n0 : p->n0 * p->n1;  // elements per transform
+    const int64_t units = p->batch;
+    const size_t target = (size_t)256 << 20;
+    int64_t per = (int64_t)(target / (unit * eb));
+    if (per < 1) per = 1;
+    if (per > units) per = units;
+    const size_t chunk_bytes = (size_t)(per * unit) * eb;
+    cudaError_t e;
+    if (p->hbuf_bytes < chunk_bytes) {
+        for (int i = 0; i < 2; ++i) {
+            if (p->hbuf[i]) cudaFree(p->hbuf[i]);
+            if (p->hbin[i]) cudaFree(p->hbin[i]);
+            p->hbuf[i] = p->hbin[i] = nullptr;
+        }
+        p->hbuf_bytes = 0;
+        for (int i = 0; i < 2; ++i) {
+            e = cudaMalloc(&p->hbuf[i], chunk_bytes);
+            if (e == cudaSuccess) e = cudaMalloc(&p->hbin[i], chunk_bytes);
+            if (e != cudaSuccess) return fail(FFT_E_ALLOC, "host-execution staging buffers");
+        }
+        p->hbuf_bytes = chunk_bytes;
+    }
+    for (int i = 0; i < 2; ++i)
+        if (!p->hstream[i]) {
+            e = cudaStreamCreateWithFlags(&p->hstream[i], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        }
+    if (!p->hev) {
+        e = cudaEventCreateWithFlags(&p->hev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+    }
+    // order after the work already queued on the plan stream
+    e = cudaEventRecord(p->hev, p->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->hstream[0], p->hev, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->hstream[1], p->hev, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
+    const int64_t saved_batch = p->batch;
+    int launches = 0;
+    fft_status s = FFT_OK;
+    for (int64_t u0 = 0, c = 0; u0 < units && s == FFT_OK; u0 += per, ++c) {
+        const int64_t nu = (units - u0) < per ? (units - u0) : per;
+        cudaStream_t st = p->hstream[c & 1];
+        void* d = p->hbuf[c & 1];
+        void* din = p->hbin[c & 1];
+        e = cudaMemcpyAsync(din, (const char*)host_in + (size_t)(u0 * unit) * in_eb, (size_t)(nu * unit) * in_eb,
+                            cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) {
+            s = cuda_fail(e, "H2D copy");
+            break;
+        }
+        p->batch = nu;
+        if (direction == 0)
+            s = run_pipeline(p, din, d, filter, param, st);
+        else
+            s = p->rank == 1 ? run_1d(p, din, d, direction < 0, st) : run_2d(p, din, d, direction < 0, st);
+        launches += p->last_launches;
+        p->batch = saved_batch;
+        if (s != FFT_OK) break;
+        e = cudaMemcpyAsync((char*)host_out + (size_t)(u0 * unit) * eb, d, (size_t)(nu * unit) * eb,
+                            cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) s = cuda_fail(e, "D2H copy");
+    }
+    p->last_launches = launches;
+    cudaError_t e0 = cudaStreamSynchronize(p->hstream[0]);
+    cudaError_t e1 = cudaStreamSynchronize(p->hstream[1]);
+    if (s != FFT_OK) return s;
+    if (e0 != cudaSuccess) return cuda_fail(e0, "host execution");
+    if (e1 != cudaSuccess) return cuda_fail(e1, "host execution");
+    return FFT_OK;
+}
+
+fft_status fft_nccl_unique_id(unsigned char id[128]) {
+    (void)id;
+    return fail(FFT_E_UNSUPPORTED, "NCCL support not built in this library");
+}
+
+fft_status fft_plan_set_comm(fft_plan p, const unsigned char id[128], int nranks, int my_rank) {
+    (void)id;
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (nranks < 1 || my_rank < 0 || my_rank >= nranks) return fail(FFT_E_INVALID_ARG, "bad rank / nranks");
+    if (nranks == 1) return FFT_OK;
+    return fail(FFT_E_UNSUPPORTED, "NCCL support not built in this library");
+}
+
+int fft_plan_last_launch_count(fft_plan p) { return p ? p->last_launches : 0; }
+
+fft_status fft_plan_destroy(fft_plan p) {
+    if (!p) return FFT_OK;
+    cudaError_t e = cudaSuccess;
+    for (void* q : p->pa)
+        if (q) cudaFree(q);
+    for (void* q : p->pb)
+        if (q) cudaFree(q);
+    if (p->gu) cudaFree(p->gu);
+    if (p->gv) cudaFree(p->gv);
+    if (p->ws_owned && p->ws) cudaFree(p->ws);
+    for (int i = 0; i < 2; ++i) {
+        if (p->hbuf[i]) cudaFree(p->hbuf[i]);
+        if (p->hbin[i]) cudaFree(p->hbin[i]);
+        if (p->hstream[i]) cudaStreamDestroy(p->hstream[i]);
+    }
+    if (p->hev) cudaEventDestroy(p->hev);
+    e = cudaGetLastError();
+    delete p;
+    if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error at destroy");
+    return FFT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,31 @@
+"""Small invocation of the hot kernels for ncu captures (one launch each)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import fixtures  # noqa: E402
+import paper_cs_0103001_b200 as b  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "all"
+dev = torch.device("cuda:0")
+if which in ("all", "c2"):
+    batch = int(os.environ.get("C2_BATCH", "4096"))
+    x = torch.from_numpy(fixtures.complex_input(batch * 65536, 1, seed=2).reshape(batch, 65536)).to(dev)
+    y = torch.empty_like(x)
+    p = b.Plan((65536,), batch=batch)
+    p.forward(x, y)
+    torch.cuda.synchronize()
+    p.forward(x, y)
+    torch.cuda.synchronize()
+if which in ("all", "c3"):
+    img = torch.from_numpy(fixtures.sky_image(2048, 2048, seed=3)).to(dev)
+    out = torch.empty((2048, 2048), dtype=torch.complex64, device=dev)
+    p = b.Plan((2048, 2048), flags=b.IN_REAL_F32)
+    p.filter_pipeline(img, out, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    p.filter_pipeline(img, out, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+print("ok")

@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle,
+element by element on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative L2 over the whole output
+<= 1e-5 for complex64 and <= 1e-12 for complex128.
+"""
+import numpy as np
+import pytest
+
+import fixtures
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {np.complex64: 1e-5, np.complex128: 1e-12}
+
+
+@pytest.fixture(scope="module")
+def fft():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_cs_0103001_b200 as b
+
+    b.load_library()
+    return b
+
+
+def prec_of(dtype):
+    import paper_cs_0103001_b200 as b
+
+    return b.C64 if dtype == np.complex64 else b.C128
+
+
+def run_1d(b, x, inverse=False):
+    batch, n = x.shape
+    p = b.Plan((n,), batch=batch, precision=prec_of(x.dtype.type))
+    p.set_stream(torch.cuda.current_stream())
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    (p.inverse if inverse else p.forward)(xd, yd)
+    torch.cuda.synchronize()
+    out = yd.cpu().numpy()
+    p.destroy()
+    return out
+
+
+# ------------------------------------------------------------------- 1D
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+@pytest.mark.parametrize("m", range(0, 14))
+@pytest.mark.parametrize("batch", [1, 3, 64])
+def test_1d_single_pass_sizes(fft, dtype, m, batch):
+    n = 1 << m
+    x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=100 + m, dtype=dtype).reshape(batch, n)
+    y = run_1d(fft, x)
+    assert oracle.rel_l2(y, oracle.fft_batch(x)) <= TOL[dtype]
+    z = run_1d(fft, x, inverse=True)
+    assert oracle.rel_l2(z, oracle.fft_batch(x, inverse=True)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+@pytest.mark.parametrize("m", [14, 15, 16, 17, 18, 20, 21, 22])
+def test_1d_multi_pass_sizes(fft, dtype, m):
+    n = 1 << m
+    batch = 2 if m <= 20 else 1
+    x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=200 + m, dtype=dtype).reshape(batch, n)
+    y = run_1d(fft, x)
+    assert oracle.rel_l2(y, oracle.fft_batch(x)) <= TOL[dtype]
+    z = run_1d(fft, x, inverse=True)
+    assert oracle.rel_l2(z, oracle.fft_batch(x, inverse=True)) <= TOL[dtype]
+
+
+def test_c1_config(fft):
+    """BASELINE configs[0]: N=1024, batch 1, complex128, U[-1,1], seed 1;
+    forward (1/N) then inverse round trip."""
+    x = fixtures.complex_input(1024, fixtures.UNIFORM, seed=1, dtype=np.complex128).reshape(1, 1024)
+    y = run_1d(fft, x)
+    assert oracle.rel_l2(y, oracle.fft_batch(x)) <= 1e-12
+    z = run_1d(fft, y, inverse=True)
+    assert oracle.rel_l2(z, x) <= 1e-12
+
+
+def test_impulse_is_exact(fft):
+    # delta_0 -> flat 1/N exactly (F2: the power-of-two scale is exact)
+    for n in (16, 1024, 8192, 65536):
+        x = np.zeros((1, n), np.complex64)
+        x[0, 0] = 1
+        y = run_1d(fft, x)
+        assert np.array_equal(y, np.full((1, n), 1.0 / n, np.complex64))
+
+
+def test_inplace_and_empty(fft):
+    import paper_cs_0103001_b200 as b
+
+    for n in (256, 65536, 1 << 21):
+        x = fixtures.complex_input(n, fixtures.NORMAL, seed=7).reshape(1, n)
+        p = b.Plan((n,), batch=1)
+        xd = torch.from_numpy(x).cuda()
+        p.forward(xd)  # out == in
+        torch.cuda.synchronize()
+        assert oracle.rel_l2(xd.cpu().numpy(), oracle.fft_batch(x)) <= 1e-5
+    p0 = b.Plan((256,), batch=0)
+    p0.forward(torch.empty(1, dtype=torch.complex64, device="cuda"))
+    torch.cuda.synchronize()
+
+
+def test_c2_full_size_sampled(fft):
+    """BASELINE configs[1]: 4096 x 65536 complex64, N(0,1), seed 2, in the
+    launch configuration bench.py times; 16 sampled rows against the oracle,
+    plus the round trip over the whole batch."""
+    import paper_cs_0103001_b200 as b
+
+    n, batch = 65536, 4096
+    x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=2).reshape(batch, n)
+    p = b.Plan((n,), batch=batch)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    p.forward(xd, yd)
+    zd = torch.empty_like(xd)
+    p.inverse(yd, zd)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(0).choice(batch, 16, replace=False)
+    rows = np.concatenate([rows, [0, batch - 1]])
+    y = yd[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert oracle.rel_l2(y, oracle.fft_batch(x[rows])) <= 1e-5
+    zr = zd[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert oracle.rel_l2(zr, oracle.fft_batch(y, inverse=True)) <= 1e-5
+    # whole-batch round trip (property at any size)
+    err = torch.linalg.vector_norm(zd - xd) / torch.linalg.vector_norm(xd)
+    assert float(err) <= 1e-5
+
+
+# ------------------------------------------------------------------- 2D
+def run_2d(b, f, inverse=False):
+    N, M = f.shape
+    p = b.Plan((N, M), batch=1, precision=prec_of(f.dtype.type))
+    fd = torch.from_numpy(f).cuda()
+    od = torch.empty_like(fd)
+    (p.inverse if inverse else p.forward)(fd, od)
+    torch.cuda.synchronize()
+    p.destroy()
+    return od.cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+@pytest.mark.parametrize("N,M", [(1, 1), (2, 8), (8, 2), (16, 16), (64, 32), (32, 1024), (256, 512),
+                                 (4096, 16), (16, 4096), (1024, 1024)])
+def test_2d_forward_inverse(fft, dtype, N, M):
+    f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=300 + N + M, dtype=dtype).reshape(N, M)
+    F = run_2d(fft, f)
+    assert oracle.rel_l2(F, oracle.fft2d(f)) <= TOL[dtype]
+    g = run_2d(fft, f, inverse=True)
+    assert oracle.rel_l2(g, oracle.ifft2d(f)) <= TOL[dtype]
+
+
+def test_2d_8192_columns(fft):
+    f = fixtures.complex_input(8192 * 16, fixtures.UNIFORM, seed=5).reshape(8192, 16)
+    assert oracle.rel_l2(run_2d(fft, f), oracle.fft2d(f)) <= 1e-5
+
+
+def run_pipeline(b, f, filt, param, real=False):
+    N, M = f.shape
+    flags = b.IN_REAL_F32 if real else 0
+    prec = b.C64 if (real or f.dtype == np.complex64) else b.C128
+    p = b.Plan((N, M), batch=1, precision=prec, flags=flags)
+    fd = torch.from_numpy(f).cuda()
+    od = torch.empty((N, M), dtype=torch.complex64 if prec == b.C64 else torch.complex128, device="cuda")
+    p.filter_pipeline(fd, od, filt, param)
+    torch.cuda.synchronize()
+    p.destroy()
+    return od.cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+@pytest.mark.parametrize("N,M", [(16, 16), (64, 64), (128, 32), (512, 512)])
+def test_gauss_pipeline(fft, dtype, N, M):
+    import paper_cs_0103001_b200 as b
+
+    f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=400 + N, dtype=dtype).reshape(N, M)
+    out = run_pipeline(b, f, b.FILTER_GAUSS, 0.1)
+    assert oracle.rel_l2(out, oracle.gauss_pipeline(f, 0.1)) <= TOL[dtype]
+
+
+def ideal_mask(N, M, b_, literal):
+    u = np.arange(N)[:, None]
+    v = np.arange(M)[None, :]
+    if literal:  # Eq. (filtro): 0 inside radius b of the centre, 1 outside
+        return np.where((u - N // 2) ** 2 + (v - M // 2) ** 2 <= b_ * b_, 0.0, 1.0)
+    ku = np.where(u < N // 2, u, u - N)
+    kv = np.where(v < M // 2, v, v - M)
+    return np.where(ku ** 2 + kv ** 2 <= b_ * b_, 1.0, 0.0)
+
+
+@pytest.mark.parametrize("literal", [True, False])
+def test_ideal_filter_pipeline(fft, literal):
+    import paper_cs_0103001_b200 as b
+
+    N = M = 512
+    f = fixtures.sky_image(N, M, seed=9, nsrc=30)
+    radius = 340.0 if literal else 40.0
+    kind = b.FILTER_IDEAL_LITERAL if literal else b.FILTER_IDEAL_LOWPASS
+    out = run_pipeline(b, f, kind, radius, real=True)
+    ref = oracle.filter_pipeline(f.astype(np.complex128), ideal_mask(N, M, radius, literal))
+    assert oracle.rel_l2(out, ref) <= 1e-5
+
+
+def test_c3_config(fft):
+    """BASELINE configs[2]: 2048^2 float32 sky image -> 2D FFT -> Gaussian
+    (0.1 Nyquist) -> inverse 2D FFT, complex64, against the oracle."""
+    import paper_cs_0103001_b200 as b
+
+    img = fixtures.sky_image(2048, 2048, seed=3)
+    out = run_pipeline(b, img, b.FILTER_GAUSS, 0.1, real=True)
+    ref = oracle.gauss_pipeline(img.astype(np.complex128), 0.1)
+    assert oracle.rel_l2(out, ref) <= 1e-5
+
+
+def test_c4_config_single_gpu(fft):
+    """BASELINE configs[3] at P=1: 8192^2 complex64 U[-1,1], seed 4, same
+    Gaussian; compared with the oracle over the whole grid."""
+    import paper_cs_0103001_b200 as b
+
+    N = 8192
+    f = fixtures.complex_input(N * N, fixtures.UNIFORM, seed=4).reshape(N, N)
+    out = run_pipeline(b, f, b.FILTER_GAUSS, 0.1)
+    ref = oracle.gauss_pipeline(f, 0.1)
+    assert oracle.rel_l2(out, ref) <= 1e-5
+
+
+def test_c5_config_single_gpu_sampled(fft):
+    """BASELINE configs[4] at P=1: N = 2^30 complex64, N(0,1), seed 5.  The
+    oracle's direct compensated sums give 16 sampled bins (O7); the round trip
+    and Parseval hold over the whole transform."""
+    import paper_cs_0103001_b200 as b
+
+    n = 1 << 30
+    x = np.empty(n, np.complex64)
+    fixtures.complex_input(n, fixtures.NORMAL, seed=5, out=x)
+    p = b.Plan((n,), batch=1)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    p.forward(xd, yd)
+    torch.cuda.synchronize()
+    bins = np.concatenate([[0, 1, n // 2, n - 1], np.random.default_rng(5).integers(0, n, 12)])
+    got = yd[torch.from_numpy(bins).cuda()].cpu().numpy()
+    ref = oracle.dft_bins(x, bins)
+    assert oracle.rel_l2(got, ref) <= 1e-5
+    # Parseval with the 1/N convention: sum|x|^2 = N sum|X|^2
+    sx = float(torch.sum(xd.abs().double() ** 2))
+    sX = float(torch.sum(yd.abs().double() ** 2)) * n
+    assert abs(sx - sX) / sx < 1e-5
+    zd = torch.empty_like(xd)
+    p.inverse(yd, zd)
+    torch.cuda.synchronize()
+    err = torch.linalg.vector_norm(zd - xd) / torch.linalg.vector_norm(xd)
+    assert float(err) <= 1e-5

@@ -285,6 +285,8 @@ def test_dft_bins_match_library(m):
     got = oracle.dft_bins(x, bins)
     ref = (np.fft.fft(x) / N)[bins]
     assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-12
+    x32 = x.astype(np.complex64)
+    assert np.max(np.abs(oracle.dft_bins(x32, bins) - (np.fft.fft(x32.astype(complex)) / N)[bins])) < 1e-12
     goti = oracle.dft_bins(x, bins, inverse=True)
     refi = (np.fft.ifft(x) * N)[bins]
     assert np.max(np.abs(goti - refi)) / np.max(np.abs(refi)) < 1e-12
