@@ -28,4 +28,10 @@ cudaError_t launch_pass(int prec, bool inv, int64_t R, const void* in, void* out
                         int64_t Ns, int64_t batch, double scale, const void* tw, const void* pa,
                         const void* pb, int klo_sh, cudaStream_t st);
 
+// One-pass cluster FFT (fft_cluster.cuh): n = n1 * n2 in one thread-block
+// cluster per transform.  tw4: W_n^{n1 k2} laid out [k2][n1].
+bool cluster_supported(int prec, int64_t n, int* n1, int* n2);
+cudaError_t launch_cluster(int prec, bool inv, int64_t n, const void* in, void* out, int64_t batch,
+                           double scale, const void* tw4, const void* tw, int variant, cudaStream_t st);
+
 }  // namespace b200fft

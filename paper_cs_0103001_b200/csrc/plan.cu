@@ -128,6 +128,9 @@ struct fft_plan_s {
     std::vector<int64_t> radices;
     std::vector<void*> pa, pb;  // per pass twiddle tables [r][k_lo], [r][k_hi]
     std::vector<int> klo_sh;
+    // one-pass cluster 1D (n = cn1 * cn2): four-step twiddles [k2][n1]
+    void* tw4 = nullptr;
+    int cvariant = 0;  // tuning knob (B200FFT_CLUSTER_VARIANT), see kernels_cluster.cu
     // filter tables (Gaussian)
     void* gu = nullptr;
     void* gv = nullptr;
@@ -196,6 +199,14 @@ fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream
     const int64_t L = p->n0;
     const double scale = inv ? 1.0 : 1.0 / (double)L;
     cudaError_t e;
+    if (p->tw4) {
+        // one HBM pass: the cluster kernel reads each transform fully before
+        // it writes it, so out == in is safe
+        e = launch_cluster(p->prec, inv, L, in, out, p->batch, scale, p->tw4, p->tw, p->cvariant, st);
+        p->last_launches = 1;
+        if (e != cudaSuccess) return cuda_fail(e, "k_cluster launch");
+        return FFT_OK;
+    }
     if (p->radices.empty()) {
         e = launch_rows(p->prec, inv, false, L, in, out, p->batch, scale, p->tw, st);
         p->last_launches = 1;
@@ -378,7 +389,32 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
         delete p;
         return cuda_fail(e, "twiddle table upload");
     }
-    if (rank == 1 && p->n0 > kRowsMax) {
+    int cn1 = 0, cn2 = 0;
+    const char* no_cluster = getenv("B200FFT_NO_CLUSTER");
+    if (rank == 1 && p->n0 > kRowsMax && !(no_cluster && no_cluster[0] == '1') &&
+        cluster_supported(ip, p->n0, &cn1, &cn2)) {
+        // W_N^{n1 k2}, [k2][n1]
+        std::vector<double> t(2 * (size_t)p->n0);
+        for (int64_t k2 = 0; k2 < cn2; ++k2)
+            for (int64_t n1 = 0; n1 < cn1; ++n1) {
+                const int64_t x = (n1 * k2) % p->n0;
+                const double ang = -2.0 * M_PI * (double)x / (double)p->n0;
+                t[2 * (k2 * cn1 + n1)] = std::cos(ang);
+                t[2 * (k2 * cn1 + n1) + 1] = std::sin(ang);
+            }
+        const char* var = getenv("B200FFT_CLUSTER_VARIANT");
+        // default: st.async transpose, 16-CTA clusters, 4 CTAs/SM (the
+        // fastest measured); 8/9 are timing-only
+        p->cvariant = var ? atoi(var) : 10;
+        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 10;
+        if (var && atoi(var) == 8 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 8;
+        if (var && atoi(var) == 9 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 9;
+        e = upload(t, ip, &p->tw4);
+        if (e != cudaSuccess) {
+            fft_plan_destroy(p);
+            return cuda_fail(e, "four-step twiddle upload");
+        }
+    } else if (rank == 1 && p->n0 > kRowsMax) {
         p->radices = split_radices(p->n0);
         // pass i (span Ns, radix R): W_{Ns R}^{k r} = pa[r][k mod KLO] * pb[r][k / KLO]
         int64_t Ns = 1;
@@ -575,6 +611,7 @@ int fft_plan_last_launch_count(fft_plan p) { return p ? p->last_launches : 0; }
 fft_status fft_plan_destroy(fft_plan p) {
     if (!p) return FFT_OK;
     cudaError_t e = cudaSuccess;
+    if (p->tw4) cudaFree(p->tw4);
     for (void* q : p->pa)
         if (q) cudaFree(q);
     for (void* q : p->pb)

@@ -70,6 +70,16 @@ def test_1d_multi_pass_sizes(fft, dtype, m):
     assert oracle.rel_l2(z, oracle.fft_batch(x, inverse=True)) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_1d_65536_multipass_fallback(fft, dtype, monkeypatch):
+    """The generic 2-pass schedule for N = 65536 (the one-pass cluster kernel
+    is disabled at plan creation) against the oracle."""
+    monkeypatch.setenv("B200FFT_NO_CLUSTER", "1")
+    x = fixtures.complex_input(3 * 65536, fixtures.NORMAL, seed=216, dtype=dtype).reshape(3, 65536)
+    assert oracle.rel_l2(run_1d(fft, x), oracle.fft_batch(x)) <= TOL[dtype]
+    assert oracle.rel_l2(run_1d(fft, x, inverse=True), oracle.fft_batch(x, inverse=True)) <= TOL[dtype]
+
+
 def test_c1_config(fft):
     """BASELINE configs[0]: N=1024, batch 1, complex128, U[-1,1], seed 1;
     forward (1/N) then inverse round trip."""
