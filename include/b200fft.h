@@ -140,7 +140,16 @@ fft_status fft_execute_host(fft_plan plan, int direction, const void* host_in, v
  * Every rank calls every distributed entry point with identical plan
  * parameters (collective semantics, NCCL-style). */
 fft_status fft_nccl_unique_id(unsigned char id[128]); /* on one rank; broadcast it */
+/* Collective over the nranks processes: creates the plan's own NCCL
+ * communicator (ncclCommInitRank).  After it, rank-2 plans take LOCAL slabs
+ * (batch x N/nranks x M elements per call); rank-1 plans keep their own
+ * (local) batch and run without any collective. */
 fft_status fft_plan_set_comm(fft_plan plan, const unsigned char id[128], int nranks, int my_rank);
+/* Tests / diagnostics: run the slab-decomposed schedule of a rank-2 plan as
+ * `nranks` virtual ranks on this one GPU (the all-to-alls become device
+ * copies); in/out stay the whole grid.  Same kernels and layouts as the NCCL
+ * path. */
+fft_status fft_plan_set_virtual_ranks(fft_plan plan, int nranks);
 
 fft_status fft_plan_destroy(fft_plan plan);
 

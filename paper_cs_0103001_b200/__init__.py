@@ -34,7 +34,8 @@ IN_REAL_F32 = 1 << 1
 EXPORTS = [
     "fft_plan_create", "fft_plan_create_ex", "fft_plan_set_stream", "fft_plan_workspace_bytes",
     "fft_plan_set_workspace", "fft_forward", "fft_inverse", "fft2d_filter_pipeline",
-    "fft_execute_host", "fft_nccl_unique_id", "fft_plan_set_comm", "fft_plan_destroy",
+    "fft_execute_host", "fft_nccl_unique_id", "fft_plan_set_comm", "fft_plan_set_virtual_ranks",
+    "fft_plan_destroy",
     "fft_status_string", "fft_last_error", "fft_plan_last_launch_count", "fft_build_info",
 ]
 
@@ -70,6 +71,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fft_execute_host": ([vp, ci, vp, vp, ci, cd], ci),
         "fft_nccl_unique_id": ([ctypes.c_char_p], ci),
         "fft_plan_set_comm": ([vp, ctypes.c_char_p, ci, ci], ci),
+        "fft_plan_set_virtual_ranks": ([vp, ci], ci),
         "fft_plan_destroy": ([vp], ci),
         "fft_status_string": ([ci], ctypes.c_char_p),
         "fft_last_error": ([], ctypes.c_char_p),
@@ -163,6 +165,11 @@ class Plan:
     def set_comm(self, unique_id: bytes, nranks: int, rank: int) -> None:
         _check(load_library().fft_plan_set_comm(self._h, unique_id, int(nranks), int(rank)),
                "fft_plan_set_comm")
+
+    def set_virtual_ranks(self, nranks: int) -> None:
+        """Tests: emulate the slab decomposition over ``nranks`` virtual ranks on this GPU."""
+        _check(load_library().fft_plan_set_virtual_ranks(self._h, int(nranks)),
+               "fft_plan_set_virtual_ranks")
 
     def last_launch_count(self) -> int:
         return int(load_library().fft_plan_last_launch_count(self._h))

@@ -111,10 +111,18 @@ struct LineFFT {
 //   out[row][i] = scale * sum_j in[row][j] W_R^{+-ij},  rows < batch.
 // W lines (rows) per CTA.  REAL_IN: input rows are float32 real values
 // (promotion to complex fused into the load, BASELINE configs[2]).
+// in_sh / out_sh >= 0: the rows are stored in column blocks of 2^sh (the
+// all-to-all pack layout of the slab-decomposed 2D transform):
+// element (row, v) at ((v >> sh) * batch + row) << sh | (v & (2^sh - 1)).
 // --------------------------------------------------------------------------
+__device__ __forceinline__ int64_t row_index(int64_t row, int64_t v, int64_t R, int64_t batch, int sh) {
+    return sh < 0 ? row * R + v : ((((v >> sh) * batch + row) << sh) | (v & ((1ll << sh) - 1)));
+}
+
 template <typename T, int R, int E, int W, bool INV, bool REAL_IN>
 __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_, cpx<T>* __restrict__ out,
-                                                    int64_t batch, T scale, const cpx<T>* __restrict__ tw) {
+                                                    int64_t batch, T scale, const cpx<T>* __restrict__ tw,
+                                                    int in_sh, int out_sh) {
     using C = cpx<T>;
     using F = LineFFT<T, R, E, INV>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -126,7 +134,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_
     C v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
-        const int64_t idx = row * R + lt + F::TPL * m;
+        const int64_t idx = row_index(row, lt + F::TPL * m, R, batch, in_sh);
         if constexpr (REAL_IN) {
             const float* in = reinterpret_cast<const float*>(in_);
             v[F::pos_in(m)] = valid ? mk((T)__ldg(in + idx), (T)0) : mk((T)0, (T)0);
@@ -138,7 +146,8 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_
     F::run(v, smem + t * F::LS, lt, tw);
     if (valid) {
 #pragma unroll
-        for (int m = 0; m < E; ++m) out[row * R + lt + F::TPL * m] = cscale(v[F::pos_out(m)], scale);
+        for (int m = 0; m < E; ++m)
+            out[row_index(row, lt + F::TPL * m, R, batch, out_sh)] = cscale(v[F::pos_out(m)], scale);
     }
 }
 
@@ -153,7 +162,8 @@ struct FilterArgs {
     double b2;          // radius^2 for the ideal filters
     const void* gu;     // T[N] (GAUSS)
     const void* gv;     // T[M] (GAUSS)
-    int64_t N, M;
+    int64_t N, M;       // global grid
+    int64_t col_off;    // global index of local column 0 (column slab of a distributed plan)
 };
 
 template <typename T>
@@ -222,7 +232,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int64_t u = lt + F::TPL * m;
-            const T h = (col < S) ? filter_value<T>(filt, u, col) * scale : (T)0;
+            const T h = (col < S) ? filter_value<T>(filt, u, col + filt.col_off) * scale : (T)0;
             w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], h);
         }
         FI::run(w, line, lt, tw);

@@ -23,6 +23,10 @@
 #include <string>
 #include <vector>
 
+#ifdef B200FFT_WITH_NCCL
+#include <nccl.h>  // the torch wheel's NCCL 2.28 (not /usr/include's 2.27)
+#endif
+
 #include "../../include/b200fft.h"
 #include "fft_engine.cuh"
 #include "launch.h"
@@ -146,17 +150,27 @@ struct fft_plan_s {
     cudaStream_t hstream[2] = {nullptr, nullptr};
     cudaEvent_t hev = nullptr;
     int last_launches = 0;
-    // distributed
+    // distributed (slab decomposition of rank-2 plans)
     int nranks = 1, my_rank = 0;
-    void* comm = nullptr;
+    void* comm = nullptr;  // ncclComm_t owned by the plan
+    int virt = 1;          // virtual ranks emulated on this GPU (tests), 1 = off
+    cudaEvent_t dev_ev = nullptr;
 
     size_t elem_bytes() const { return prec == 0 ? 8 : 16; }
-    int64_t elems() const { return batch * n0 * (rank == 2 ? n1 : 1); }
+    int P() const { return comm ? nranks : virt; }
+    // slab-decomposed schedule: a communicator (any size, 1 included) or virtual ranks
+    bool dist() const { return rank == 2 && (comm != nullptr || virt > 1); }
+    // elements addressed by one call: the local slab (NCCL) or everything (virtual)
+    int64_t elems() const {
+        if (rank == 2 && comm) return batch * (n0 / nranks) * n1;
+        return batch * n0 * (rank == 2 ? n1 : 1);
+    }
 };
 
 namespace {
 
 size_t workspace_need(const fft_plan_s* p) {
+    if (p->dist()) return 2 * (size_t)p->elems() * p->elem_bytes();  // send + recv slabs
     if (p->rank == 1 && !p->radices.empty()) {
         size_t one = (size_t)p->elems() * p->elem_bytes();
         return p->radices.size() >= 3 ? 2 * one : one;
@@ -316,6 +330,128 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
     e = launch_rows(p->prec, true, false, M, out, out, p->batch * N, 1.0, p->tw, st);
     if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
     p->last_launches = 3;
+    return FFT_OK;
+}
+
+// ---- distributed slab decomposition of rank-2 plans ---------------------
+// P ranks (NCCL processes, or P virtual ranks on one GPU for tests).  Rank r
+// owns rows [r SN, (r+1) SN) (SN = N/P) of every grid; after the first
+// all-to-all it owns columns [r SM, (r+1) SM) (SM = M/P) as an [N][SM]
+// row-major column slab.  Block q of a rank's send slab is its SN rows x the
+// SM columns of rank q, which k_rows writes directly (blocked store), so the
+// exchange needs no pack kernel; the way back lands blocked by source rank
+// and k_rows reads it blocked (fused unpack).
+//   pipeline: rows fwd -> a2a -> cols fwd*H/(NM)*inv -> a2a -> rows inv
+//   forward : rows fwd -> a2a -> cols fwd (1/N) -> a2a -> unblock copy
+//   inverse : rows inv (1/M) -> a2a -> cols inv -> a2a -> unblock copy
+fft_status dist_exchange(fft_plan_s* p, char* send, char* recv, int64_t blk, cudaStream_t st) {
+    const int P = p->P();
+    const size_t eb = p->elem_bytes(), bytes = (size_t)blk * eb;
+    if (p->comm) {
+#ifdef B200FFT_WITH_NCCL
+        ncclComm_t comm = (ncclComm_t)p->comm;
+        const ncclDataType_t dt = p->prec == 0 ? ncclFloat : ncclDouble;
+        const size_t count = 2 * (size_t)blk;
+        ncclResult_t r = ncclGroupStart();
+        for (int q = 0; q < P && r == ncclSuccess; ++q) {
+            r = ncclSend(send + q * bytes, count, dt, q, comm, st);
+            if (r == ncclSuccess) r = ncclRecv(recv + q * bytes, count, dt, q, comm, st);
+        }
+        ncclResult_t r2 = ncclGroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(FFT_E_NCCL, std::string("all-to-all: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+        return FFT_OK;
+#else
+        return fail(FFT_E_UNSUPPORTED, "library built without NCCL");
+#endif
+    }
+    // virtual ranks: slab r of send/recv at r * P * blk; recv[q][r] = send[r][q]
+    for (int r = 0; r < P; ++r) {
+        cudaError_t e = cudaMemcpy2DAsync(recv + r * bytes, P * bytes, send + (size_t)r * P * bytes, bytes, bytes,
+                                          (size_t)P, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "virtual all-to-all");
+    }
+    return FFT_OK;
+}
+
+// mode 0: forward (eq5), 1: inverse (2D-IDFT), 2: filter pipeline
+fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_filter filter, double param,
+                       cudaStream_t st) {
+    const int P = p->P();
+    const int64_t N = p->n0, M = p->n1, SN = N / P, SM = M / P;
+    if (N % P || M % P || SN < 1 || SM < 1) return fail(FFT_E_INVALID_SIZE, "grid not divisible by the rank count");
+    fft_status s = ensure_workspace(p);
+    if (s != FFT_OK) return s;
+    const size_t eb = p->elem_bytes();
+    const int64_t slab = SN * M;      // elements per rank per grid
+    const int64_t blk = SN * SM;      // elements per (rank, peer) block
+    const int sh = ilog2(SM);
+    const int nloc = p->comm ? 1 : P;  // slabs handled by this process
+    const int r0 = p->comm ? p->my_rank : 0;
+    char* ws0 = (char*)p->ws;
+    char* ws1 = ws0 + (size_t)nloc * slab * eb;
+    const bool real_in = mode == 2 && (p->flags & FFT_IN_REAL_F32);
+    const size_t in_eb = real_in ? 4 : eb;
+    FilterArgs f{};
+    f.kind = mode == 2 ? (int)filter : 0;
+    f.N = N;
+    f.M = M;
+    if (mode == 2 && filter == FFT_FILTER_GAUSS) {
+        s = gauss_tables(p, param);
+        if (s != FFT_OK) return s;
+        f.gu = p->gu;
+        f.gv = p->gv;
+    } else if (mode == 2) {
+        f.b2 = param * param;
+    }
+    cudaError_t e;
+    int launches = 0;
+    for (int64_t g = 0; g < p->batch; ++g) {
+        const char* gin = (const char*)in + (size_t)g * nloc * slab * in_eb;
+        char* gout = (char*)out + (size_t)g * nloc * slab * eb;
+        // 1. rows (length M) of every local slab, stored in peer blocks
+        for (int l = 0; l < nloc; ++l) {
+            const bool inv_rows = mode == 1;
+            const double sc = mode == 1 ? 1.0 / (double)M : 1.0;
+            e = launch_rows(p->prec, inv_rows, real_in, M, gin + (size_t)l * slab * in_eb, ws0 + (size_t)l * slab * eb,
+                            SN, sc, p->tw, st, -1, sh);
+            if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
+            ++launches;
+        }
+        s = dist_exchange(p, ws0, ws1, blk, st);
+        if (s != FFT_OK) return s;
+        // 2. columns (length N) of every local column slab [N][SM]
+        for (int l = 0; l < nloc; ++l) {
+            FilterArgs fl = f;
+            fl.col_off = (int64_t)(r0 + l) * SM;
+            const int cmode = mode == 2 ? 2 : mode;
+            const double sc = mode == 2 ? 1.0 / ((double)N * (double)M) : (mode == 0 ? 1.0 / (double)N : 1.0);
+            char* cs = ws1 + (size_t)l * slab * eb;
+            e = launch_cols(p->prec, cmode, N, cs, cs, SM, 1, sc, p->tw, fl, st);
+            if (e != cudaSuccess) return cuda_fail(e, "k_cols launch");
+            ++launches;
+        }
+        s = dist_exchange(p, ws1, ws0, blk, st);
+        if (s != FFT_OK) return s;
+        // 3. back to natural row slabs
+        for (int l = 0; l < nloc; ++l) {
+            const char* src = ws0 + (size_t)l * slab * eb;
+            char* dst = gout + (size_t)l * slab * eb;
+            if (mode == 2) {
+                e = launch_rows(p->prec, true, false, M, src, dst, SN, 1.0, p->tw, st, sh, -1);
+                ++launches;
+            } else {
+                // block q (SN x SM, from rank q) holds columns [q SM, (q+1) SM):
+                // its row x (at src + (q SN + x) SM) goes to dst + x M + q SM
+                e = cudaSuccess;
+                for (int q = 0; q < P && e == cudaSuccess; ++q)
+                    e = cudaMemcpy2DAsync(dst + (size_t)q * SM * eb, M * eb, src + (size_t)q * blk * eb, SM * eb,
+                                          SM * eb, (size_t)SN, cudaMemcpyDeviceToDevice, st);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "unblock");
+        }
+    }
+    p->last_launches = launches;
     return FFT_OK;
 }
 
@@ -484,9 +620,12 @@ fft_status fft_plan_set_workspace(fft_plan p, void* ptr, size_t bytes) {
 static fft_status exec(fft_plan p, const void* in, void* out, bool inv) {
     fft_status s = check_ptrs(p, in, out, false);
     if (s != FFT_OK) return s;
-    if (p->nranks > 1) return fail(FFT_E_UNSUPPORTED, "distributed execution not built in this library");
     if (p->elems() == 0) return FFT_OK;
-    return p->rank == 1 ? run_1d(p, in, out, inv, p->stream) : run_2d(p, in, out, inv, p->stream);
+    // rank 1 on several ranks: the batch is sharded (each rank's plan holds its
+    // own rows), so the local schedule is the whole job -- no collective
+    if (p->rank == 1) return run_1d(p, in, out, inv, p->stream);
+    if (p->dist()) return run_dist_2d(p, in, out, inv ? 1 : 0, FFT_FILTER_NONE, 0.0, p->stream);
+    return run_2d(p, in, out, inv, p->stream);
 }
 
 fft_status fft_forward(fft_plan p, const void* in, void* out) { return exec(p, in, out, false); }
@@ -503,8 +642,8 @@ fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filt
     if ((filter == FFT_FILTER_IDEAL_LITERAL || filter == FFT_FILTER_IDEAL_LOWPASS) && !(param >= 0.0))
         return fail(FFT_E_INVALID_ARG, "ideal filter needs radius >= 0");
     if (real_in && in == out) return fail(FFT_E_INVALID_ARG, "real input cannot alias the complex output");
-    if (p->nranks > 1) return fail(FFT_E_UNSUPPORTED, "distributed execution not built in this library");
     if (p->elems() == 0) return FFT_OK;
+    if (p->dist()) return run_dist_2d(p, in, out, 2, filter, param, p->stream);
     return run_pipeline(p, in, out, filter, param, p->stream);
 }
 
@@ -514,7 +653,7 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
     if (!host_in || !host_out) return fail(FFT_E_INVALID_ARG, "null host pointer");
     if (direction == 0 && p->rank != 2) return fail(FFT_E_INVALID_ARG, "pipeline needs a rank-2 plan");
     if (direction < -1 || direction > 1) return fail(FFT_E_INVALID_ARG, "direction must be -1, 0 or +1");
-    if (p->nranks > 1) return fail(FFT_E_UNSUPPORTED, "host execution of a distributed plan");
+    if (p->dist()) return fail(FFT_E_UNSUPPORTED, "host execution of a distributed plan");
     const int64_t total = p->elems();
     if (total == 0) return FFT_OK;
     const bool real_in = direction == 0 && (p->flags & FFT_IN_REAL_F32);
@@ -594,16 +733,65 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
 }
 
 fft_status fft_nccl_unique_id(unsigned char id[128]) {
-    (void)id;
-    return fail(FFT_E_UNSUPPORTED, "NCCL support not built in this library");
+    if (!id) return fail(FFT_E_INVALID_ARG, "null id buffer");
+#ifdef B200FFT_WITH_NCCL
+    ncclUniqueId u;
+    ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) return fail(FFT_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    memcpy(id, &u, 128);
+    return FFT_OK;
+#else
+    return fail(FFT_E_UNSUPPORTED, "library built without NCCL");
+#endif
 }
 
 fft_status fft_plan_set_comm(fft_plan p, const unsigned char id[128], int nranks, int my_rank) {
-    (void)id;
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (nranks < 1 || my_rank < 0 || my_rank >= nranks) return fail(FFT_E_INVALID_ARG, "bad rank / nranks");
-    if (nranks == 1) return FFT_OK;
-    return fail(FFT_E_UNSUPPORTED, "NCCL support not built in this library");
+    if (p->comm) return fail(FFT_E_STATE, "plan already has a communicator");
+    if (p->virt > 1) return fail(FFT_E_STATE, "plan emulates virtual ranks");
+    if (p->rank == 2 && (p->n0 % nranks || p->n1 % nranks))
+        return fail(FFT_E_INVALID_SIZE, "2D sides must be divisible by the rank count");
+    if (!id) return fail(FFT_E_INVALID_ARG, "null unique id");
+    if (p->rank == 1) {  // batch-sharded: no collective on the data path
+        p->nranks = nranks;
+        p->my_rank = my_rank;
+        return FFT_OK;
+    }
+#ifdef B200FFT_WITH_NCCL
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclComm_t comm = nullptr;
+    ncclResult_t r = ncclCommInitRank(&comm, nranks, u, my_rank);
+    if (r != ncclSuccess) return fail(FFT_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    p->comm = comm;
+    p->nranks = nranks;
+    p->my_rank = my_rank;
+    if (p->ws_owned && p->ws) {  // slab-sized workspace from now on
+        cudaFree(p->ws);
+        p->ws = nullptr;
+        p->ws_bytes = 0;
+    }
+    return FFT_OK;
+#else
+    return fail(FFT_E_UNSUPPORTED, "library built without NCCL");
+#endif
+}
+
+fft_status fft_plan_set_virtual_ranks(fft_plan p, int nranks) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (p->rank != 2) return fail(FFT_E_INVALID_ARG, "virtual ranks apply to rank-2 plans");
+    if (p->comm) return fail(FFT_E_STATE, "plan has a communicator");
+    if (nranks < 1 || p->n0 % nranks || p->n1 % nranks)
+        return fail(FFT_E_INVALID_SIZE, "2D sides must be divisible by the rank count");
+    p->virt = nranks;
+    if (p->ws_owned && p->ws) {
+        cudaFree(p->ws);
+        p->ws = nullptr;
+        p->ws_bytes = 0;
+    }
+    return FFT_OK;
 }
 
 int fft_plan_last_launch_count(fft_plan p) { return p ? p->last_launches : 0; }
@@ -625,6 +813,9 @@ fft_status fft_plan_destroy(fft_plan p) {
         if (p->hstream[i]) cudaStreamDestroy(p->hstream[i]);
     }
     if (p->hev) cudaEventDestroy(p->hev);
+#ifdef B200FFT_WITH_NCCL
+    if (p->comm) ncclCommDestroy((ncclComm_t)p->comm);
+#endif
     e = cudaGetLastError();
     delete p;
     if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error at destroy");

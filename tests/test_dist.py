@@ -1,0 +1,199 @@
+"""Multi-rank paths.
+
+* GPU (-m gpu): the slab-decomposed 2D schedule of the library run as P
+  virtual ranks on one GPU (the same kernels, blocked layouts and column
+  offsets as the NCCL path; the all-to-alls become device copies), and the
+  NCCL path itself with a 1-rank communicator -- against the oracle.
+* CPU (gloo, world_size 2): the decomposition the library implements
+  (row slabs, blocked all-to-all, column slabs,
+  filter column offsets, scales), written out with numpy block moves and the
+  oracle's 1D transforms as the local steps, exchanged with
+  torch.distributed.all_to_all over gloo, must equal the oracle's full
+  pipeline.  This pins the index maps and the host-side schedule.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import fixtures
+import oracle
+
+torch = pytest.importorskip("torch")
+
+
+# ------------------------------------------------------------------ GPU
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_cs_0103001_b200 as b
+
+    b.load_library()
+    return b
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("N,M", [(64, 64), (256, 512), (2048, 2048)])
+def test_virtual_ranks_pipeline(P, N, M):
+    b = _lib()
+    f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=500 + P, dtype=np.complex64).reshape(N, M)
+    p = b.Plan((N, M))
+    p.set_virtual_ranks(P)
+    fd = torch.from_numpy(f).cuda()
+    od = torch.empty_like(fd)
+    p.filter_pipeline(fd, od, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(od.cpu().numpy(), oracle.gauss_pipeline(f, 0.1)) <= 1e-5
+    F = torch.empty_like(fd)
+    p.forward(fd, F)
+    g = torch.empty_like(fd)
+    p.inverse(fd, g)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(F.cpu().numpy(), oracle.fft2d(f)) <= 1e-5
+    assert oracle.rel_l2(g.cpu().numpy(), oracle.ifft2d(f)) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_virtual_ranks_c4_shape_real_input():
+    b = _lib()
+    N = 8192
+    f = fixtures.complex_input(N * N, fixtures.UNIFORM, seed=4).reshape(N, N)
+    p = b.Plan((N, N))
+    p.set_virtual_ranks(8)
+    fd = torch.from_numpy(f).cuda()
+    od = torch.empty_like(fd)
+    p.filter_pipeline(fd, od, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(od.cpu().numpy(), oracle.gauss_pipeline(f, 0.1)) <= 1e-5
+    img = fixtures.sky_image(512, 512, seed=3, nsrc=50)
+    q = b.Plan((512, 512), flags=b.IN_REAL_F32)
+    q.set_virtual_ranks(4)
+    o2 = torch.empty((512, 512), dtype=torch.complex64, device="cuda")
+    q.filter_pipeline(torch.from_numpy(img).cuda(), o2, b.FILTER_IDEAL_LITERAL, 200.0)
+    torch.cuda.synchronize()
+    u = np.arange(512)[:, None]
+    v = np.arange(512)[None, :]
+    H = np.where((u - 256) ** 2 + (v - 256) ** 2 <= 200.0 ** 2, 0.0, 1.0)
+    assert oracle.rel_l2(o2.cpu().numpy(), oracle.filter_pipeline(img.astype(complex), H)) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_nccl_single_rank_communicator():
+    """The NCCL data path (ncclSend/ncclRecv all-to-all) with one rank."""
+    b = _lib()
+    N = M = 512
+    f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=77).reshape(N, M)
+    p = b.Plan((N, M))
+    p.set_comm(b.nccl_unique_id(), 1, 0)
+    fd = torch.from_numpy(f).cuda()
+    od = torch.empty_like(fd)
+    p.filter_pipeline(fd, od, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(od.cpu().numpy(), oracle.gauss_pipeline(f, 0.1)) <= 1e-5
+    p.destroy()
+
+
+# ------------------------------------------------------- CPU (gloo, 2 ranks)
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rows_blocked(a, SM):
+    """k_rows' blocked store: slab [SN][M] -> blocks q of [SN][SM] (peer q's columns)."""
+    SN, M = a.shape
+    return np.ascontiguousarray(a.reshape(SN, M // SM, SM).transpose(1, 0, 2))  # [q][SN][SM]
+
+
+def _unblock(blocks):
+    """k_rows' blocked load: blocks [q][SN][SM] -> slab [SN][M]."""
+    P, SN, SM = blocks.shape
+    return np.ascontiguousarray(blocks.transpose(1, 0, 2).reshape(SN, P * SM))
+
+
+def _a2a(dist, blocks):
+    """All-to-all of blocks[q] -> rank q as point-to-point pairs (the library
+    issues the same per-peer ncclSend/ncclRecv inside one NCCL group; gloo
+    has no alltoall)."""
+    send = torch.from_numpy(np.ascontiguousarray(blocks))
+    recv = torch.empty_like(send)
+    me = dist.get_rank()
+    reqs = []
+    for q in range(dist.get_world_size()):
+        if q == me:
+            recv[q].copy_(send[q])
+        else:
+            reqs.append(dist.isend(send[q].contiguous(), q))
+            reqs.append(dist.irecv(recv[q], q))
+    for r in reqs:
+        r.wait()
+    return recv.numpy()
+
+
+def _worker(rank, world, port, N, M, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        P = world
+        SN, SM = N // P, M // P
+        f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=11, dtype=np.complex128).reshape(N, M)
+        slab = f[rank * SN:(rank + 1) * SN]
+        # 1. rows: unnormalised forward (M * the paper's 1/M DFT), blocked store
+        rows = np.stack([oracle.fft(r) * M for r in slab])
+        recv = _a2a(dist, _rows_blocked(rows, SM))  # [p][SN][SM] = column slab [N][SM]
+        cs = recv.reshape(N, SM)
+        # 2. columns: forward (1/N) -> * H(u, v + r SM) / M ... the library's
+        #    combined scale H/(N M) on the unnormalised transforms
+        H = oracle.gauss_filter(N, M, 0.1)[:, rank * SM:(rank + 1) * SM]
+        colf = np.stack([oracle.fft(cs[:, j]) for j in range(SM)], axis=1)  # (1/N) sum
+        colf *= H / M  # eq5's 1/N is in oracle.fft; the 2D-IDFT's 1/M here
+        coli = np.stack([oracle.ifft(colf[:, j]) for j in range(SM)], axis=1)
+        back = _a2a(dist, coli.reshape(P, SN, SM))  # blocks by source rank
+        # 3. rows inverse (unscaled) from the blocked layout
+        out = np.stack([oracle.ifft(r) for r in _unblock(back)])
+        ref = oracle.gauss_pipeline(f, 0.1)[rank * SN:(rank + 1) * SN]
+        q.put((rank, oracle.rel_l2(out, ref)))
+    except Exception as exc:  # report instead of hanging the parent
+        q.put((rank, f"error: {exc!r}"))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N,M", [(16, 16), (64, 32)])
+def test_gloo_two_rank_slab_schedule(N, M):
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, N, M, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=60) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[0] <= 1e-13 and res[1] <= 1e-13, res
+
+
+def test_block_layout_roundtrip():
+    a = np.arange(4 * 16).reshape(4, 16)
+    blocks = _rows_blocked(a, 4)
+    assert blocks.shape == (4, 4, 4)
+    assert np.array_equal(blocks[2], a[:, 8:12])
+    assert np.array_equal(_unblock(blocks), a)
+    # the library's flat map: element (row, v) at ((v >> sh) * SN + row) << sh | (v & (SM-1))
+    SN, SM, sh = 4, 4, 2
+    flat = blocks.ravel()
+    for row in range(SN):
+        for v in range(16):
+            assert flat[(((v >> sh) * SN + row) << sh) | (v & (SM - 1))] == a[row, v]
