@@ -114,7 +114,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(ClusterCfg<T, N1, N2
     const int k2 = c * G::WB + tb;
     Cx* lineb = smem + tb * G::LSB;
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[FB::pos_in(m)] = lineb[pad16(lb + G::TPB * m)];
+    for (int m = 0; m < E; ++m) v[FB::pos_in(m)] = lineb[FB::bpos(lb, m)];
     FB::run(v, lineb, lb, twb);
 #pragma unroll
     for (int m = 0; m < E; ++m) {
@@ -232,13 +232,298 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(ClusterCfg<T, N1, N2
     const int k2 = c * G::WB + tb;
     Cx* lineb = rx + tb * G::LSB;
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[FB::pos_in(m)] = lineb[pad16(lb + G::TPB * m)];
+    for (int m = 0; m < E; ++m) v[FB::pos_in(m)] = lineb[FB::bpos(lb, m)];
     FB::run(v, lineb, lb, twb);
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const int k1 = lb + G::TPB * m;
         dst[k2 + (int64_t)N2 * k1] = cscale(v[FB::pos_out(m)], scale);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Variant 3: the transpose as TMA bulk copies.  After (A) every CTA writes its
+// outputs into its own smem grouped by owner (one 16 x 16 chunk per peer,
+// XOR-swizzled so the owner reads it conflict-free), and 16 threads each issue
+// one cp.async.bulk shared::cta -> shared::cluster copy of a whole chunk,
+// completing on the owner's mbarrier.  Far fewer DSMEM transactions than one
+// store per element.  Specialised to WA = WB = TPA = TPB = 16 (N1 = N2 = 256,
+// C = 16, E = 16, 256 threads).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void bulk_s2s(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                         uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            dst_cluster),
+        "r"(src_cta), "r"(bytes), "r"(bar_cluster)
+        : "memory");
+}
+
+template <typename T, int MINB, bool INV>
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, MINB)
+    k_cluster3(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, int64_t batch, T scale,
+               const cpx<T>* __restrict__ tw4, const cpx<T>* __restrict__ twa, const cpx<T>* __restrict__ twb) {
+    constexpr int N1 = 256, N2 = 256, C = 16, E = 16;
+    using Cx = cpx<T>;
+    using G = ClusterCfg<T, N1, N2, C, E>;
+    static_assert(G::WA == 16 && G::WB == 16 && G::TPA == 16 && G::TPB == 16 && G::NT == 256, "shape");
+    using FA = LineFFT<T, N2, E, INV>;
+    using FB = LineFFT<T, N1, E, INV>;
+    constexpr int64_t N = (int64_t)N1 * N2;
+    constexpr uint32_t CHUNK = 256 * sizeof(Cx);            // 16 x 16 elements per peer
+    constexpr size_t A_BYTES = sizeof(Cx) * G::WA * G::LSA;  // >= 16 chunks
+    static_assert(A_BYTES >= 16 * CHUNK, "send chunks must fit in the phase-A buffer");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Cx* bufa = reinterpret_cast<Cx*>(smem_raw);
+    Cx* rx = reinterpret_cast<Cx*>(smem_raw + A_BYTES);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + A_BYTES + 16 * CHUNK);
+    const uint32_t bar_s = smem_u32(bar);
+    namespace cg = cooperative_groups;
+    const int c = (int)cg::this_cluster().block_rank();
+    const int64_t b = (int64_t)blockIdx.x / C;
+    const int tid = threadIdx.x;
+    const Cx* src = in + b * N;
+    Cx* dst = out + b * N;
+
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_s), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s), "r"(16 * CHUNK)
+                     : "memory");
+    }
+    cluster_arrive_relaxed();
+
+    // ---- (A) columns n1 = 16 c + t, elements n2 = la + 16 m --------------
+    const int t = tid & 15, la = tid >> 4;
+    const int n1 = c * 16 + t;
+    Cx v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[FA::pos_in(m)] = src[n1 + (int64_t)N1 * (la + 16 * m)];
+    FA::run(v, bufa + t * G::LSA, la, twa);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k2 = la + 16 * m;
+        v[FA::pos_out(m)] = cmul_dir<INV>(v[FA::pos_out(m)], __ldg(tw4 + (int64_t)k2 * N1 + n1));
+    }
+    __syncthreads();  // every thread is done reading bufa
+    // element k2 = la + 16 m belongs to owner m, row k2l = la: chunk m, swizzled
+#pragma unroll
+    for (int m = 0; m < E; ++m) bufa[m * 256 + la * 16 + (t ^ la)] = v[FA::pos_out(m)];
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    cluster_wait_acquire();  // every peer's mbarrier is initialised
+    if (tid < 16) {
+        const uint32_t q = (uint32_t)tid;
+        const uint32_t dst_s = mapa_u32(smem_u32(rx) + (uint32_t)c * CHUNK, q);
+        bulk_s2s(dst_s, smem_u32(bufa) + q * CHUNK, CHUNK, mapa_u32(bar_s, q));
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // bufa reusable
+    }
+    // ---- (B) rows k2 = 16 c + tb once the 16 chunks have landed -------------
+    mbar_wait_parity_cluster(bar_s, 0);
+    __syncthreads();  // the bulk reads of bufa are complete (tid < 16 waited)
+    const int tb = tid & 15, lb = tid >> 4;
+    const int k2 = c * 16 + tb;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[FB::pos_in(m)] = rx[m * 256 + tb * 16 + (lb ^ tb)];
+    Cx* lineb = bufa + tb * G::LSB;
+    FB::run(v, lineb, lb, twb);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k1 = lb + 16 * m;
+        dst[k2 + (int64_t)N2 * k1] = cscale(v[FB::pos_out(m)], scale);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The same four-step split as two cluster-free kernels that exchange through
+// an L2-resident scratch (the batch is processed in chunks small enough that
+// Y never leaves L2): k_step_a does (A)+(T) for WA columns and stores
+// Y[k2][n1] (row k2 of Y = the input of (B)); k_step_b does (B) for WB rows.
+// ---------------------------------------------------------------------------
+template <typename T, int N1, int N2, int WA, int E, int MINB, bool INV>
+__global__ void __launch_bounds__(WA*(N2 / E), MINB)
+    k_step_a(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ y, const cpx<T>* __restrict__ tw4,
+             const cpx<T>* __restrict__ twa) {
+    using Cx = cpx<T>;
+    using FA = LineFFT<T, N2, E, INV>;
+    constexpr int TPA = N2 / E, LSA = pad16c(N2) + 1;
+    constexpr int64_t N = (int64_t)N1 * N2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Cx* smem = reinterpret_cast<Cx*>(smem_raw);
+    const int64_t b = (int64_t)blockIdx.x / (N1 / WA);
+    const int c = (int)(blockIdx.x % (N1 / WA));
+    const int tid = threadIdx.x;
+    const int t = tid % WA, la = tid / WA;
+    const int n1 = c * WA + t;
+    const Cx* src = in + b * N;
+    Cx* dst = y + b * N;
+    Cx v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[FA::pos_in(m)] = src[n1 + (int64_t)N1 * (la + TPA * m)];
+    FA::run(v, smem + t * LSA, la, twa);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k2 = la + TPA * m;
+        dst[(int64_t)k2 * N1 + n1] = cmul_dir<INV>(v[FA::pos_out(m)], __ldg(tw4 + (int64_t)k2 * N1 + n1));
+    }
+}
+
+template <typename T, int N1, int N2, int WB, int E, int MINB, bool INV>
+__global__ void __launch_bounds__(WB*(N1 / E), MINB)
+    k_step_b(const cpx<T>* __restrict__ y, cpx<T>* __restrict__ out, T scale, const cpx<T>* __restrict__ twb) {
+    using Cx = cpx<T>;
+    using FB = LineFFT<T, N1, E, INV>;
+    constexpr int TPB = N1 / E, LSB = pad16c(N1) + 1;
+    constexpr int64_t N = (int64_t)N1 * N2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Cx* smem = reinterpret_cast<Cx*>(smem_raw);
+    const int64_t b = (int64_t)blockIdx.x / (N2 / WB);
+    const int c = (int)(blockIdx.x % (N2 / WB));
+    const int tid = threadIdx.x;
+    // rows k2 are contiguous in y: lane-fastest mapping for coalesced loads
+    const int tb = tid / TPB, lb = tid % TPB;
+    const int k2 = c * WB + tb;
+    const Cx* src = y + b * N + (int64_t)k2 * N1;
+    Cx v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[FB::pos_in(m)] = src[lb + TPB * m];
+    Cx* line = smem + tb * LSB;
+    FB::run(v, line, lb, twb);
+    // X[k2 + N2 k1]: stage through smem so that consecutive threads store
+    // consecutive k2 (WB-element runs)
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) line[FB::bpos(lb, m)] = cscale(v[FB::pos_out(m)], scale);
+    __syncthreads();
+    Cx* dst = out + b * N + c * WB;
+    for (int idx = tid; idx < WB * N1; idx += WB * TPB) {
+        const int l = idx % WB, k1 = idx / WB;
+        dst[(int64_t)N2 * k1 + l] = smem[l * LSB + pad16(k1)];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent single-kernel form of the two steps: CTAs take tasks from a
+// global ticket in the order A(0..Wr-1), B(0), A(Wr), B(1), A(Wr+1), ...,
+// where A(b) / B(b) are the 16 column / 16 row tasks of transform b.  Y(b)
+// lives in slot b mod Wr of a scratch ring small enough to stay in L2
+// (Wr x 512 KiB), so HBM sees one read and one write per point.  B(b) waits
+// for the 16 A(b) tasks (counter), A(b) waits for B(b - Wr) to free its slot.
+// Every wait is on a task with a smaller ticket, held by a resident CTA
+// (the grid is sized to the resident capacity), so the schedule cannot
+// deadlock.  Streaming data uses evict-first loads/stores; Y uses .cg (L2).
+// ---------------------------------------------------------------------------
+struct FusedCtl {
+    int* ticket;   // [1]
+    int* done_a;   // [batch]
+    int* done_b;   // [batch]
+};
+
+__device__ __forceinline__ void spin_until_geq(const int* p, int v) {
+    int cur;
+    while (true) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(cur) : "l"(p) : "memory");
+        if (cur >= v) break;
+        __nanosleep(64);
+    }
+}
+
+template <typename T, int E, bool INV>
+__global__ void __launch_bounds__(256, 4)
+    k_fused_ab(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, cpx<T>* __restrict__ ring, int64_t batch,
+               int wr, T scale, const cpx<T>* __restrict__ tw4, const cpx<T>* __restrict__ twa,
+               const cpx<T>* __restrict__ twb, FusedCtl ctl) {
+    constexpr int N1 = 256, N2 = 256, W = 16, TP = 16, LS = pad16c(256) + 1;
+    static_assert(E == 16, "256 threads = 16 lines x 16 threads");
+    using Cx = cpx<T>;
+    using F = LineFFT<T, 256, E, INV>;
+    constexpr int64_t N = (int64_t)N1 * N2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Cx* smem = reinterpret_cast<Cx*>(smem_raw);
+    __shared__ int s_ticket;
+    const int tid = threadIdx.x;
+    const int64_t units = 2 * batch;
+    const int64_t wq = batch < wr ? batch : wr;
+    // dynamic tickets (measured faster than a static round-robin, which turns
+    // CTA speed differences into dependency waits)
+    while (true) {
+        if (tid == 0) s_ticket = atomicAdd(ctl.ticket, 1);
+        __syncthreads();
+        const int64_t tk = s_ticket;
+        __syncthreads();
+        if (tk >= units * 16) break;
+        const int64_t u = tk / 16;
+        const int part = (int)(tk % 16);
+        bool is_a;
+        int64_t b;
+        if (u < wq) {
+            is_a = true;
+            b = u;
+        } else {
+            const int64_t v = u - wq;
+            if (v < 2 * (batch - wq)) {
+                is_a = (v & 1) != 0;
+                b = is_a ? v / 2 + wq : v / 2;
+            } else {
+                is_a = false;
+                b = (batch - wq) + (v - 2 * (batch - wq));
+            }
+        }
+        Cx* y = ring + (b % wr) * N;
+        if (is_a) {
+            if (b >= wr) {
+                if (tid == 0) spin_until_geq(ctl.done_b + (b - wr), 16);
+                __syncthreads();
+            }
+            const int t = tid % W, la = tid / W;
+            const int n1 = part * W + t;
+            const Cx* src = in + b * N;
+            Cx v[E];
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[F::pos_in(m)] = __ldcs(src + n1 + (int64_t)N1 * (la + TP * m));
+            F::run(v, smem + t * LS, la, twa);
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int k2 = la + TP * m;
+                __stcg(y + (int64_t)k2 * N1 + n1, cmul_dir<INV>(v[F::pos_out(m)], __ldg(tw4 + (int64_t)k2 * N1 + n1)));
+            }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicAdd(ctl.done_a + b, 1);
+        } else {
+            if (tid == 0) spin_until_geq(ctl.done_a + b, 16);
+            __syncthreads();
+            const int tb = tid / TP, lb = tid % TP;
+            const int k2 = part * W + tb;
+            const Cx* src = y + (int64_t)k2 * N1;
+            Cx v[E];
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[F::pos_in(m)] = __ldcg(src + lb + TP * m);
+            Cx* line = smem + tb * LS;
+            F::run(v, line, lb, twb);
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < E; ++m) line[F::bpos(lb, m)] = cscale(v[F::pos_out(m)], scale);
+            __syncthreads();
+            Cx* dst = out + b * N + part * W;
+            for (int idx = tid; idx < W * N1; idx += 256) {
+                const int l = idx % W, k1 = idx / W;
+                __stcs(dst + (int64_t)N2 * k1 + l, smem[l * LS + pad16(k1)]);
+            }
+            __syncthreads();  // all reads of this Y slot are done before the release
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(ctl.done_b + b, 1);
+            }
+        }
+    }
+}
+
+template <typename T>
+constexpr size_t cluster3_smem() {
+    using G = ClusterCfg<T, 256, 256, 16, 16>;
+    return sizeof(cpx<T>) * G::WA * G::LSA + 16 * 256 * sizeof(cpx<T>) + 16;
 }
 
 }  // namespace b200fft

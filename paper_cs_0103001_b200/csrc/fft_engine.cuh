@@ -63,6 +63,9 @@ struct LineFFT {
         }
     }
 
+    // Padded smem indices.  pad16(x + c) = pad16(x) + c + c/16 whenever c is a
+    // multiple of 16, so one pad16 per butterfly and compile-time offsets
+    // (folded into the LDS/STS immediates) cover every element.
     template <int s>
     __device__ __forceinline__ static void write_out(C* line, const C* v, int lt) {
         constexpr int rho = radix_at(R, s), Ns = span_at(R, s), nb = E / rho;
@@ -71,20 +74,43 @@ struct LineFFT {
             const int j = lt + b * TPL;
             const int k = j & (Ns - 1);
             const int base = (j - k) * rho + k;
+            if constexpr (Ns % 16 == 0) {
+                const int pb = pad16(base);
 #pragma unroll
-            for (int q = 0; q < rho; ++q) line[pad16(base + q * Ns)] = v[b * rho + q];
+                for (int q = 0; q < rho; ++q) line[pb + q * (Ns + Ns / 16)] = v[b * rho + q];
+            } else if constexpr (Ns == 1 && rho == 16) {
+                const int pb = 17 * j;  // base = 16 j: pad16(16 j + q) = 17 j + q
+#pragma unroll
+                for (int q = 0; q < rho; ++q) line[pb + q] = v[b * rho + q];
+            } else {
+#pragma unroll
+                for (int q = 0; q < rho; ++q) line[pad16(base + q * Ns)] = v[b * rho + q];
+            }
         }
     }
 
     template <int s>
     __device__ __forceinline__ static void read_in(const C* line, C* v, int lt) {
         constexpr int rho = radix_at(R, s), nb = E / rho;
+        constexpr int st = R / rho;
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
             const int j = lt + b * TPL;
+            if constexpr (st % 16 == 0) {
+                const int pj = pad16(j);
 #pragma unroll
-            for (int r = 0; r < rho; ++r) v[b * rho + r] = line[pad16(j + r * (R / rho))];
+                for (int r = 0; r < rho; ++r) v[b * rho + r] = line[pj + r * (st + st / 16)];
+            } else {
+#pragma unroll
+                for (int r = 0; r < rho; ++r) v[b * rho + r] = line[pad16(j + r * st)];
+            }
         }
+    }
+
+    // padded index of boundary element m (element lt + TPL m of the line)
+    __device__ __forceinline__ static int bpos(int lt, int m) {
+        if constexpr (TPL % 16 == 0) return pad16(lt) + m * (TPL + TPL / 16);
+        else return pad16(lt + TPL * m);
     }
 
     template <int s>
@@ -133,21 +159,39 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_
     const bool valid = row < batch;
     C v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int64_t idx = row_index(row, lt + F::TPL * m, R, batch, in_sh);
-        if constexpr (REAL_IN) {
-            const float* in = reinterpret_cast<const float*>(in_);
-            v[F::pos_in(m)] = valid ? mk((T)__ldg(in + idx), (T)0) : mk((T)0, (T)0);
+    for (int m = 0; m < E; ++m) v[m] = mk((T)0, (T)0);
+    if (valid) {
+        if (in_sh < 0) {  // natural rows: one base address, compile-time offsets
+            const int64_t base = row * R + lt;
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                if constexpr (REAL_IN)
+                    v[F::pos_in(m)] = mk((T)__ldg(reinterpret_cast<const float*>(in_) + base + F::TPL * m), (T)0);
+                else
+                    v[F::pos_in(m)] = reinterpret_cast<const C*>(in_)[base + F::TPL * m];
+            }
         } else {
-            const C* in = reinterpret_cast<const C*>(in_);
-            v[F::pos_in(m)] = valid ? in[idx] : mk((T)0, (T)0);
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int64_t idx = row_index(row, lt + F::TPL * m, R, batch, in_sh);
+                if constexpr (REAL_IN)
+                    v[F::pos_in(m)] = mk((T)__ldg(reinterpret_cast<const float*>(in_) + idx), (T)0);
+                else
+                    v[F::pos_in(m)] = reinterpret_cast<const C*>(in_)[idx];
+            }
         }
     }
     F::run(v, smem + t * F::LS, lt, tw);
     if (valid) {
+        if (out_sh < 0) {
+            C* o = out + row * R + lt;
 #pragma unroll
-        for (int m = 0; m < E; ++m)
-            out[row_index(row, lt + F::TPL * m, R, batch, out_sh)] = cscale(v[F::pos_out(m)], scale);
+            for (int m = 0; m < E; ++m) o[F::TPL * m] = cscale(v[F::pos_out(m)], scale);
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                out[row_index(row, lt + F::TPL * m, R, batch, out_sh)] = cscale(v[F::pos_out(m)], scale);
+        }
     }
 }
 
@@ -224,7 +268,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
     C* line = smem + t * LSC;
     C v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[pad16(lt + F::TPL * m)];
+    for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
     F::run(v, line, lt, tw);
     if constexpr (MODE == 2) {
         C w[E];
@@ -238,11 +282,11 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
         FI::run(w, line, lt, tw);
         __syncthreads();
 #pragma unroll
-        for (int m = 0; m < E; ++m) line[pad16(lt + F::TPL * m)] = w[FI::pos_out(m)];
+        for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = w[FI::pos_out(m)];
     } else {
         __syncthreads();
 #pragma unroll
-        for (int m = 0; m < E; ++m) line[pad16(lt + F::TPL * m)] = cscale(v[F::pos_out(m)], scale);
+        for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = cscale(v[F::pos_out(m)], scale);
     }
     __syncthreads();
     for (int idx = tid; idx < W * R; idx += NT) {
@@ -298,11 +342,11 @@ __global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ i
     C* line = smem + t * F::LS;
     C v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[pad16(lt + F::TPL * m)];
+    for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
     F::run(v, line, lt, tw);
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < E; ++m) line[pad16(lt + F::TPL * m)] = cscale(v[F::pos_out(m)], scale);
+    for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = cscale(v[F::pos_out(m)], scale);
     __syncthreads();
     if (Ns >= W) {
         for (int idx = tid; idx < W * R; idx += NT) {

@@ -48,6 +48,103 @@ cudaError_t cluster2_t(const void* in, void* out, int64_t batch, double scale, c
     return cudaGetLastError();
 }
 
+template <typename T, int MINB, bool INV>
+cudaError_t cluster3_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                       cudaStream_t st) {
+    constexpr size_t smem = cluster3_smem<T>();
+    auto kern = k_cluster3<T, MINB, INV>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    if (batch <= 0) return cudaSuccess;
+    const cpx<T>* t = reinterpret_cast<const cpx<T>*>(tw);
+    kern<<<(unsigned)(batch * 16), 256, smem, st>>>(reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<cpx<T>*>(out),
+                                                   batch, (T)scale, reinterpret_cast<const cpx<T>*>(tw4),
+                                                   t + tw_base(256), t + tw_base(256));
+    return cudaGetLastError();
+}
+
+// two cluster-free kernels per chunk of transforms; Y stays in L2 between them
+template <typename T, int WA, int WB, int E, int MINB, bool INV>
+cudaError_t step_ab_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                      cudaStream_t st) {
+    constexpr int N1 = 256, N2 = 256;
+    constexpr size_t smem_a = sizeof(cpx<T>) * WA * (pad16c(N2) + 1);
+    constexpr size_t smem_b = sizeof(cpx<T>) * WB * (pad16c(N1) + 1);
+    auto ka = k_step_a<T, N1, N2, WA, E, MINB, INV>;
+    auto kb = k_step_b<T, N1, N2, WB, E, MINB, INV>;
+    static bool attr = false;
+    static void* scratch = nullptr;
+    static int64_t chunk = 0;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
+        const char* cs = getenv("B200FFT_STEP_CHUNK");
+        chunk = cs ? atoll(cs) : 64;
+        if (e == cudaSuccess) e = cudaMalloc(&scratch, (size_t)chunk * N1 * N2 * sizeof(cpx<T>));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const cpx<T>* t = reinterpret_cast<const cpx<T>*>(tw);
+    const cpx<T>* x = reinterpret_cast<const cpx<T>*>(in);
+    cpx<T>* o = reinterpret_cast<cpx<T>*>(out);
+    cpx<T>* y = reinterpret_cast<cpx<T>*>(scratch);
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+        const int64_t nb = batch - b0 < chunk ? batch - b0 : chunk;
+        ka<<<(unsigned)(nb * (N1 / WA)), WA * (N2 / E), smem_a, st>>>(x + b0 * N1 * N2, y,
+                                                                    reinterpret_cast<const cpx<T>*>(tw4),
+                                                                    t + tw_base(N2));
+        kb<<<(unsigned)(nb * (N2 / WB)), WB * (N1 / E), smem_b, st>>>(y, o + b0 * N1 * N2, (T)scale, t + tw_base(N1));
+    }
+    return cudaGetLastError();
+}
+
+template <typename T, bool INV>
+cudaError_t fused_ab_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                       cudaStream_t st) {
+    constexpr size_t smem = sizeof(cpx<T>) * 16 * (pad16c(256) + 1);
+    auto k = k_fused_ab<T, 16, INV>;
+    static bool attr = false;
+    static void* ring = nullptr;
+    static int* ctl = nullptr;
+    static int64_t ctl_n = 0;
+    static int wr = 0, grid = 0;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const char* rs = getenv("B200FFT_RING");
+        wr = rs ? atoi(rs) : 32;
+        if (e == cudaSuccess) e = cudaMalloc(&ring, (size_t)wr * 65536 * sizeof(cpx<T>));
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
+        if (e != cudaSuccess) return e;
+        grid = sms * occ;
+        attr = true;
+    }
+    if (batch <= 0) return cudaSuccess;
+    if (ctl_n < 1 + 2 * batch) {
+        if (ctl) cudaFree(ctl);
+        cudaError_t e = cudaMalloc(&ctl, sizeof(int) * (1 + 2 * batch));
+        if (e != cudaSuccess) return e;
+        ctl_n = 1 + 2 * batch;
+    }
+    cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(int) * (1 + 2 * batch), st);
+    if (e != cudaSuccess) return e;
+    FusedCtl c{ctl, ctl + 1, ctl + 1 + batch};
+    const cpx<T>* t = reinterpret_cast<const cpx<T>*>(tw);
+    const int64_t tasks = 32 * batch;
+    const int g = (int)(tasks < grid ? tasks : grid);
+    k<<<g, 256, smem, st>>>(reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<cpx<T>*>(out),
+                            reinterpret_cast<cpx<T>*>(ring), batch, wr, (T)scale,
+                            reinterpret_cast<const cpx<T>*>(tw4), t + tw_base(256), t + tw_base(256), c);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2) {
@@ -78,6 +175,10 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 7: return cluster2_t<float, 256, 256, 8, 16, 1, INV>(in, out, batch, scale, tw4, tw, st);
         case 10: return cluster2_t<float, 256, 256, 16, 16, 4, INV, true>(in, out, batch, scale, tw4, tw, st);
         case 11: return cluster2_t<float, 256, 256, 8, 32, 2, INV, true>(in, out, batch, scale, tw4, tw, st);
+        case 12: return cluster3_t<float, 3, INV>(in, out, batch, scale, tw4, tw, st);
+        case 13: return step_ab_t<float, 16, 16, 16, 4, INV>(in, out, batch, scale, tw4, tw, st);
+        case 14: return step_ab_t<float, 32, 32, 16, 2, INV>(in, out, batch, scale, tw4, tw, st);
+        case 15: return fused_ab_t<float, INV>(in, out, batch, scale, tw4, tw, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -3,19 +3,33 @@
 #include "fft_engine.cuh"
 #include "launch.h"
 
+#include <cstdlib>
+
 namespace b200fft {
 
 namespace {
 
 template <typename T> constexpr int cols_budget() { return sizeof(T) == 4 ? 16384 : 8192; }
 
-template <typename T, int R, int MODE>
+template <typename T, int R> constexpr int cols_e() { return R < 32 ? (R < 16 ? R : 16) : 32; }
+template <typename T, int R> constexpr int cols_w() {
+    return cols_budget<T>() / R > 16 ? 16 : (cols_budget<T>() / R < 2 ? 2 : cols_budget<T>() / R);
+}
+
+// tuning knob (B200FFT_COLS_VARIANT, read once): alternative tile widths /
+// registers per thread for the C3 and C4 column lengths
+int cols_variant() {
+    static int v = [] {
+        const char* e = getenv("B200FFT_COLS_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <typename T, int R, int MODE, int W = cols_w<T, R>(), int E = cols_e<T, R>()>
 cudaError_t cols_t(const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
                    const FilterArgs& f, cudaStream_t st) {
-    constexpr int E = R < 32 ? (R < 16 ? R : 16) : 32;
     constexpr int TPL = R / E;
-    constexpr int W0 = cols_budget<T>() / R;
-    constexpr int W = W0 > 16 ? 16 : (W0 < 2 ? 2 : W0);
     using F = LineFFT<T, R, E, MODE == 1>;
     constexpr size_t smem = sizeof(cpx<T>) * W * cols_ls<T, R, W>();
     static_assert(smem <= 227 * 1024, "column tile exceeds shared memory");
@@ -41,10 +55,23 @@ cudaError_t cols_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg
     case r: return cols_t<T, r, MODE>(in, out, S, nimg, scale, tw, f, st);
         B200_COLS_CASE(1) B200_COLS_CASE(2) B200_COLS_CASE(4) B200_COLS_CASE(8) B200_COLS_CASE(16)
         B200_COLS_CASE(32) B200_COLS_CASE(64) B200_COLS_CASE(128) B200_COLS_CASE(256)
-        B200_COLS_CASE(512) B200_COLS_CASE(1024) B200_COLS_CASE(2048) B200_COLS_CASE(4096)
+        B200_COLS_CASE(512) B200_COLS_CASE(1024) B200_COLS_CASE(4096)
 #undef B200_COLS_CASE
+        case 2048:
+            if constexpr (sizeof(T) == 4) {
+                switch (cols_variant()) {
+                    case 1: return cols_t<T, 2048, MODE, 4, 32>(in, out, S, nimg, scale, tw, f, st);
+                    case 2: return cols_t<T, 2048, MODE, 4, 16>(in, out, S, nimg, scale, tw, f, st);
+                    case 3: return cols_t<T, 2048, MODE, 8, 16>(in, out, S, nimg, scale, tw, f, st);
+                    default: break;
+                }
+            }
+            return cols_t<T, 2048, MODE>(in, out, S, nimg, scale, tw, f, st);
         case 8192:
-            if constexpr (sizeof(T) == 4) return cols_t<T, 8192, MODE>(in, out, S, nimg, scale, tw, f, st);
+            if constexpr (sizeof(T) == 4) {
+                if (cols_variant() == 2) return cols_t<T, 8192, MODE, 2, 16>(in, out, S, nimg, scale, tw, f, st);
+                return cols_t<T, 8192, MODE>(in, out, S, nimg, scale, tw, f, st);
+            }
             return cudaErrorInvalidValue;
         default: return cudaErrorInvalidValue;
     }
