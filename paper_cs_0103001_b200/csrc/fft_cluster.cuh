@@ -172,7 +172,14 @@ struct Cluster2Cfg {
     static constexpr uint32_t RX_BYTES = (uint32_t)(sizeof(cpx<T>) * G::WB * N1);  // payload per CTA
 };
 
-template <typename T, int N1, int N2, int C, int E, int MINB, bool INV, bool ALIAS = false>
+// v[F::pos_out(m)] for a runtime m (a select chain; m is warp-uniform)
+template <int M, int E, typename F, typename Cx>
+__device__ __forceinline__ Cx pick_out(const Cx* v, int m) {
+    if constexpr (M == E - 1) return v[F::pos_out(M)];
+    else return (m == M) ? v[F::pos_out(M)] : pick_out<M + 1, E, F>(v, m);
+}
+
+template <typename T, int N1, int N2, int C, int E, int MINB, bool INV, bool ALIAS = false, bool ROT = false>
 __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(ClusterCfg<T, N1, N2, C, E>::NT, MINB)
     k_cluster2(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, int64_t batch, T scale,
                const cpx<T>* __restrict__ tw4, const cpx<T>* __restrict__ twa, const cpx<T>* __restrict__ twb) {
@@ -219,12 +226,25 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(ClusterCfg<T, N1, N2
     cluster_wait_acquire();  // every peer's mbarrier is initialised
     // ---- transpose: st.async Y[n1][k2] into the owner's receive buffer ----
     const uint32_t rx_s = smem_u32(rx);
+    if constexpr (ROT) {
+        // rotate the send order by the CTA rank so that at every moment the
+        // 16 CTAs of the cluster target 16 different owners (no incast)
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int k2 = la + G::TPA * m;
-        const uint32_t owner = (uint32_t)(k2 / G::WB), line = (uint32_t)(k2 % G::WB);
-        const uint32_t laddr = rx_s + (uint32_t)sizeof(Cx) * (line * G::LSB + pad16(n1));
-        st_async_v2(mapa_u32(laddr, owner), v[FA::pos_out(m)], mapa_u32(bar_s, owner));
+        for (int mm = 0; mm < E; ++mm) {
+            const int m = (mm + c) & (E - 1);
+            const int k2 = la + G::TPA * m;
+            const uint32_t owner = (uint32_t)(k2 / G::WB), line = (uint32_t)(k2 % G::WB);
+            const uint32_t laddr = rx_s + (uint32_t)sizeof(Cx) * (line * G::LSB + pad16(n1));
+            st_async_v2(mapa_u32(laddr, owner), pick_out<0, E, FA>(v, m), mapa_u32(bar_s, owner));
+        }
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int k2 = la + G::TPA * m;
+            const uint32_t owner = (uint32_t)(k2 / G::WB), line = (uint32_t)(k2 % G::WB);
+            const uint32_t laddr = rx_s + (uint32_t)sizeof(Cx) * (line * G::LSB + pad16(n1));
+            st_async_v2(mapa_u32(laddr, owner), v[FA::pos_out(m)], mapa_u32(bar_s, owner));
+        }
     }
     // ---- (B) rows k2 = c WB + tb, once all RX_BYTES have landed -------------
     mbar_wait_parity_cluster(bar_s, 0);

@@ -27,12 +27,12 @@ cudaError_t cluster_t(const void* in, void* out, int64_t batch, double scale, co
     return cudaGetLastError();
 }
 
-template <typename T, int N1, int N2, int C, int E, int MINB, bool INV, bool ALIAS = false>
+template <typename T, int N1, int N2, int C, int E, int MINB, bool INV, bool ALIAS = false, bool ROT = false>
 cudaError_t cluster2_t(const void* in, void* out, int64_t batch, double scale, const void* tw4,
                        const void* tw, cudaStream_t st) {
     using G = ClusterCfg<T, N1, N2, C, E>;
     using H = Cluster2Cfg<T, N1, N2, C, E, ALIAS>;
-    auto kern = k_cluster2<T, N1, N2, C, E, MINB, INV, ALIAS>;
+    auto kern = k_cluster2<T, N1, N2, C, E, MINB, INV, ALIAS, ROT>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM_BYTES);
@@ -175,6 +175,8 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 7: return cluster2_t<float, 256, 256, 8, 16, 1, INV>(in, out, batch, scale, tw4, tw, st);
         case 10: return cluster2_t<float, 256, 256, 16, 16, 4, INV, true>(in, out, batch, scale, tw4, tw, st);
         case 11: return cluster2_t<float, 256, 256, 8, 32, 2, INV, true>(in, out, batch, scale, tw4, tw, st);
+        case 16: return cluster2_t<float, 256, 256, 16, 16, 4, INV, true, true>(in, out, batch, scale, tw4, tw, st);
+        case 17: return cluster2_t<float, 256, 256, 16, 16, 3, INV, false, true>(in, out, batch, scale, tw4, tw, st);
         case 12: return cluster3_t<float, 3, INV>(in, out, batch, scale, tw4, tw, st);
         case 13: return step_ab_t<float, 16, 16, 16, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 14: return step_ab_t<float, 32, 32, 16, 2, INV>(in, out, batch, scale, tw4, tw, st);

@@ -1,0 +1,96 @@
+// kernels_misc.cu -- the data-movement and twiddle kernels of the distributed
+// four-step 1D transform (BASELINE configs[4]):
+//   k_transpose : out[c][r] = in[r][c] for a batch of [R][Cn] matrices (the
+//                 all-to-all pack: the columns owned by rank q become the
+//                 contiguous block q), 32 x 32 tiles through padded smem,
+//                 coalesced on both sides.
+//   k_twiddle4  : Y[row][k2] *= W_N^{(row0 + row) k2} (the four-step twiddle,
+//                 step (T) of fft_cluster.cuh), W_N^x = A[x >> sh] * B[x & mask]
+//                 from two fp64-generated tables (x < N, no wrap).
+#include "fft_common.cuh"
+#include "launch.h"
+
+namespace b200fft {
+
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out,
+                                                   int64_t R, int64_t Cn) {
+    __shared__ cpx<T> tile[32][33];
+    const int64_t mat = blockIdx.z;
+    const cpx<T>* src = in + mat * R * Cn;
+    cpx<T>* dst = out + mat * R * Cn;
+    const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int64_t r = r0 + ty + i, c = c0 + tx;
+        if (r < R && c < Cn) tile[ty + i][tx] = src[r * Cn + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int64_t c = c0 + ty + i, r = r0 + tx;
+        if (r < R && c < Cn) dst[c * R + r] = tile[tx][ty + i];
+    }
+}
+
+template <typename T, bool INV>
+__global__ void __launch_bounds__(256) k_twiddle4(cpx<T>* __restrict__ y, int64_t rows, int64_t L, int64_t row0,
+                                                  const cpx<T>* __restrict__ ta, const cpx<T>* __restrict__ tb,
+                                                  int sh) {
+    const int64_t total = rows * L;
+    const int64_t mask = ((int64_t)1 << sh) - 1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / L, k2 = i - row * L;
+        const int64_t x = (row0 + row) * k2;
+        const cpx<T> w = cmul(__ldg(ta + (x >> sh)), __ldg(tb + (x & mask)));
+        y[i] = cmul_dir<INV>(y[i], w);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_transpose(int prec, const void* in, void* out, int64_t R, int64_t Cn, int64_t nmat,
+                             cudaStream_t st) {
+    if (R <= 0 || Cn <= 0 || nmat <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((Cn + 31) / 32), (unsigned)((R + 31) / 32), (unsigned)nmat);
+    if (prec == 0)
+        k_transpose<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out), R,
+                                                 Cn);
+    else
+        k_transpose<double><<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(in), reinterpret_cast<double2*>(out),
+                                                  R, Cn);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_twiddle4(int prec, bool inv, void* y, int64_t rows, int64_t L, int64_t row0, const void* ta,
+                            const void* tb, int sh, cudaStream_t st) {
+    const int64_t total = rows * L;
+    if (total <= 0) return cudaSuccess;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (prec == 0) {
+        if (inv)
+            k_twiddle4<float, true><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float2*>(y), rows, L, row0,
+                                                                     reinterpret_cast<const float2*>(ta),
+                                                                     reinterpret_cast<const float2*>(tb), sh);
+        else
+            k_twiddle4<float, false><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float2*>(y), rows, L, row0,
+                                                                      reinterpret_cast<const float2*>(ta),
+                                                                      reinterpret_cast<const float2*>(tb), sh);
+    } else {
+        if (inv)
+            k_twiddle4<double, true><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<double2*>(y), rows, L, row0,
+                                                                      reinterpret_cast<const double2*>(ta),
+                                                                      reinterpret_cast<const double2*>(tb), sh);
+        else
+            k_twiddle4<double, false><<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<double2*>(y), rows, L, row0,
+                                                                       reinterpret_cast<const double2*>(ta),
+                                                                       reinterpret_cast<const double2*>(tb), sh);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace b200fft

@@ -31,6 +31,14 @@ cudaError_t launch_pass(int prec, bool inv, int64_t R, const void* in, void* out
                         int64_t Ns, int64_t batch, double scale, const void* tw, const void* pa,
                         const void* pb, int klo_sh, cudaStream_t st);
 
+// Distributed four-step helpers (kernels_misc.cu): batched transpose
+// out[c][r] = in[r][c] of nmat [R][Cn] matrices; four-step twiddle
+// y[row][k2] *= W_N^{(row0 + row) k2} with W_N^x = ta[x >> sh] * tb[x & mask].
+cudaError_t launch_transpose(int prec, const void* in, void* out, int64_t R, int64_t Cn, int64_t nmat,
+                             cudaStream_t st);
+cudaError_t launch_twiddle4(int prec, bool inv, void* y, int64_t rows, int64_t L, int64_t row0, const void* ta,
+                            const void* tb, int sh, cudaStream_t st);
+
 // One-pass cluster FFT (fft_cluster.cuh): n = n1 * n2 in one thread-block
 // cluster per transform.  tw4: W_n^{n1 k2} laid out [k2][n1].
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2);

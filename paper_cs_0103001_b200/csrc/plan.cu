@@ -155,13 +155,22 @@ struct fft_plan_s {
     void* comm = nullptr;  // ncclComm_t owned by the plan
     int virt = 1;          // virtual ranks emulated on this GPU (tests), 1 = off
     cudaEvent_t dev_ev = nullptr;
+    // distributed four-step 1D (one transform of n = fs1 * fs2 over the ranks)
+    int64_t fs1 = 0, fs2 = 0;
+    fft_plan_s* sub_a = nullptr;  // length fs2, batch fs1 / P (step A)
+    fft_plan_s* sub_b = nullptr;  // length fs1, batch fs2 / P (step B)
+    void* fta = nullptr;          // W_n^{i << fsh}
+    void* ftb = nullptr;          // W_n^{i}
+    int fsh = 0;
+    double scale_override = 0.0;  // sub-plans: scale of the last pass (0 = the default)
 
     size_t elem_bytes() const { return prec == 0 ? 8 : 16; }
     int P() const { return comm ? nranks : virt; }
     // slab-decomposed schedule: a communicator (any size, 1 included) or virtual ranks
-    bool dist() const { return rank == 2 && (comm != nullptr || virt > 1); }
+    bool dist() const { return (rank == 2 || batch == 1) && (comm != nullptr || virt > 1); }
     // elements addressed by one call: the local slab (NCCL) or everything (virtual)
     int64_t elems() const {
+        if (rank == 1 && batch == 1 && comm) return n0 / nranks;
         if (rank == 2 && comm) return batch * (n0 / nranks) * n1;
         return batch * n0 * (rank == 2 ? n1 : 1);
     }
@@ -211,7 +220,7 @@ std::vector<int64_t> split_radices(int64_t L) {
 
 fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
     const int64_t L = p->n0;
-    const double scale = inv ? 1.0 : 1.0 / (double)L;
+    const double scale = p->scale_override != 0.0 ? p->scale_override : (inv ? 1.0 : 1.0 / (double)L);
     cudaError_t e;
     if (p->tw4) {
         // one HBM pass: the cluster kernel reads each transform fully before
@@ -455,6 +464,130 @@ fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_f
     return FFT_OK;
 }
 
+// ---- distributed four-step 1D (one transform of n = N1 N2 over P ranks) ----
+// Rank r owns x[r n/P, (r+1) n/P) = rows n2 in [r S2, (r+1) S2) of the view
+// A[n2][n1] = x[n1 + N1 n2] (S2 = N2/P).  Four-step (fft_cluster.cuh):
+//   (A) FFT over n2 for each n1, (T) * W_n^{n1 k2}, (B) FFT over n1 for each
+//   k2, X[k2 + N2 k1].
+// Schedule per rank: transpose (pack) -> a2a -> unpack to [S1][N2] -> (A)
+// rows -> (T) -> transpose -> a2a -> unpack to [S2][N1] -> (B) rows (1/n) ->
+// transpose -> a2a -> unpack: rank r ends with X[r n/P, (r+1) n/P)
+// (natural order, three all-to-alls).
+fft_status fs_prepare(fft_plan_s* p) {
+    const int P = p->P();
+    const int m = ilog2(p->n0);
+    const int64_t N1 = (int64_t)1 << (m - m / 2), N2 = (int64_t)1 << (m / 2);
+    if (N1 % P || N2 % P) return fail(FFT_E_INVALID_SIZE, "transform too small for the rank count");
+    if (p->sub_a && p->fs1 == N1) return FFT_OK;
+    p->fs1 = N1;
+    p->fs2 = N2;
+    fft_precision prec = p->prec == 0 ? FFT_C64 : FFT_C128;
+    int64_t d2 = N2, d1 = N1;
+    fft_status s = fft_plan_create_ex(&p->sub_a, &d2, 1, N1 / P, prec, 0);
+    if (s == FFT_OK) s = fft_plan_create_ex(&p->sub_b, &d1, 1, N2 / P, prec, 0);
+    if (s != FFT_OK) return s;
+    p->sub_a->scale_override = 1.0;                       // (A) unnormalised
+    p->sub_b->scale_override = 1.0 / (double)p->n0;       // the paper's 1/n, once
+    p->fsh = (m + 1) / 2;
+    std::vector<double> a, b;
+    const int64_t na = (int64_t)1 << (m - p->fsh), nb = (int64_t)1 << p->fsh;
+    a.resize(2 * na);
+    b.resize(2 * nb);
+    for (int64_t i = 0; i < na; ++i) {
+        const double ang = -2.0 * M_PI * (double)((i << p->fsh) % p->n0) / (double)p->n0;
+        a[2 * i] = std::cos(ang);
+        a[2 * i + 1] = std::sin(ang);
+    }
+    for (int64_t i = 0; i < nb; ++i) {
+        const double ang = -2.0 * M_PI * (double)i / (double)p->n0;
+        b[2 * i] = std::cos(ang);
+        b[2 * i + 1] = std::sin(ang);
+    }
+    cudaError_t e = upload(a, p->prec, &p->fta);
+    if (e == cudaSuccess) e = upload(b, p->prec, &p->ftb);
+    if (e != cudaSuccess) return cuda_fail(e, "four-step twiddle upload");
+    return FFT_OK;
+}
+
+// [P][R][Cb] blocks (by source rank) -> [R][P * Cb] rows, for each local slab
+cudaError_t unpack_blocks(char* dst, const char* src, int64_t R, int64_t Cb, int P, size_t eb, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    for (int q = 0; q < P && e == cudaSuccess; ++q)
+        e = cudaMemcpy2DAsync(dst + (size_t)q * Cb * eb, (size_t)P * Cb * eb, src + (size_t)q * R * Cb * eb, Cb * eb,
+                              Cb * eb, (size_t)R, cudaMemcpyDeviceToDevice, st);
+    return e;
+}
+
+fft_status run_dist_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
+    fft_status s = fs_prepare(p);
+    if (s == FFT_OK) s = ensure_workspace(p);
+    if (s != FFT_OK) return s;
+    p->sub_a->stream = st;
+    p->sub_b->stream = st;
+    const int P = p->P();
+    const int64_t N1 = p->fs1, N2 = p->fs2, S1 = N1 / P, S2 = N2 / P;
+    const int64_t loc = p->n0 / P;  // elements per rank
+    const size_t eb = p->elem_bytes();
+    const int nloc = p->comm ? 1 : P;
+    const int r0 = p->comm ? p->my_rank : 0;
+    char* w0 = (char*)p->ws;
+    char* w1 = w0 + (size_t)nloc * loc * eb;
+    cudaError_t e;
+    int launches = 0;
+    auto slab = [&](const void* base, int l) { return (char*)base + (size_t)l * loc * eb; };
+    // 1. pack: A[S2][N1] -> [N1][S2] (block q = columns n1 of rank q)
+    e = launch_transpose(p->prec, in, w0, S2, N1, nloc, st);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose");
+    ++launches;
+    s = dist_exchange(p, w0, w1, S1 * S2, st);
+    if (s != FFT_OK) return s;
+    // 2. unpack to [S1][N2] (row n1, n2 = q S2 + local)
+    for (int l = 0; l < nloc; ++l) {
+        e = unpack_blocks(slab(w0, l), slab(w1, l), S1, S2, P, eb, st);
+        if (e != cudaSuccess) return cuda_fail(e, "unpack");
+    }
+    // 3. (A) FFT over n2 (unnormalised) and (T) the four-step twiddle
+    for (int l = 0; l < nloc; ++l) {
+        s = run_1d(p->sub_a, slab(w0, l), slab(w0, l), inv, st);
+        if (s != FFT_OK) return s;
+        launches += p->sub_a->last_launches;
+        e = launch_twiddle4(p->prec, inv, slab(w0, l), S1, N2, (int64_t)(r0 + l) * S1, p->fta, p->ftb, p->fsh, st);
+        if (e != cudaSuccess) return cuda_fail(e, "twiddle");
+        ++launches;
+    }
+    // 4. pack [S1][N2] -> [N2][S1] (block q = rows k2 of rank q), exchange, unpack to [S2][N1]
+    e = launch_transpose(p->prec, w0, w1, S1, N2, nloc, st);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose");
+    ++launches;
+    s = dist_exchange(p, w1, w0, S1 * S2, st);
+    if (s != FFT_OK) return s;
+    for (int l = 0; l < nloc; ++l) {
+        e = unpack_blocks(slab(w1, l), slab(w0, l), S2, S1, P, eb, st);
+        if (e != cudaSuccess) return cuda_fail(e, "unpack");
+    }
+    // 5. (B) FFT over n1 with the paper's 1/n (forward): Z[k2 local][k1]
+    for (int l = 0; l < nloc; ++l) {
+        const double saved = p->sub_b->scale_override;
+        if (inv) p->sub_b->scale_override = 1.0;
+        s = run_1d(p->sub_b, slab(w1, l), slab(w1, l), inv, st);
+        p->sub_b->scale_override = saved;
+        if (s != FFT_OK) return s;
+        launches += p->sub_b->last_launches;
+    }
+    // 6. natural order: pack [S2][N1] -> [N1][S2] (block q = k1 of rank q), exchange, unpack
+    e = launch_transpose(p->prec, w1, w0, S2, N1, nloc, st);
+    if (e != cudaSuccess) return cuda_fail(e, "transpose");
+    ++launches;
+    s = dist_exchange(p, w0, w1, S1 * S2, st);
+    if (s != FFT_OK) return s;
+    for (int l = 0; l < nloc; ++l) {
+        e = unpack_blocks(slab(out, l), slab(w1, l), S1, S2, P, eb, st);
+        if (e != cudaSuccess) return cuda_fail(e, "unpack");
+    }
+    p->last_launches = launches;
+    return FFT_OK;
+}
+
 fft_status check_ptrs(fft_plan_s* p, const void* in, void* out, bool real_in) {
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (!in || !out) return fail(FFT_E_INVALID_ARG, "null data pointer");
@@ -539,10 +672,11 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
                 t[2 * (k2 * cn1 + n1) + 1] = std::sin(ang);
             }
         const char* var = getenv("B200FFT_CLUSTER_VARIANT");
-        // default: st.async transpose, 16-CTA clusters, 4 CTAs/SM (the
+        // default 16: st.async transpose with rank-rotated send order (no
+        // incast), 16-CTA clusters, 4 CTAs/SM (the
         // fastest measured); 8/9 are timing-only
-        p->cvariant = var ? atoi(var) : 10;
-        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 10;
+        p->cvariant = var ? atoi(var) : 16;
+        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 16;
         if (var && atoi(var) == 8 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 8;
         if (var && atoi(var) == 9 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 9;
         e = upload(t, ip, &p->tw4);
@@ -623,7 +757,7 @@ static fft_status exec(fft_plan p, const void* in, void* out, bool inv) {
     if (p->elems() == 0) return FFT_OK;
     // rank 1 on several ranks: the batch is sharded (each rank's plan holds its
     // own rows), so the local schedule is the whole job -- no collective
-    if (p->rank == 1) return run_1d(p, in, out, inv, p->stream);
+    if (p->rank == 1) return p->dist() ? run_dist_1d(p, in, out, inv, p->stream) : run_1d(p, in, out, inv, p->stream);
     if (p->dist()) return run_dist_2d(p, in, out, inv ? 1 : 0, FFT_FILTER_NONE, 0.0, p->stream);
     return run_2d(p, in, out, inv, p->stream);
 }
@@ -754,11 +888,13 @@ fft_status fft_plan_set_comm(fft_plan p, const unsigned char id[128], int nranks
     if (p->rank == 2 && (p->n0 % nranks || p->n1 % nranks))
         return fail(FFT_E_INVALID_SIZE, "2D sides must be divisible by the rank count");
     if (!id) return fail(FFT_E_INVALID_ARG, "null unique id");
-    if (p->rank == 1) {  // batch-sharded: no collective on the data path
+    if (p->rank == 1 && p->batch != 1) {  // batch-sharded: no collective on the data path
         p->nranks = nranks;
         p->my_rank = my_rank;
         return FFT_OK;
     }
+    if (p->rank == 1 && ((int64_t)nranks * nranks > p->n0 || p->n0 % nranks))
+        return fail(FFT_E_INVALID_SIZE, "1D four-step needs n >= nranks^2");
 #ifdef B200FFT_WITH_NCCL
     ncclUniqueId u;
     memcpy(&u, id, 128);
@@ -781,10 +917,13 @@ fft_status fft_plan_set_comm(fft_plan p, const unsigned char id[128], int nranks
 
 fft_status fft_plan_set_virtual_ranks(fft_plan p, int nranks) {
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
-    if (p->rank != 2) return fail(FFT_E_INVALID_ARG, "virtual ranks apply to rank-2 plans");
+    if (p->rank != 2 && p->batch != 1)
+        return fail(FFT_E_INVALID_ARG, "virtual ranks apply to rank-2 plans and single 1D transforms");
     if (p->comm) return fail(FFT_E_STATE, "plan has a communicator");
-    if (nranks < 1 || p->n0 % nranks || p->n1 % nranks)
-        return fail(FFT_E_INVALID_SIZE, "2D sides must be divisible by the rank count");
+    if (nranks < 1 || p->n0 % nranks || (p->rank == 2 && p->n1 % nranks))
+        return fail(FFT_E_INVALID_SIZE, "sizes must be divisible by the rank count");
+    if (p->rank == 1 && (int64_t)nranks * nranks > p->n0)
+        return fail(FFT_E_INVALID_SIZE, "1D four-step needs n >= nranks^2");
     p->virt = nranks;
     if (p->ws_owned && p->ws) {
         cudaFree(p->ws);
@@ -800,6 +939,10 @@ fft_status fft_plan_destroy(fft_plan p) {
     if (!p) return FFT_OK;
     cudaError_t e = cudaSuccess;
     if (p->tw4) cudaFree(p->tw4);
+    if (p->fta) cudaFree(p->fta);
+    if (p->ftb) cudaFree(p->ftb);
+    if (p->sub_a) fft_plan_destroy(p->sub_a);
+    if (p->sub_b) fft_plan_destroy(p->sub_b);
     for (void* q : p->pa)
         if (q) cudaFree(q);
     for (void* q : p->pb)

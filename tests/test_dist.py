@@ -80,6 +80,54 @@ def test_virtual_ranks_c4_shape_real_input():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("m,dtype", [(8, np.complex64), (16, np.complex64), (20, np.complex64),
+                                     (22, np.complex64), (18, np.complex128)])
+def test_virtual_ranks_four_step_1d(P, m, dtype):
+    """The distributed four-step 1D schedule (3 all-to-alls, natural order)
+    as P virtual ranks; forward (1/N) and inverse against the oracle."""
+    b = _lib()
+    n = 1 << m
+    x = fixtures.complex_input(n, fixtures.NORMAL, seed=600 + m, dtype=dtype)
+    prec = b.C64 if dtype == np.complex64 else b.C128
+    p = b.Plan((n,), batch=1, precision=prec)
+    if P > 1:
+        p.set_virtual_ranks(P)
+    else:
+        p.set_comm(b.nccl_unique_id(), 1, 0)  # the NCCL exchange with one rank
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    zd = torch.empty_like(xd)
+    p.forward(xd, yd)
+    p.inverse(xd, zd)
+    torch.cuda.synchronize()
+    tol = 1e-5 if dtype == np.complex64 else 1e-12
+    assert oracle.rel_l2(yd.cpu().numpy(), oracle.fft(x)) <= tol
+    assert oracle.rel_l2(zd.cpu().numpy(), oracle.ifft(x)) <= tol
+    p.destroy()
+
+
+@pytest.mark.gpu
+def test_virtual_ranks_c5_shape():
+    """BASELINE configs[4] layout: N = 2^30 over 8 virtual ranks (32768 x
+    32768 four-step); 16 sampled bins against the oracle's direct sums."""
+    b = _lib()
+    n = 1 << 30
+    x = np.empty(n, np.complex64)
+    fixtures.complex_input(n, fixtures.NORMAL, seed=5, out=x)
+    p = b.Plan((n,), batch=1)
+    p.set_virtual_ranks(8)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    p.forward(xd, yd)
+    torch.cuda.synchronize()
+    bins = np.concatenate([[0, 1, n // 2, n - 1], np.random.default_rng(55).integers(0, n, 12)])
+    got = yd[torch.from_numpy(bins).cuda()].cpu().numpy()
+    assert oracle.rel_l2(got, oracle.dft_bins(x, bins)) <= 1e-5
+    p.destroy()
+
+
+@pytest.mark.gpu
 def test_nccl_single_rank_communicator():
     """The NCCL data path (ncclSend/ncclRecv all-to-all) with one rank."""
     b = _lib()
