@@ -387,9 +387,90 @@ def reference_arm(args, ws, rank):
     }
 
 
+def bench_sharded(args, ws, rank, local, cfg):
+    """C4 (8192^2 Gaussian pipeline, row slabs) or C5 (one 2^30 transform,
+    four-step) across the ranks: the library's NCCL path when ws > 1."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_cs_0103001_b200 as b
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    if cfg == "C4":
+        N = 8192
+        loc = N * N // ws
+        x = fixtures.complex_input(loc, fixtures.UNIFORM, seed=4, offset=rank * loc)
+        plan = b.Plan((N, N), stream=stream)
+        flops = 2 * 5.0 * N * N * math.log2(N * N)
+        a2a_per_step, alg_bytes = 2, 32.0 * loc
+        workload = "C4: 8192^2 complex64 Gaussian pipeline, row slabs, 2 all-to-alls"
+    else:
+        n = 1 << 30
+        loc = n // ws
+        x = np.empty(loc, np.complex64)
+        fixtures.complex_input(loc, fixtures.NORMAL, seed=5, offset=rank * loc, out=x)
+        plan = b.Plan((n,), batch=1, stream=stream)
+        flops = 2 * 5.0 * n * math.log2(n)
+        a2a_per_step, alg_bytes = 6, 32.0 * loc
+        workload = "C5: N=2^30 complex64 forward(1/N)+inverse, four-step, 3 all-to-alls per direction"
+    if ws > 1:
+        uid = [b.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        plan.set_comm(uid[0], ws, rank)
+    xd = torch.from_numpy(x).to(dev)
+    yd = torch.empty_like(xd)
+    zd = torch.empty_like(xd)
+
+    def step():
+        if cfg == "C4":
+            plan.filter_pipeline(xd, yd, b.FILTER_GAUSS, 0.1)
+            return plan.last_launch_count()
+        plan.forward(xd, yd)
+        l1 = plan.last_launch_count()
+        plan.inverse(yd, zd)
+        return l1 + plan.last_launch_count()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        s.record(stream)
+        for _ in range(args.steps):
+            launches += step()
+        e.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    ms = allreduce_max(ws, s.elapsed_time(e)) / args.steps
+    peak, peak_kind = hbm_peak()
+    nvl = 8.0 * loc * (ws - 1) / ws * a2a_per_step  # bytes each GPU sends per step
+    res = {
+        "metric": "FFT GFLOP/s (5N*log2N), sharded", "value": round(flops / (ms / 1e3) / 1e9, 3),
+        "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c64 (fp32 arithmetic)", "data": "synthetic (counter-based seeded)",
+        "config": {"workload": workload, "parallelism": f"slabs x{ws}, NCCL all-to-all" if ws > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm" if ws == 1 else "nvlink", "hbm_achieved_GBps_per_gpu":
+                     round(alg_bytes / (ms / 1e3) / 1e9, 1), "hbm_peak": peak, "peak_source": peak_kind,
+                     "nvlink_bytes_per_gpu_per_step": nvl,
+                     "nvlink_GBps_per_gpu": round(nvl / (ms / 1e3) / 1e9, 1) if ws > 1 else None,
+                     "nvlink_peak_GBps": 900.0},
+        "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    plan.destroy()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--config", default="C2", choices=["C2", "C4", "C5"],
+                    help="C2 (default, the metric's config), or the sharded C4 / C5")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -403,6 +484,15 @@ def main():
         res = reference_arm(args, ws, rank)
         if res is not None:
             print(json.dumps(res), flush=True)
+        return
+    if args.config != "C2":
+        res = bench_sharded(args, ws, rank, local, args.config)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
         return
     res = bench_c2(args, ws, rank, local)
     if rank == 0:

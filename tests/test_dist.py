@@ -233,6 +233,63 @@ def test_gloo_two_rank_slab_schedule(N, M):
     assert res[0] <= 1e-13 and res[1] <= 1e-13, res
 
 
+def _unpack(recv, P):
+    """[P][R][Cb] blocks by source rank -> [R][P*Cb] (the library's unpack_blocks)."""
+    _, R, Cb = recv.shape
+    return np.ascontiguousarray(recv.transpose(1, 0, 2).reshape(R, P * Cb))
+
+
+def _worker_1d(rank, world, port, m, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        P = world
+        n = 1 << m
+        N1, N2 = 1 << (m - m // 2), 1 << (m // 2)
+        S1, S2 = N1 // P, N2 // P
+        x = fixtures.complex_input(n, fixtures.NORMAL, seed=21, dtype=np.complex128)
+        A = x[rank * n // P:(rank + 1) * n // P].reshape(S2, N1)  # rows n2 of x[n1 + N1 n2]
+        # 1. pack = transpose; exchange blocks of [S1][S2]; unpack to [S1][N2]
+        u = _unpack(_a2a(dist, A.T.copy().reshape(P, S1, S2)), P)
+        # 2. (A) unnormalised FFT over n2, (T) twiddle W_n^{n1 k2}
+        u = np.stack([oracle.fft(r) * N2 for r in u])
+        n1 = rank * S1 + np.arange(S1)[:, None]
+        k2 = np.arange(N2)[None, :]
+        u = u * np.exp(-2j * np.pi * ((n1 * k2) % n) / n)
+        # 3. pack, exchange, unpack to [S2][N1]; (B) FFT over n1 with 1/n overall
+        z = _unpack(_a2a(dist, u.T.copy().reshape(P, S2, S1)), P)
+        z = np.stack([oracle.fft(r) * N1 for r in z]) / n
+        # 4. natural order: pack, exchange, unpack to [S1][N2] = X[r n/P, (r+1) n/P)
+        out = _unpack(_a2a(dist, z.T.copy().reshape(P, S1, S2)), P).ravel()
+        ref = oracle.fft(x)[rank * n // P:(rank + 1) * n // P]
+        q.put((rank, oracle.rel_l2(out, ref)))
+    except Exception as exc:
+        q.put((rank, f"error: {exc!r}"))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m", [8, 11])
+def test_gloo_two_rank_four_step_1d(m):
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_1d, args=(r, 2, port, m, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=60) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[0] <= 1e-13 and res[1] <= 1e-13, res
+
+
 def test_block_layout_roundtrip():
     a = np.arange(4 * 16).reshape(4, 16)
     blocks = _rows_blocked(a, 4)
