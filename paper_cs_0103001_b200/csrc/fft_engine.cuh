@@ -26,7 +26,12 @@ constexpr int RMAX = 8192;  // largest in-CTA DFT
 // fft_common.cuh (tw_base / tw_off), fp64-generated on the host and rounded
 // once; kernels receive the pointer to their R's table.
 
-template <typename T, int R, int E, bool INV>
+// unpadded smem layout (LAYOUT 1): XOR the low 4 index bits with bits 4..7,
+// a permutation inside every 16-element group that makes both the
+// consecutive and the stride-16 access patterns of the steps conflict-free
+__device__ __forceinline__ int swz16(int i) { return i ^ ((i >> 4) & 15); }
+
+template <typename T, int R, int E, bool INV, int LAYOUT = 0>
 struct LineFFT {
     using C = cpx<T>;
     static constexpr int TPL = R / E;
@@ -74,7 +79,10 @@ struct LineFFT {
             const int j = lt + b * TPL;
             const int k = j & (Ns - 1);
             const int base = (j - k) * rho + k;
-            if constexpr (Ns % 16 == 0) {
+            if constexpr (LAYOUT == 1) {
+#pragma unroll
+                for (int q = 0; q < rho; ++q) line[swz16(base + q * Ns)] = v[b * rho + q];
+            } else if constexpr (Ns % 16 == 0) {
                 const int pb = pad16(base);
 #pragma unroll
                 for (int q = 0; q < rho; ++q) line[pb + q * (Ns + Ns / 16)] = v[b * rho + q];
@@ -96,7 +104,10 @@ struct LineFFT {
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
             const int j = lt + b * TPL;
-            if constexpr (st % 16 == 0) {
+            if constexpr (LAYOUT == 1) {
+#pragma unroll
+                for (int r = 0; r < rho; ++r) v[b * rho + r] = line[swz16(j + r * st)];
+            } else if constexpr (st % 16 == 0) {
                 const int pj = pad16(j);
 #pragma unroll
                 for (int r = 0; r < rho; ++r) v[b * rho + r] = line[pj + r * (st + st / 16)];
@@ -109,7 +120,8 @@ struct LineFFT {
 
     // padded index of boundary element m (element lt + TPL m of the line)
     __device__ __forceinline__ static int bpos(int lt, int m) {
-        if constexpr (TPL % 16 == 0) return pad16(lt) + m * (TPL + TPL / 16);
+        if constexpr (LAYOUT == 1) return swz16(lt + TPL * m);
+        else if constexpr (TPL % 16 == 0) return pad16(lt) + m * (TPL + TPL / 16);
         else return pad16(lt + TPL * m);
     }
 
@@ -260,7 +272,10 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
     C* dst = out + img * (int64_t)R * S + s0;
     const int wv = (int)((S - s0) < W ? (S - s0) : W);  // ragged last tile
 
-    for (int idx = tid; idx < W * R; idx += NT) {
+    // fully unrolled so that all of a thread's loads are in flight at once
+#pragma unroll
+    for (int it = 0; it < (W * R) / NT; ++it) {
+        const int idx = tid + it * NT;
         const int tt = idx % W, r = idx / W;
         smem[tt * LSC + pad16(r)] = (tt < wv) ? src[(int64_t)r * S + tt] : mk((T)0, (T)0);
     }
@@ -289,7 +304,10 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
         for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = cscale(v[F::pos_out(m)], scale);
     }
     __syncthreads();
-    for (int idx = tid; idx < W * R; idx += NT) {
+    // fully unrolled so that all of a thread's loads are in flight at once
+#pragma unroll
+    for (int it = 0; it < (W * R) / NT; ++it) {
+        const int idx = tid + it * NT;
         const int tt = idx % W, r = idx / W;
         if (tt < wv) dst[(int64_t)r * S + tt] = smem[tt * LSC + pad16(r)];
     }
@@ -326,7 +344,10 @@ __global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ i
     const int64_t KLO = (int64_t)1 << klo_sh;
     const int64_t nhi = Ns >> klo_sh;
 
-    for (int idx = tid; idx < W * R; idx += NT) {
+    // fully unrolled so that all of a thread's loads are in flight at once
+#pragma unroll
+    for (int it = 0; it < (W * R) / NT; ++it) {
+        const int idx = tid + it * NT;
         const int tt = idx % W, r = idx / W;
         const int64_t j = j0 + tt;
         C a = src[j + (int64_t)r * LR];
@@ -349,13 +370,19 @@ __global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ i
     for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = cscale(v[F::pos_out(m)], scale);
     __syncthreads();
     if (Ns >= W) {
-        for (int idx = tid; idx < W * R; idx += NT) {
+        // fully unrolled so that all of a thread's loads are in flight at once
+#pragma unroll
+    for (int it = 0; it < (W * R) / NT; ++it) {
+        const int idx = tid + it * NT;
             const int tt = idx % W, q = idx / W;
             const int64_t j = j0 + tt, k = j & (Ns - 1);
             dst[(j - k) * R + k + (int64_t)q * Ns] = smem[tt * F::LS + pad16(q)];
         }
     } else {
-        for (int idx = tid; idx < W * R; idx += NT) {
+        // fully unrolled so that all of a thread's loads are in flight at once
+#pragma unroll
+    for (int it = 0; it < (W * R) / NT; ++it) {
+        const int idx = tid + it * NT;
             const int q = idx % R, tt = idx / R;
             const int64_t j = j0 + tt, k = j & (Ns - 1);
             dst[(j - k) * R + k + (int64_t)q * Ns] = smem[tt * F::LS + pad16(q)];

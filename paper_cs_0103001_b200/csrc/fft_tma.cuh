@@ -1,0 +1,115 @@
+// fft_tma.cuh -- persistent, TMA-fed row FFT kernel (sm_100a).
+//
+// Same computation as k_rows (the paper's DFT, Eq. E2 / Eq. E3, on
+// contiguous rows), but every CTA is persistent and keeps STAGES tiles of
+// W rows in flight: one thread issues a bulk copy (cp.async.bulk, the TMA
+// engine) of the next tiles into a ring of shared-memory stages, completing
+// on per-stage mbarriers, while all threads run the Stockham steps IN PLACE
+// in the current stage (unpadded, XOR-swizzled exchanges, LineFFT LAYOUT 1)
+// and store the results straight from registers (coalesced).  HBM reads are
+// therefore always outstanding, independent of the compute phase, instead of
+// the load -> compute -> store convoy of one tile per CTA.
+#pragma once
+#include "fft_engine.cuh"
+
+namespace b200fft {
+
+__device__ __forceinline__ uint32_t smem_addr_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TMA_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TMA_WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+template <typename T, int R, int W, bool REAL_IN, int STAGES>
+struct RowsTmaCfg {
+    static constexpr size_t STAGE_BYTES = sizeof(cpx<T>) * W * R;
+    static constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 8 * STAGES;
+    static constexpr uint32_t ROW_IN_BYTES = (uint32_t)(R * (REAL_IN ? sizeof(float) : sizeof(cpx<T>)));
+};
+
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES>
+__global__ void __launch_bounds__(W*(R / E), 1)
+    k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
+               const cpx<T>* __restrict__ tw) {
+    using C = cpx<T>;
+    using F = LineFFT<T, R, E, INV, 1>;
+    using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
+    static_assert(R >= 256 && (R * sizeof(cpx<T>)) % 16 == 0, "bulk copies need >= 16 B rows");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t bar0 = smem_addr_u32(smem_raw + STAGES * G::STAGE_BYTES);
+    const int tid = threadIdx.x;
+    const int t = tid / F::TPL, lt = tid % F::TPL;
+    const int64_t ntiles = (batch + W - 1) / W;
+    const char* in = reinterpret_cast<const char*>(in_);
+
+    auto issue = [&](int64_t tile, int s) {
+        const int64_t r0 = tile * W;
+        const int64_t nr = (batch - r0) < W ? (batch - r0) : W;
+        const uint32_t bytes = (uint32_t)(nr * G::ROW_IN_BYTES);
+        const uint32_t bar = bar0 + 8 * s;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(smem_addr_u32(smem_raw + s * G::STAGE_BYTES), in + r0 * G::ROW_IN_BYTES, bytes, bar);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        for (int s = 0; s < STAGES; ++s) {
+            const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+            if (tile < ntiles) issue(tile, s);
+        }
+    }
+    __syncthreads();
+
+    for (int64_t k = 0;; ++k) {
+        const int64_t tile = blockIdx.x + k * gridDim.x;
+        if (tile >= ntiles) break;
+        const int s = (int)(k % STAGES);
+        mbar_wait(bar0 + 8 * s, (uint32_t)((k / STAGES) & 1));
+        C* line = reinterpret_cast<C*>(smem_raw + s * G::STAGE_BYTES) + t * R;
+        C v[E];
+        if constexpr (REAL_IN) {
+            const float* fl = reinterpret_cast<const float*>(smem_raw + s * G::STAGE_BYTES) + t * R;
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[F::pos_in(m)] = mk((T)fl[lt + F::TPL * m], (T)0);
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[lt + F::TPL * m];
+        }
+        F::run(v, line, lt, tw);
+        const int64_t row = tile * W + t;
+        if (row < batch) {
+            C* o = out + row * R + lt;
+#pragma unroll
+            for (int m = 0; m < E; ++m) o[F::TPL * m] = cscale(v[F::pos_out(m)], scale);
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const int64_t nt = blockIdx.x + (k + STAGES) * gridDim.x;
+            if (nt < ntiles) issue(nt, s);
+        }
+    }
+}
+
+}  // namespace b200fft

@@ -1,5 +1,8 @@
 // kernels_rows.cu -- instantiations and launcher of kernel family A (rows).
+#include <cstdlib>
+
 #include "fft_engine.cuh"
+#include "fft_tma.cuh"
 #include "launch.h"
 
 namespace b200fft {
@@ -43,10 +46,65 @@ cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double s
     }
 }
 
+// persistent TMA-fed variant (fft_tma.cuh): 3 stages of ~64 KiB, 512 threads
+template <typename T, int R, bool INV, bool REAL_IN>
+cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw, cudaStream_t st) {
+    constexpr int E = 16;
+    constexpr int W = (int)((64 * 1024) / (R * sizeof(cpx<T>))) < 1 ? 1 : (int)((64 * 1024) / (R * sizeof(cpx<T>)));
+    constexpr int STAGES = 3;
+    using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
+    auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES>;
+    static int grid_max = 0;
+    if (!grid_max) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * (R / E), G::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        grid_max = sms * (occ > 0 ? occ : 1);
+    }
+    if (batch <= 0) return cudaSuccess;
+    const int64_t tiles = (batch + W - 1) / W;
+    const int grid = (int)(tiles < grid_max ? tiles : grid_max);
+    kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(in, reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
+                                                   reinterpret_cast<const cpx<T>*>(tw) + tw_base(R));
+    return cudaGetLastError();
+}
+
+template <bool INV, bool REAL_IN>
+cudaError_t rows_tma_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw,
+                       cudaStream_t st) {
+    switch (R) {
+        case 256: return rows_tma_t<float, 256, INV, REAL_IN>(in, out, batch, scale, tw, st);
+        case 512: return rows_tma_t<float, 512, INV, REAL_IN>(in, out, batch, scale, tw, st);
+        case 1024: return rows_tma_t<float, 1024, INV, REAL_IN>(in, out, batch, scale, tw, st);
+        case 2048: return rows_tma_t<float, 2048, INV, REAL_IN>(in, out, batch, scale, tw, st);
+        case 4096: return rows_tma_t<float, 4096, INV, REAL_IN>(in, out, batch, scale, tw, st);
+        case 8192: return rows_tma_t<float, 8192, INV, REAL_IN>(in, out, batch, scale, tw, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool use_tma_rows(int prec, int64_t R, int in_sh, int out_sh) {
+    static const bool off = [] {
+        const char* e = getenv("B200FFT_NO_TMA");
+        return e && e[0] == '1';
+    }();
+    return !off && prec == 0 && R >= 256 && R <= 8192 && in_sh < 0 && out_sh < 0;
+}
+
 }  // namespace
 
 cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void* in, void* out,
                         int64_t batch, double scale, const void* tw, cudaStream_t st, int in_sh, int out_sh) {
+    // in == out is safe: every tile is read (prefetched) by the CTA that later
+    // writes it, and no other CTA touches it
+    if (use_tma_rows(prec, R, in_sh, out_sh)) {
+        if (real_in) return rows_tma_r<false, true>(R, in, out, batch, scale, tw, st);
+        return inv ? rows_tma_r<true, false>(R, in, out, batch, scale, tw, st)
+                   : rows_tma_r<false, false>(R, in, out, batch, scale, tw, st);
+    }
     if (prec == 0) {
         if (real_in) return rows_r<float, false, true>(R, in, out, batch, scale, tw, in_sh, out_sh, st);
         return inv ? rows_r<float, true, false>(R, in, out, batch, scale, tw, in_sh, out_sh, st)
