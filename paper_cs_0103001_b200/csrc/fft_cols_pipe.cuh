@@ -1,0 +1,118 @@
+// fft_cols_pipe.cuh -- persistent, double-buffered column kernel (sm_100a).
+//
+// Same computation as k_cols (column DFTs of an [R][S] grid, MODE 2 = the
+// fused forward -> filter -> inverse of the pipeline), but each CTA is
+// persistent over column tiles and prefetches tile k+1 with cp.async
+// (LDGSTS, asynchronous global -> shared copies straight into the padded
+// line layout of the engine) while it transforms tile k in place.  The plain
+// k_cols issues a tile's loads, waits for all of them, computes and stores:
+// its warps mostly wait on long-scoreboard stalls (ncu, profiles/).
+#pragma once
+#include "fft_engine.cuh"
+
+namespace b200fft {
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    const int sz = valid ? 8 : 0;  // src-size 0 zero-fills
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <typename T, int R, int W>
+struct ColsPipeCfg {
+    static constexpr int LSC = cols_ls<T, R, W>();
+    static constexpr size_t STAGE_ELEMS = (size_t)W * LSC;
+    static constexpr size_t SMEM_BYTES = 2 * STAGE_ELEMS * sizeof(cpx<T>);
+};
+
+template <typename T, int R, int E, int W, int MODE>
+__global__ void __launch_bounds__(W*(R / E), 1)
+    k_cols_pipe(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, int64_t S, int64_t nimg, T scale,
+                const cpx<T>* __restrict__ tw, FilterArgs filt) {
+    using C = cpx<T>;
+    constexpr bool INV0 = (MODE == 1);
+    using F = LineFFT<T, R, E, INV0>;
+    using FI = LineFFT<T, R, E, true>;
+    using G = ColsPipeCfg<T, R, W>;
+    constexpr int NT = W * F::TPL;
+    constexpr int LSC = G::LSC;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* stage0 = reinterpret_cast<C*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int t = tid / F::TPL, lt = tid % F::TPL;
+    const int64_t tiles_per_img = (S + W - 1) / W;
+    const int64_t ntiles = tiles_per_img * nimg;
+
+    auto prefetch = [&](int64_t tile, int buf) {
+        if (tile < ntiles) {
+            const int64_t img = tile / tiles_per_img;
+            const int64_t s0 = (tile - img * tiles_per_img) * W;
+            const C* src = in + img * (int64_t)R * S + s0;
+            const int wv = (int)((S - s0) < W ? (S - s0) : W);
+            C* sm = stage0 + buf * G::STAGE_ELEMS;
+#pragma unroll
+            for (int it = 0; it < (W * R) / NT; ++it) {
+                const int idx = tid + it * NT;
+                const int tt = idx % W, r = idx / W;
+                const bool ok = tt < wv;
+                cp_async8(sm + tt * LSC + pad16(r), ok ? src + (int64_t)r * S + tt : src, ok);
+            }
+        }
+        cp_async_commit();  // one group per call (possibly empty): uniform wait counts
+    };
+
+    prefetch(blockIdx.x, 0);
+    for (int64_t k = 0;; ++k) {
+        const int64_t tile = blockIdx.x + k * gridDim.x;
+        if (tile >= ntiles) break;
+        const int buf = (int)(k & 1);
+        prefetch(tile + gridDim.x, buf ^ 1);
+        cp_async_wait<1>();  // this thread's copies of tile k have landed
+        __syncthreads();     // ... and everyone else's
+        const int64_t img = tile / tiles_per_img;
+        const int64_t s0 = (tile - img * tiles_per_img) * W;
+        const int wv = (int)((S - s0) < W ? (S - s0) : W);
+        C* sm = stage0 + buf * G::STAGE_ELEMS;
+        C* line = sm + t * LSC;
+        C v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
+        const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
+        F::run(v, line, lt, tw, bar);
+        if constexpr (MODE == 2) {
+            C w[E];
+            const int64_t col = s0 + t;
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int64_t u = lt + F::TPL * m;
+                const T h = (col < S) ? filter_value<T>(filt, u, col + filt.col_off) * scale : (T)0;
+                w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], h);
+            }
+            FI::run(w, line, lt, tw, bar);
+            F::lsync(bar);
+#pragma unroll
+            for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = w[FI::pos_out(m)];
+        } else {
+            F::lsync(bar);
+#pragma unroll
+            for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = cscale(v[F::pos_out(m)], scale);
+        }
+        __syncthreads();
+        C* dst = out + img * (int64_t)R * S + s0;
+#pragma unroll
+        for (int it = 0; it < (W * R) / NT; ++it) {
+            const int idx = tid + it * NT;
+            const int tt = idx % W, r = idx / W;
+            if (tt < wv) dst[(int64_t)r * S + tt] = sm[tt * LSC + pad16(r)];
+        }
+        __syncthreads();  // buffer `buf` is free for the prefetch two tiles ahead
+    }
+    cp_async_wait<0>();
+}
+
+}  // namespace b200fft

@@ -125,22 +125,35 @@ struct LineFFT {
         else return pad16(lt + TPL * m);
     }
 
+    // Barrier between steps: the whole CTA, or (bar >= 1) only the TPL
+    // threads of this line through named barrier `bar` -- lines of one CTA
+    // then never wait for each other.  Needs TPL % 32 == 0 (whole warps).
+    __device__ __forceinline__ static void lsync(int bar) {
+        if constexpr (TPL % 32 == 0) {
+            if (bar > 0) {
+                asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "n"(TPL) : "memory");
+                return;
+            }
+        }
+        __syncthreads();
+    }
+
     template <int s>
-    __device__ __forceinline__ static void run_from(C* v, C* line, int lt, const C* __restrict__ tw) {
+    __device__ __forceinline__ static void run_from(C* v, C* line, int lt, const C* __restrict__ tw, int bar) {
         if constexpr (s < S) {
-            __syncthreads();
+            lsync(bar);
             write_out<s - 1>(line, v, lt);
-            __syncthreads();
+            lsync(bar);
             read_in<s>(line, v, lt);
             compute<s>(v, lt, tw);
-            run_from<s + 1>(v, line, lt, tw);
+            run_from<s + 1>(v, line, lt, tw, bar);
         }
     }
 
     // v holds the step-0 inputs (pos_in layout) -> v holds the outputs (pos_out layout)
-    __device__ __forceinline__ static void run(C* v, C* line, int lt, const C* __restrict__ tw) {
+    __device__ __forceinline__ static void run(C* v, C* line, int lt, const C* __restrict__ tw, int bar = 0) {
         compute<0>(v, lt, tw);
-        run_from<1>(v, line, lt, tw);
+        run_from<1>(v, line, lt, tw, bar);
     }
 };
 
@@ -157,10 +170,29 @@ __device__ __forceinline__ int64_t row_index(int64_t row, int64_t v, int64_t R, 
     return sh < 0 ? row * R + v : ((((v >> sh) * batch + row) << sh) | (v & ((1ll << sh) - 1)));
 }
 
-template <typename T, int R, int E, int W, bool INV, bool REAL_IN>
+// FILT: a row filter pass of the separable pipeline: forward
+// transform -> * rowfilt[v] * scale -> inverse transform, stored unscaled.
+template <typename T, int R, int E, bool FILT, int LAYOUT = 0>
+__device__ __forceinline__ void row_filter_pass(cpx<T>* v, cpx<T>* line, int lt, const cpx<T>* __restrict__ tw,
+                                                const T* __restrict__ rowfilt, T& scale, int bar = 0) {
+    if constexpr (FILT) {
+        using F = LineFFT<T, R, E, false, LAYOUT>;
+        using FI = LineFFT<T, R, E, true, LAYOUT>;
+        cpx<T> w[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+            w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], __ldg(rowfilt + lt + F::TPL * m) * scale);
+        FI::run(w, line, lt, tw, bar);
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[F::pos_out(m)] = w[FI::pos_out(m)];
+        scale = (T)1;
+    }
+}
+
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN, bool FILT = false>
 __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_, cpx<T>* __restrict__ out,
                                                     int64_t batch, T scale, const cpx<T>* __restrict__ tw,
-                                                    int in_sh, int out_sh) {
+                                                    int in_sh, int out_sh, const T* __restrict__ rowfilt) {
     using C = cpx<T>;
     using F = LineFFT<T, R, E, INV>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -194,6 +226,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_
         }
     }
     F::run(v, smem + t * F::LS, lt, tw);
+    row_filter_pass<T, R, E, FILT>(v, smem + t * F::LS, lt, tw, rowfilt, scale);
     if (valid) {
         if (out_sh < 0) {
             C* o = out + row * R + lt;
@@ -232,6 +265,8 @@ __device__ __forceinline__ T filter_value(const FilterArgs& f, int64_t u, int64_
     } else if (f.kind == 3) {
         const double ku = (double)(u < f.N / 2 ? u : u - f.N), kv = (double)(v < f.M / 2 ? v : v - f.M);
         return (ku * ku + kv * kv <= f.b2) ? (T)1 : (T)0;
+    } else if (f.kind == 5) {  // column factor of a separable filter (the row factor ran in k_rows)
+        return __ldg(reinterpret_cast<const T*>(f.gu) + u);
     }
     return (T)1;
 }
@@ -284,7 +319,9 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
     C v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
-    F::run(v, line, lt, tw);
+    // lines synchronise on their own named barrier (1 + t) between steps
+    const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
+    F::run(v, line, lt, tw, bar);
     if constexpr (MODE == 2) {
         C w[E];
         const int64_t col = s0 + t;
@@ -294,12 +331,12 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
             const T h = (col < S) ? filter_value<T>(filt, u, col + filt.col_off) * scale : (T)0;
             w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], h);
         }
-        FI::run(w, line, lt, tw);
-        __syncthreads();
+        FI::run(w, line, lt, tw, bar);
+        F::lsync(bar);
 #pragma unroll
         for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = w[FI::pos_out(m)];
     } else {
-        __syncthreads();
+        F::lsync(bar);
 #pragma unroll
         for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = cscale(v[F::pos_out(m)], scale);
     }

@@ -40,19 +40,24 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         : "memory");
 }
 
+// Each row lands (one bulk copy per row) at the start of its padded line
+// region (LS = pad16(R) + 2 slots: even, so every row start is 16-B
+// aligned); step 0 reads it unpadded, every later exchange uses the padded
+// index (LineFFT LAYOUT 0) in place.
 template <typename T, int R, int W, bool REAL_IN, int STAGES>
 struct RowsTmaCfg {
-    static constexpr size_t STAGE_BYTES = sizeof(cpx<T>) * W * R;
+    static constexpr int LS = pad16c(R) + 2;
+    static constexpr size_t STAGE_BYTES = sizeof(cpx<T>) * W * LS;
     static constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 8 * STAGES;
     static constexpr uint32_t ROW_IN_BYTES = (uint32_t)(R * (REAL_IN ? sizeof(float) : sizeof(cpx<T>)));
 };
 
-template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES>
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false>
 __global__ void __launch_bounds__(W*(R / E), 1)
     k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
-               const cpx<T>* __restrict__ tw) {
+               const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt) {
     using C = cpx<T>;
-    using F = LineFFT<T, R, E, INV, 1>;
+    using F = LineFFT<T, R, E, INV, 0>;
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
     static_assert(R >= 256 && (R * sizeof(cpx<T>)) % 16 == 0, "bulk copies need >= 16 B rows");
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -65,10 +70,11 @@ __global__ void __launch_bounds__(W*(R / E), 1)
     auto issue = [&](int64_t tile, int s) {
         const int64_t r0 = tile * W;
         const int64_t nr = (batch - r0) < W ? (batch - r0) : W;
-        const uint32_t bytes = (uint32_t)(nr * G::ROW_IN_BYTES);
         const uint32_t bar = bar0 + 8 * s;
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s(smem_addr_u32(smem_raw + s * G::STAGE_BYTES), in + r0 * G::ROW_IN_BYTES, bytes, bar);
+        mbar_expect_tx(bar, (uint32_t)(nr * G::ROW_IN_BYTES));
+        const uint32_t dst = smem_addr_u32(smem_raw + s * G::STAGE_BYTES);
+        for (int64_t i = 0; i < nr; ++i)
+            bulk_g2s(dst + (uint32_t)(i * G::LS * sizeof(C)), in + (r0 + i) * G::ROW_IN_BYTES, G::ROW_IN_BYTES, bar);
     };
 
     if (tid == 0) {
@@ -86,22 +92,25 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         if (tile >= ntiles) break;
         const int s = (int)(k % STAGES);
         mbar_wait(bar0 + 8 * s, (uint32_t)((k / STAGES) & 1));
-        C* line = reinterpret_cast<C*>(smem_raw + s * G::STAGE_BYTES) + t * R;
+        C* line = reinterpret_cast<C*>(smem_raw + s * G::STAGE_BYTES) + t * G::LS;
         C v[E];
         if constexpr (REAL_IN) {
-            const float* fl = reinterpret_cast<const float*>(smem_raw + s * G::STAGE_BYTES) + t * R;
+            const float* fl = reinterpret_cast<const float*>(line);
 #pragma unroll
             for (int m = 0; m < E; ++m) v[F::pos_in(m)] = mk((T)fl[lt + F::TPL * m], (T)0);
         } else {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[lt + F::TPL * m];
         }
-        F::run(v, line, lt, tw);
+        const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
+        F::run(v, line, lt, tw, bar);
+        T sc = scale;
+        row_filter_pass<T, R, E, FILT, 0>(v, line, lt, tw, rowfilt, sc, bar);
         const int64_t row = tile * W + t;
         if (row < batch) {
             C* o = out + row * R + lt;
 #pragma unroll
-            for (int m = 0; m < E; ++m) o[F::TPL * m] = cscale(v[F::pos_out(m)], scale);
+            for (int m = 0; m < E; ++m) o[F::TPL * m] = cscale(v[F::pos_out(m)], sc);
         }
         __syncthreads();  // every thread is done with stage s
         if (tid == 0) {

@@ -1,5 +1,6 @@
 // kernels_cols.cu -- instantiations and launcher of kernel family B (columns,
 // and the fused column forward -> filter -> column inverse of the pipeline).
+#include "fft_cols_pipe.cuh"
 #include "fft_engine.cuh"
 #include "launch.h"
 
@@ -8,6 +9,56 @@
 namespace b200fft {
 
 namespace {
+
+// persistent double-buffered variant (fft_cols_pipe.cuh), complex64,
+// 256 <= R <= 4096: W columns per tile so that two tiles fit in smem
+template <int R> constexpr int pipe_w() { return R >= 4096 ? 2 : (R >= 2048 ? 4 : (R >= 1024 ? 8 : 16)); }
+
+template <int R, int MODE>
+cudaError_t cols_pipe_t(const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
+                        const FilterArgs& f, cudaStream_t st) {
+    constexpr int E = 16, W = pipe_w<R>();
+    using G = ColsPipeCfg<float, R, W>;
+    auto kern = k_cols_pipe<float, R, E, W, MODE>;
+    static int grid_max = 0;
+    if (!grid_max) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * (R / E), G::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        grid_max = sms * (occ > 0 ? occ : 1);
+    }
+    if (S <= 0 || nimg <= 0) return cudaSuccess;
+    const int64_t tiles = (S + W - 1) / W * nimg;
+    const int grid = (int)(tiles < grid_max ? tiles : grid_max);
+    kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out),
+                                                   S, nimg, (float)scale,
+                                                   reinterpret_cast<const float2*>(tw) + tw_base(R), f);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t cols_pipe_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
+                        const FilterArgs& f, cudaStream_t st) {
+    switch (R) {
+        case 256: return cols_pipe_t<256, MODE>(in, out, S, nimg, scale, tw, f, st);
+        case 512: return cols_pipe_t<512, MODE>(in, out, S, nimg, scale, tw, f, st);
+        case 1024: return cols_pipe_t<1024, MODE>(in, out, S, nimg, scale, tw, f, st);
+        case 2048: return cols_pipe_t<2048, MODE>(in, out, S, nimg, scale, tw, f, st);
+        case 4096: return cols_pipe_t<4096, MODE>(in, out, S, nimg, scale, tw, f, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool use_cols_pipe(int prec, int64_t R) {
+    static const bool off = [] {
+        const char* e = getenv("B200FFT_NO_COLPIPE");
+        return e && e[0] == '1';
+    }();
+    return !off && prec == 0 && R >= 256 && R <= 4096;
+}
 
 template <typename T> constexpr int cols_budget() { return sizeof(T) == 4 ? 16384 : 8192; }
 
@@ -82,6 +133,13 @@ cudaError_t cols_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg
 cudaError_t launch_cols(int prec, int mode, int64_t R, const void* in, void* out, int64_t S,
                         int64_t nimg, double scale, const void* tw, const FilterArgs& f,
                         cudaStream_t st) {
+    if (use_cols_pipe(prec, R)) {
+        switch (mode) {
+            case 0: return cols_pipe_r<0>(R, in, out, S, nimg, scale, tw, f, st);
+            case 1: return cols_pipe_r<1>(R, in, out, S, nimg, scale, tw, f, st);
+            case 2: return cols_pipe_r<2>(R, in, out, S, nimg, scale, tw, f, st);
+        }
+    }
     if (prec == 0) {
         switch (mode) {
             case 0: return cols_r<float, 0>(R, in, out, S, nimg, scale, tw, f, st);

@@ -1,4 +1,6 @@
-// kernels_rows.cu -- instantiations and launcher of kernel family A (rows).
+// kernels_rows.cu -- instantiations and launcher of kernel family A (rows):
+// the per-CTA k_rows (any R, any precision, blocked layouts) and the
+// persistent TMA-fed k_rows_tma (complex64, 256 <= R <= 8192, natural rows).
 #include <cstdlib>
 
 #include "fft_engine.cuh"
@@ -9,15 +11,15 @@ namespace b200fft {
 
 namespace {
 
-template <typename T, int R, bool INV, bool REAL_IN>
+template <typename T, int R, bool INV, bool REAL_IN, bool FILT>
 cudaError_t rows_t(const void* in, void* out, int64_t batch, double scale, const void* tw, int in_sh, int out_sh,
-                   cudaStream_t st) {
+                   const void* rowfilt, cudaStream_t st) {
     constexpr int E = R < 16 ? R : 16;
     constexpr int TPL = R / E;
     constexpr int W = TPL >= 256 ? 1 : 256 / TPL;
     using F = LineFFT<T, R, E, INV>;
     constexpr size_t smem = sizeof(cpx<T>) * W * F::LS;
-    auto kern = k_rows<T, R, E, W, INV, REAL_IN>;
+    auto kern = k_rows<T, R, E, W, INV, REAL_IN, FILT>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -27,16 +29,17 @@ cudaError_t rows_t(const void* in, void* out, int64_t batch, double scale, const
     if (batch <= 0) return cudaSuccess;
     const int64_t grid = (batch + W - 1) / W;
     kern<<<(unsigned)grid, W * TPL, smem, st>>>(in, reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
-                                                 reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), in_sh, out_sh);
+                                                 reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), in_sh, out_sh,
+                                                 reinterpret_cast<const T*>(rowfilt));
     return cudaGetLastError();
 }
 
-template <typename T, bool INV, bool REAL_IN>
+template <typename T, bool INV, bool REAL_IN, bool FILT>
 cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw, int in_sh,
-                   int out_sh, cudaStream_t st) {
+                   int out_sh, const void* rowfilt, cudaStream_t st) {
     switch (R) {
 #define B200_ROWS_CASE(r) \
-    case r: return rows_t<T, r, INV, REAL_IN>(in, out, batch, scale, tw, in_sh, out_sh, st);
+    case r: return rows_t<T, r, INV, REAL_IN, FILT>(in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st);
         B200_ROWS_CASE(1) B200_ROWS_CASE(2) B200_ROWS_CASE(4) B200_ROWS_CASE(8) B200_ROWS_CASE(16)
         B200_ROWS_CASE(32) B200_ROWS_CASE(64) B200_ROWS_CASE(128) B200_ROWS_CASE(256)
         B200_ROWS_CASE(512) B200_ROWS_CASE(1024) B200_ROWS_CASE(2048) B200_ROWS_CASE(4096)
@@ -47,13 +50,14 @@ cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double s
 }
 
 // persistent TMA-fed variant (fft_tma.cuh): 3 stages of ~64 KiB, 512 threads
-template <typename T, int R, bool INV, bool REAL_IN>
-cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw, cudaStream_t st) {
+template <typename T, int R, bool INV, bool REAL_IN, bool FILT>
+cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw, const void* rowfilt,
+                       cudaStream_t st) {
     constexpr int E = 16;
     constexpr int W = (int)((64 * 1024) / (R * sizeof(cpx<T>))) < 1 ? 1 : (int)((64 * 1024) / (R * sizeof(cpx<T>)));
     constexpr int STAGES = 3;
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
-    auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES>;
+    auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT>;
     static int grid_max = 0;
     if (!grid_max) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
@@ -68,20 +72,21 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     const int64_t tiles = (batch + W - 1) / W;
     const int grid = (int)(tiles < grid_max ? tiles : grid_max);
     kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(in, reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
-                                                   reinterpret_cast<const cpx<T>*>(tw) + tw_base(R));
+                                                   reinterpret_cast<const cpx<T>*>(tw) + tw_base(R),
+                                                   reinterpret_cast<const T*>(rowfilt));
     return cudaGetLastError();
 }
 
-template <bool INV, bool REAL_IN>
+template <bool INV, bool REAL_IN, bool FILT>
 cudaError_t rows_tma_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw,
-                       cudaStream_t st) {
+                       const void* rowfilt, cudaStream_t st) {
     switch (R) {
-        case 256: return rows_tma_t<float, 256, INV, REAL_IN>(in, out, batch, scale, tw, st);
-        case 512: return rows_tma_t<float, 512, INV, REAL_IN>(in, out, batch, scale, tw, st);
-        case 1024: return rows_tma_t<float, 1024, INV, REAL_IN>(in, out, batch, scale, tw, st);
-        case 2048: return rows_tma_t<float, 2048, INV, REAL_IN>(in, out, batch, scale, tw, st);
-        case 4096: return rows_tma_t<float, 4096, INV, REAL_IN>(in, out, batch, scale, tw, st);
-        case 8192: return rows_tma_t<float, 8192, INV, REAL_IN>(in, out, batch, scale, tw, st);
+        case 256: return rows_tma_t<float, 256, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 512: return rows_tma_t<float, 512, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 1024: return rows_tma_t<float, 1024, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 2048: return rows_tma_t<float, 2048, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 4096: return rows_tma_t<float, 4096, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 8192: return rows_tma_t<float, 8192, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -97,22 +102,32 @@ bool use_tma_rows(int prec, int64_t R, int in_sh, int out_sh) {
 }  // namespace
 
 cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void* in, void* out,
-                        int64_t batch, double scale, const void* tw, cudaStream_t st, int in_sh, int out_sh) {
-    // in == out is safe: every tile is read (prefetched) by the CTA that later
-    // writes it, and no other CTA touches it
+                        int64_t batch, double scale, const void* tw, cudaStream_t st, int in_sh, int out_sh,
+                        const void* rowfilt) {
+    if (rowfilt && inv) return cudaErrorInvalidValue;  // filter passes start with the forward transform
+    // in == out is safe for the TMA kernel: every tile is read (prefetched)
+    // by the CTA that later writes it, and no other CTA touches it
     if (use_tma_rows(prec, R, in_sh, out_sh)) {
-        if (real_in) return rows_tma_r<false, true>(R, in, out, batch, scale, tw, st);
-        return inv ? rows_tma_r<true, false>(R, in, out, batch, scale, tw, st)
-                   : rows_tma_r<false, false>(R, in, out, batch, scale, tw, st);
+        if (rowfilt)
+            return real_in ? rows_tma_r<false, true, true>(R, in, out, batch, scale, tw, rowfilt, st)
+                           : rows_tma_r<false, false, true>(R, in, out, batch, scale, tw, rowfilt, st);
+        if (real_in) return rows_tma_r<false, true, false>(R, in, out, batch, scale, tw, nullptr, st);
+        return inv ? rows_tma_r<true, false, false>(R, in, out, batch, scale, tw, nullptr, st)
+                   : rows_tma_r<false, false, false>(R, in, out, batch, scale, tw, nullptr, st);
     }
     if (prec == 0) {
-        if (real_in) return rows_r<float, false, true>(R, in, out, batch, scale, tw, in_sh, out_sh, st);
-        return inv ? rows_r<float, true, false>(R, in, out, batch, scale, tw, in_sh, out_sh, st)
-                   : rows_r<float, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, st);
+        if (rowfilt)
+            return real_in ? rows_r<float, false, true, true>(R, in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st)
+                           : rows_r<float, false, false, true>(R, in, out, batch, scale, tw, in_sh, out_sh, rowfilt,
+                                                               st);
+        if (real_in) return rows_r<float, false, true, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st);
+        return inv ? rows_r<float, true, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st)
+                   : rows_r<float, false, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st);
     }
     if (real_in) return cudaErrorInvalidValue;
-    return inv ? rows_r<double, true, false>(R, in, out, batch, scale, tw, in_sh, out_sh, st)
-               : rows_r<double, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, st);
+    if (rowfilt) return rows_r<double, false, false, true>(R, in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st);
+    return inv ? rows_r<double, true, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st)
+               : rows_r<double, false, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st);
 }
 
 }  // namespace b200fft

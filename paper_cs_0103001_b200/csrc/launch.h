@@ -14,9 +14,11 @@ constexpr int64_t kColsMax[2] = {8192, 4096};
 // Kernel family A: batch contiguous rows of length R (power of two <= 8192).
 // in_sh / out_sh >= 0: rows stored in column blocks of 2^sh (all-to-all pack
 // layout, fft_engine.cuh row_index); -1: natural row-major.
+// rowfilt (T[R], optional): the separable-pipeline row pass, forward ->
+// * rowfilt[v] * scale -> inverse, stored unscaled (inv must be false).
 cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void* in, void* out,
                         int64_t batch, double scale, const void* tw, cudaStream_t st, int in_sh = -1,
-                        int out_sh = -1);
+                        int out_sh = -1, const void* rowfilt = nullptr);
 
 // Kernel family B: column transforms of nimg grids [R][S]; mode 0 fwd, 1 inv,
 // 2 fwd -> filter*scale -> inv.

@@ -332,7 +332,26 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
         f.b2 = param * param;
     }
     const bool real_in = (p->flags & FFT_IN_REAL_F32) != 0;
-    cudaError_t e = launch_rows(p->prec, false, real_in, M, in, out, p->batch * N, 1.0, p->tw, st);
+    cudaError_t e;
+    // Separable filter (the Gaussian, H = g_N(u) g_M(v)): the row and column
+    // operators commute, so IDFT2(H DFT2 f) = [IDFT_c g_N DFT_c][IDFT_r g_M
+    // DFT_r] f exactly -- two fused passes (rows fwd*g*inv, then columns
+    // fwd*g*inv), 32 B/point of HBM instead of 48 (DESIGN.md "Separable
+    // pipeline").  B200FFT_PIPE_LITERAL=1 keeps the three-pass order.
+    const char* lit_env = getenv("B200FFT_PIPE_LITERAL");
+    const bool literal = lit_env && lit_env[0] == '1';
+    if (filter == FFT_FILTER_GAUSS && !literal) {
+        e = launch_rows(p->prec, false, real_in, M, in, out, p->batch * N, 1.0 / (double)M, p->tw, st, -1, -1,
+                        p->gv);
+        if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
+        FilterArgs fc = f;
+        fc.kind = 5;
+        e = launch_cols(p->prec, 2, N, out, out, M, p->batch, 1.0 / (double)N, p->tw, fc, st);
+        if (e != cudaSuccess) return cuda_fail(e, "k_cols launch");
+        p->last_launches = 2;
+        return FFT_OK;
+    }
+    e = launch_rows(p->prec, false, real_in, M, in, out, p->batch * N, 1.0, p->tw, st);
     if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
     e = launch_cols(p->prec, 2, N, out, out, M, p->batch, 1.0 / ((double)N * (double)M), p->tw, f, st);
     if (e != cudaSuccess) return cuda_fail(e, "k_cols launch");

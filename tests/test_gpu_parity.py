@@ -191,6 +191,21 @@ def test_gauss_pipeline(fft, dtype, N, M):
     assert oracle.rel_l2(out, oracle.gauss_pipeline(f, 0.1)) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("N,M", [(64, 64), (128, 32), (2048, 2048)])
+def test_gauss_pipeline_literal_three_pass_order(fft, N, M, monkeypatch):
+    """The literal order 2D-FFT -> x H -> 2D-IFFT (rows, fused columns, rows),
+    i.e. the separable fast path disabled, against the oracle."""
+    import paper_cs_0103001_b200 as b
+
+    monkeypatch.setenv("B200FFT_PIPE_LITERAL", "1")
+    f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=410 + N, dtype=np.complex64).reshape(N, M)
+    out = run_pipeline(b, f, b.FILTER_GAUSS, 0.1)
+    assert oracle.rel_l2(out, oracle.gauss_pipeline(f, 0.1)) <= 1e-5
+    img = fixtures.sky_image(256, 256, seed=3, nsrc=20)
+    out = run_pipeline(b, img, b.FILTER_GAUSS, 0.1, real=True)
+    assert oracle.rel_l2(out, oracle.gauss_pipeline(img.astype(np.complex128), 0.1)) <= 1e-5
+
+
 def ideal_mask(N, M, b_, literal):
     u = np.arange(N)[:, None]
     v = np.arange(M)[None, :]
