@@ -36,8 +36,8 @@ __global__ void __launch_bounds__(W*(R / E), 1)
                 const cpx<T>* __restrict__ tw, FilterArgs filt) {
     using C = cpx<T>;
     constexpr bool INV0 = (MODE == 1);
-    using F = LineFFT<T, R, E, INV0>;
-    using FI = LineFFT<T, R, E, true>;
+    using F = LineFFT<T, R, E, INV0, 0, true>;
+    using FI = LineFFT<T, R, E, true, 0, true>;
     using G = ColsPipeCfg<T, R, W>;
     constexpr int NT = W * F::TPL;
     constexpr int LSC = G::LSC;

@@ -31,7 +31,9 @@ constexpr int RMAX = 8192;  // largest in-CTA DFT
 // consecutive and the stride-16 access patterns of the steps conflict-free
 __device__ __forceinline__ int swz16(int i) { return i ^ ((i >> 4) & 15); }
 
-template <typename T, int R, int E, bool INV, int LAYOUT = 0>
+// PF: prefetch each step's twiddles into registers before its exchange
+// barriers (for kernels with a 128-register budget)
+template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false>
 struct LineFFT {
     using C = cpx<T>;
     static constexpr int TPL = R / E;
@@ -64,6 +66,39 @@ struct LineFFT {
                     v[b * rho + r] = cmul_dir<INV>(v[b * rho + r], w);
                 }
             }
+            dft<rho, INV>(v + b * rho);
+        }
+    }
+
+    // Twiddles of step s prefetched into registers (issued before the
+    // exchange barriers of the step, so their latency hides behind them) when
+    // they are few enough: (rho - 1) * nb <= 16 complex values.
+    template <int s>
+    static constexpr int ntw() {
+        return (span_at(R, s) > 1) ? (radix_at(R, s) - 1) * (E / radix_at(R, s)) : 0;
+    }
+    template <int s>
+    static constexpr bool prefetch_tw() {
+        return PF && ntw<s>() > 0 && ntw<s>() <= 16;
+    }
+    template <int s>
+    __device__ __forceinline__ static void load_tw(C* w, int lt, const C* __restrict__ tw) {
+        constexpr int rho = radix_at(R, s), Ns = span_at(R, s), nb = E / rho;
+#pragma unroll
+        for (int b = 0; b < nb; ++b) {
+            const int k = (lt + b * TPL) & (Ns - 1);
+            const C* __restrict__ ts = tw + tw_off(R, s) + k;
+#pragma unroll
+            for (int r = 1; r < rho; ++r) w[b * (rho - 1) + r - 1] = __ldg(ts + (r - 1) * Ns);
+        }
+    }
+    template <int s>
+    __device__ __forceinline__ static void compute_tw(C* v, const C* w) {
+        constexpr int rho = radix_at(R, s), nb = E / rho;
+#pragma unroll
+        for (int b = 0; b < nb; ++b) {
+#pragma unroll
+            for (int r = 1; r < rho; ++r) v[b * rho + r] = cmul_dir<INV>(v[b * rho + r], w[b * (rho - 1) + r - 1]);
             dft<rho, INV>(v + b * rho);
         }
     }
@@ -141,11 +176,21 @@ struct LineFFT {
     template <int s>
     __device__ __forceinline__ static void run_from(C* v, C* line, int lt, const C* __restrict__ tw, int bar) {
         if constexpr (s < S) {
-            lsync(bar);
-            write_out<s - 1>(line, v, lt);
-            lsync(bar);
-            read_in<s>(line, v, lt);
-            compute<s>(v, lt, tw);
+            if constexpr (prefetch_tw<s>()) {
+                C w[ntw<s>()];
+                load_tw<s>(w, lt, tw);
+                lsync(bar);
+                write_out<s - 1>(line, v, lt);
+                lsync(bar);
+                read_in<s>(line, v, lt);
+                compute_tw<s>(v, w);
+            } else {
+                lsync(bar);
+                write_out<s - 1>(line, v, lt);
+                lsync(bar);
+                read_in<s>(line, v, lt);
+                compute<s>(v, lt, tw);
+            }
             run_from<s + 1>(v, line, lt, tw, bar);
         }
     }
@@ -172,12 +217,12 @@ __device__ __forceinline__ int64_t row_index(int64_t row, int64_t v, int64_t R, 
 
 // FILT: a row filter pass of the separable pipeline: forward
 // transform -> * rowfilt[v] * scale -> inverse transform, stored unscaled.
-template <typename T, int R, int E, bool FILT, int LAYOUT = 0>
+template <typename T, int R, int E, bool FILT, int LAYOUT = 0, bool PF = false>
 __device__ __forceinline__ void row_filter_pass(cpx<T>* v, cpx<T>* line, int lt, const cpx<T>* __restrict__ tw,
                                                 const T* __restrict__ rowfilt, T& scale, int bar = 0) {
     if constexpr (FILT) {
-        using F = LineFFT<T, R, E, false, LAYOUT>;
-        using FI = LineFFT<T, R, E, true, LAYOUT>;
+        using F = LineFFT<T, R, E, false, LAYOUT, PF>;
+        using FI = LineFFT<T, R, E, true, LAYOUT, PF>;
         cpx<T> w[E];
 #pragma unroll
         for (int m = 0; m < E; ++m)
