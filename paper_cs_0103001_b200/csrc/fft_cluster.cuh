@@ -540,6 +540,145 @@ __global__ void __launch_bounds__(256, 4)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Variant 4: persistent, software-pipelined cluster kernel.  Each 16-CTA
+// cluster loops over transforms; iteration i runs (A)+(T) of transform i,
+// pushes it (st.async, rank-rotated) into slot i%2 of the owners' receive
+// buffers, and only THEN runs (B) of transform i-1 -- so the DSMEM transfer
+// of i overlaps the row work of i-1 instead of being waited for.
+// Per slot: full[s] (owner side; 1 arrival = the owner's expect_tx + the
+// peers' bytes) and empty[s] (sender side; 16 remote arrivals, one per owner
+// that has consumed the slot).  Specialised to N1 = N2 = 256, C = 16, E = 16.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity_cta(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "W4_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W4_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+template <typename T>
+struct Cluster4Cfg {
+    using G = ClusterCfg<T, 256, 256, 16, 16>;
+    static constexpr size_t A_BYTES = sizeof(cpx<T>) * G::WA * G::LSA;
+    static constexpr size_t RX_BYTES_SLOT = sizeof(cpx<T>) * G::WB * G::LSB;
+    static constexpr size_t BAR_OFF = A_BYTES + 2 * RX_BYTES_SLOT;
+    static constexpr size_t SMEM_BYTES = BAR_OFF + 64;
+    static constexpr uint32_t PAYLOAD = (uint32_t)(sizeof(cpx<T>) * 16 * 256);
+};
+
+template <typename T, int MINB, bool INV>
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, MINB)
+    k_cluster4(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, int64_t batch, T scale,
+               const cpx<T>* __restrict__ tw4, const cpx<T>* __restrict__ twa, const cpx<T>* __restrict__ twb) {
+    constexpr int N1 = 256, N2 = 256, E = 16;
+    using Cx = cpx<T>;
+    using G = ClusterCfg<T, N1, N2, 16, E>;
+    using H = Cluster4Cfg<T>;
+    using FA = LineFFT<T, N2, E, INV>;
+    using FB = LineFFT<T, N1, E, INV>;
+    constexpr int64_t N = (int64_t)N1 * N2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Cx* bufa = reinterpret_cast<Cx*>(smem_raw);
+    const uint32_t rx_s0 = smem_u32(smem_raw + H::A_BYTES);
+    const uint32_t full0 = smem_u32(smem_raw + H::BAR_OFF);       // full[0], full[1]
+    const uint32_t empty0 = full0 + 16;                            // empty[0], empty[1]
+    namespace cg = cooperative_groups;
+    const int c = (int)cg::this_cluster().block_rank();
+    const int64_t cid = (int64_t)blockIdx.x / 16, ncl = (int64_t)gridDim.x / 16;
+    const int tid = threadIdx.x;
+    const int t = tid & 15, la = tid >> 4;  // phase A: line t (column), lane la
+    const int n1 = c * 16 + t;
+    const int64_t iters = (batch - cid + ncl - 1) / ncl;  // transforms of this cluster
+
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(full0 + 8 * s), "r"(1) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(empty0 + 8 * s), "r"(16) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        for (int s = 0; s < 2; ++s)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(full0 + 8 * s),
+                         "r"(H::PAYLOAD)
+                         : "memory");
+    }
+    cluster_arrive_relaxed();
+    bool cluster_synced = false;
+
+    Cx v[E];
+    auto phase_b = [&](int64_t j) {  // rows of transform j (iteration j of this cluster)
+        const int s = (int)(j & 1);
+        const uint32_t u = (uint32_t)(j >> 1);
+        mbar_wait_parity_cta(full0 + 8 * s, u & 1);
+        Cx* rx = reinterpret_cast<Cx*>(smem_raw + H::A_BYTES + s * H::RX_BYTES_SLOT);
+        const int tb = tid & 15, lb = tid >> 4;
+        Cx* lineb = rx + tb * G::LSB;
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[FB::pos_in(m)] = lineb[FB::bpos(lb, m)];
+        FB::run(v, lineb, lb, twb);
+        const int64_t b = cid + j * ncl;
+        const int k2 = c * 16 + tb;
+        Cx* dst = out + b * N;
+#pragma unroll
+        for (int m = 0; m < E; ++m) dst[k2 + (int64_t)N2 * (lb + 16 * m)] = cscale(v[FB::pos_out(m)], scale);
+        __syncthreads();  // everyone is done with slot s
+        if (j + 2 < iters) {
+            if (tid == 0)  // re-arm this slot's next phase before releasing it
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(full0 + 8 * s),
+                             "r"(H::PAYLOAD)
+                             : "memory");
+            __syncthreads();
+            if (tid < 16) mbar_arrive_remote(mapa_u32(empty0 + 8 * s, (uint32_t)tid));
+        }
+    };
+
+    for (int64_t i = 0; i < iters; ++i) {
+        const int64_t b = cid + i * ncl;
+        const Cx* src = in + b * N;
+        // ---- (A) + (T) of transform i ----
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[FA::pos_in(m)] = src[n1 + (int64_t)N1 * (la + 16 * m)];
+        FA::run(v, bufa + t * G::LSA, la, twa);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int k2 = la + 16 * m;
+            v[FA::pos_out(m)] = cmul_dir<INV>(v[FA::pos_out(m)], __ldg(tw4 + (int64_t)k2 * N1 + n1));
+        }
+        if (!cluster_synced) {
+            cluster_wait_acquire();  // every peer's mbarriers are initialised
+            cluster_synced = true;
+        }
+        // ---- push into slot i%2 of the owners, once they have freed it ----
+        const int s = (int)(i & 1);
+        const uint32_t u = (uint32_t)(i >> 1);
+        if (u >= 1) mbar_wait_parity_cta(empty0 + 8 * s, (u - 1) & 1);
+        const uint32_t rx_s = rx_s0 + (uint32_t)(s * H::RX_BYTES_SLOT);
+#pragma unroll
+        for (int mm = 0; mm < E; ++mm) {
+            const int m = (mm + c) & (E - 1);
+            const uint32_t owner = (uint32_t)m, line = (uint32_t)la;  // k2 = la + 16 m
+            const uint32_t laddr = rx_s + (uint32_t)sizeof(Cx) * (line * G::LSB + pad16(n1));
+            st_async_v2(mapa_u32(laddr, owner), pick_out<0, E, FA>(v, m), mapa_u32(full0 + 8 * s, owner));
+        }
+        __syncthreads();  // bufa is reused by the next (A); v is free
+        // ---- (B) of the previous transform overlaps the transfer of this one ----
+        if (i >= 1) phase_b(i - 1);
+    }
+    if (iters >= 1) phase_b(iters - 1);
+    if (!cluster_synced) cluster_wait_acquire();
+    // no CTA leaves while a peer may still signal or send to it
+    cluster_arrive_release();
+    cluster_wait_acquire();
+}
+
 template <typename T>
 constexpr size_t cluster3_smem() {
     using G = ClusterCfg<T, 256, 256, 16, 16>;

@@ -145,6 +145,41 @@ cudaError_t fused_ab_t(const void* in, void* out, int64_t batch, double scale, c
     return cudaGetLastError();
 }
 
+template <typename T, int MINB, bool INV>
+cudaError_t cluster4_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                       cudaStream_t st) {
+    using H = Cluster4Cfg<T>;
+    auto kern = k_cluster4<T, MINB, INV>;
+    static int max_clusters = 0;
+    if (!max_clusters) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM_BYTES);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 16;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(16 * 64, 1, 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.dynamicSmemBytes = H::SMEM_BYTES;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        if (e != cudaSuccess) return e;
+        max_clusters = n > 0 ? n : 1;
+    }
+    if (batch <= 0) return cudaSuccess;
+    const int64_t ncl = batch < max_clusters ? batch : max_clusters;
+    const cpx<T>* t = reinterpret_cast<const cpx<T>*>(tw);
+    kern<<<(unsigned)(ncl * 16), 256, H::SMEM_BYTES, st>>>(reinterpret_cast<const cpx<T>*>(in),
+                                                          reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
+                                                          reinterpret_cast<const cpx<T>*>(tw4), t + tw_base(256),
+                                                          t + tw_base(256));
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2) {
@@ -181,6 +216,7 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 13: return step_ab_t<float, 16, 16, 16, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 14: return step_ab_t<float, 32, 32, 16, 2, INV>(in, out, batch, scale, tw4, tw, st);
         case 15: return fused_ab_t<float, INV>(in, out, batch, scale, tw4, tw, st);
+        case 18: return cluster4_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
         default: return cudaErrorInvalidValue;
     }
 }

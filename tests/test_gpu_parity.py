@@ -80,6 +80,77 @@ def test_1d_65536_multipass_fallback(fft, dtype, monkeypatch):
     assert oracle.rel_l2(run_1d(fft, x, inverse=True), oracle.fft_batch(x, inverse=True)) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("case", ["1d-8", "1d-2048", "1d-8192", "1d-65536", "1d-2^17", "1d-2^21",
+                                  "2d-256x512", "pipe-2048-real", "pipe-8192x16", "pipe-literal",
+                                  "dist2d-4", "dist1d-4"])
+def test_no_writes_outside_the_buffers(fft, case):
+    """Canary bounds check (compute-sanitizer is not available on this pool):
+    every call runs on the interior of a buffer whose 64 KiB guard zones on
+    both sides hold a sentinel, for output and input; the guards must come
+    back untouched and the input unchanged when out != in."""
+    import paper_cs_0103001_b200 as b
+
+    G = 8192  # guard elements (complex64) = 64 KiB
+    kind, _, rest = case.partition("-")
+
+    def guarded(n, dtype=torch.complex64):
+        buf = torch.full((n + 2 * G,), complex(1.2345e6, -6.789e5), dtype=dtype, device="cuda")
+        return buf, buf[G:G + n]
+
+    def check(buf, n):
+        ref = torch.tensor(complex(1.2345e6, -6.789e5), dtype=buf.dtype)
+        assert bool((buf[:G].cpu() == ref).all()) and bool((buf[G + n:].cpu() == ref).all())
+
+    if kind == "1d":
+        n = {"8": 8, "2048": 2048, "8192": 8192, "65536": 65536, "2^17": 1 << 17, "2^21": 1 << 21}[rest]
+        batch = 3 if n <= 65536 else (2 if n < (1 << 21) else 1)
+        p = b.Plan((n,), batch=batch)
+        shapes = [(n * batch, lambda x, y: p.forward(x, y)), (n * batch, lambda x, y: p.inverse(x, y))]
+    elif kind == "dist1d":
+        n = 1 << 16
+        p = b.Plan((n,), batch=1)
+        p.set_virtual_ranks(4)
+        shapes = [(n, lambda x, y: p.forward(x, y))]
+    elif kind == "2d" or kind == "dist2d":
+        N, M = (256, 512)
+        p = b.Plan((N, M))
+        if kind == "dist2d":
+            p.set_virtual_ranks(4)
+        shapes = [(N * M, lambda x, y: p.forward(x, y)),
+                  (N * M, lambda x, y: p.filter_pipeline(x, y, b.FILTER_GAUSS, 0.1))]
+    else:  # pipelines
+        if rest == "2048-real":
+            N = M = 2048
+            p = b.Plan((N, M), flags=b.IN_REAL_F32)
+            fin = torch.full((N * M + 2 * G,), 7.5, device="cuda")
+            fin[G:G + N * M] = torch.rand(N * M, device="cuda")
+            obuf, o = guarded(N * M)
+            before = fin.clone()
+            p.filter_pipeline(fin[G:G + N * M], o, b.FILTER_GAUSS, 0.1)
+            torch.cuda.synchronize()
+            check(obuf, N * M)
+            assert torch.equal(fin, before)
+            return
+        if rest == "8192x16":
+            N, M = 8192, 16
+            p = b.Plan((N, M))
+        else:
+            N, M = 128, 64
+            p = b.Plan((N, M))
+        shapes = [(N * M, lambda x, y: p.filter_pipeline(x, y, b.FILTER_IDEAL_LITERAL if rest == "literal"
+                                                         else b.FILTER_GAUSS, 30.0 if rest == "literal" else 0.1))]
+    for n, call in shapes:
+        ibuf, x = guarded(n)
+        x.copy_(torch.randn(n, dtype=torch.complex64, device="cuda"))
+        obuf, y = guarded(n)
+        before = ibuf.clone()
+        call(x, y)
+        torch.cuda.synchronize()
+        check(obuf, n)
+        assert torch.equal(ibuf, before)  # out != in: the input is read only
+    p.destroy()
+
+
 def test_c1_config(fft):
     """BASELINE configs[0]: N=1024, batch 1, complex128, U[-1,1], seed 1;
     forward (1/N) then inverse round trip."""
