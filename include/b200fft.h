@@ -85,8 +85,11 @@ enum {
     /* fft2d_filter_pipeline input is float32 real [N][M] (promoted to complex
      * in the first pass's load, BASELINE configs[2]); output stays complex. */
     FFT_IN_REAL_F32 = 1u << 1,
-    /* distributed 1D: leave the output in the four-step transposed order
-     * X[k1 + N1 k2] stored at [k1][k2] (one all-to-all less).  */
+    /* distributed single 1D transform (n = N1 N2, N1 = 2^ceil(m/2),
+     * N2 = 2^floor(m/2)), fft_forward only: rank r keeps the four-step
+     * transposed order -- X[k2 + N2 k1] for k2 in [r N2/P, (r+1) N2/P) at
+     * local index (k2 - r N2/P) N1 + k1 -- one all-to-all less.  Ignored by
+     * fft_inverse (its input is always in natural order). */
     FFT_OUT_TRANSPOSED = 1u << 0
 };
 

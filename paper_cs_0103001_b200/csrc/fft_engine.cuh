@@ -425,21 +425,32 @@ __global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ i
     C* dst = out + bidx * L;
     const int64_t KLO = (int64_t)1 << klo_sh;
     const int64_t nhi = Ns >> klo_sh;
-
-    // fully unrolled so that all of a thread's loads are in flight at once
+    // Thread tid always handles tile line tt = tid % W and elements
+    // r = tid / W + it * RS (RS = NT / W = TPL, a multiple of 16 for R >= 256):
+    // one base address per thread and constant strides per iteration.
+    constexpr int RS = NT / W;
+    static_assert(NT % W == 0, "tile shape");
+    const int tt = tid % W, r0 = tid / W;
+    const int64_t jt = j0 + tt;
+    const int64_t kt = jt & (Ns - 1);
+    {
+        const C* s = src + jt + (int64_t)r0 * LR;
+        const int64_t sstep = (int64_t)RS * LR;
+        const C* wa = pa + (int64_t)r0 * KLO + (kt & (KLO - 1));
+        const C* wb = pb + (int64_t)r0 * nhi + (kt >> klo_sh);
+        C* d = smem + tt * F::LS;
+        const int pr0 = pad16(r0);
+        // fully unrolled so that all of a thread's loads are in flight at once
 #pragma unroll
-    for (int it = 0; it < (W * R) / NT; ++it) {
-        const int idx = tid + it * NT;
-        const int tt = idx % W, r = idx / W;
-        const int64_t j = j0 + tt;
-        C a = src[j + (int64_t)r * LR];
-        if (Ns > 1) {
-            const int64_t k = j & (Ns - 1);
-            C w = __ldg(pa + (int64_t)r * KLO + (k & (KLO - 1)));
-            if (nhi > 1) w = cmul(w, __ldg(pb + (int64_t)r * nhi + (k >> klo_sh)));
-            a = cmul_dir<INV>(a, w);
+        for (int it = 0; it < (W * R) / NT; ++it) {
+            C a = s[it * sstep];
+            if (Ns > 1) {
+                C w = __ldg(wa + (int64_t)it * RS * KLO);
+                if (nhi > 1) w = cmul(w, __ldg(wb + (int64_t)it * RS * nhi));
+                a = cmul_dir<INV>(a, w);
+            }
+            d[(RS % 16 == 0) ? pr0 + it * (RS + RS / 16) : pad16(r0 + it * RS)] = a;
         }
-        smem[tt * F::LS + pad16(r)] = a;
     }
     __syncthreads();
     C* line = smem + t * F::LS;
@@ -451,23 +462,20 @@ __global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ i
 #pragma unroll
     for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = cscale(v[F::pos_out(m)], scale);
     __syncthreads();
-    if (Ns >= W) {
-        // fully unrolled so that all of a thread's loads are in flight at once
+    if (Ns >= W) {  // consecutive threads -> consecutive k: W-element runs per q
+        C* d = dst + (jt - kt) * R + kt + (int64_t)r0 * Ns;
+        const C* sm = smem + tt * F::LS;
+        const int pq0 = pad16(r0);
 #pragma unroll
-    for (int it = 0; it < (W * R) / NT; ++it) {
-        const int idx = tid + it * NT;
-            const int tt = idx % W, q = idx / W;
-            const int64_t j = j0 + tt, k = j & (Ns - 1);
-            dst[(j - k) * R + k + (int64_t)q * Ns] = smem[tt * F::LS + pad16(q)];
-        }
-    } else {
-        // fully unrolled so that all of a thread's loads are in flight at once
+        for (int it = 0; it < (W * R) / NT; ++it)
+            d[(int64_t)it * RS * Ns] = sm[(RS % 16 == 0) ? pq0 + it * (RS + RS / 16) : pad16(r0 + it * RS)];
+    } else {  // Ns == 1: the tile's output is one contiguous block of W R elements
 #pragma unroll
-    for (int it = 0; it < (W * R) / NT; ++it) {
-        const int idx = tid + it * NT;
-            const int q = idx % R, tt = idx / R;
-            const int64_t j = j0 + tt, k = j & (Ns - 1);
-            dst[(j - k) * R + k + (int64_t)q * Ns] = smem[tt * F::LS + pad16(q)];
+        for (int it = 0; it < (W * R) / NT; ++it) {
+            const int idx = tid + it * NT;
+            const int q = idx % R, tl = idx / R;
+            const int64_t j = j0 + tl, k = j & (Ns - 1);
+            dst[(j - k) * R + k + (int64_t)q * Ns] = smem[tl * F::LS + pad16(q)];
         }
     }
 }

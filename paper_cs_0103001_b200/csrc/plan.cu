@@ -593,6 +593,16 @@ fft_status run_dist_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaS
         if (s != FFT_OK) return s;
         launches += p->sub_b->last_launches;
     }
+    // 6a. FFT_OUT_TRANSPOSED (forward only): keep Z[k2 local][k1] = X[k2 + N2 k1]
+    //     for this rank's k2 range -- one all-to-all less
+    if (!inv && (p->flags & FFT_OUT_TRANSPOSED)) {
+        for (int l = 0; l < nloc; ++l) {
+            e = cudaMemcpyAsync(slab(out, l), slab(w1, l), (size_t)loc * eb, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "copy out");
+        }
+        p->last_launches = launches;
+        return FFT_OK;
+    }
     // 6. natural order: pack [S2][N1] -> [N1][S2] (block q = k1 of rank q), exchange, unpack
     e = launch_transpose(p->prec, w1, w0, S2, N1, nloc, st);
     if (e != cudaSuccess) return cuda_fail(e, "transpose");

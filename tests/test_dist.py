@@ -108,6 +108,28 @@ def test_virtual_ranks_four_step_1d(P, m, dtype):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P,m", [(2, 12), (4, 16), (8, 19)])
+def test_virtual_ranks_four_step_transposed_output(P, m):
+    """FFT_OUT_TRANSPOSED: rank r holds X[k2 + N2 k1] for its k2 block at
+    local index (k2 - r N2/P) N1 + k1."""
+    b = _lib()
+    n = 1 << m
+    N1, N2 = 1 << (m - m // 2), 1 << (m // 2)
+    x = fixtures.complex_input(n, fixtures.NORMAL, seed=700 + m)
+    p = b.Plan((n,), batch=1, flags=b.OUT_TRANSPOSED)
+    p.set_virtual_ranks(P)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    p.forward(xd, yd)
+    torch.cuda.synchronize()
+    X = oracle.fft(x)
+    # rank-major concatenation of [k2 local][k1] blocks == [k2][k1] overall
+    expected = X.reshape(N1, N2).T.ravel()  # X[k2 + N2 k1] at k2 * N1 + k1
+    assert oracle.rel_l2(yd.cpu().numpy(), expected) <= 1e-5
+    p.destroy()
+
+
+@pytest.mark.gpu
 def test_virtual_ranks_c5_shape():
     """BASELINE configs[4] layout: N = 2^30 over 8 virtual ranks (32768 x
     32768 four-step); 16 sampled bins against the oracle's direct sums."""
