@@ -679,6 +679,82 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, MINB)
     cluster_wait_acquire();
 }
 
+// ---------------------------------------------------------------------------
+// Variant 5: persistent 16-CTA clusters that exchange through an L2-resident
+// per-cluster scratch slot (512 KiB, ~37 slots in flight) instead of DSMEM;
+// cluster barriers order the slot's writes (A) and reads (B).  The second
+// barrier (slot free again) is split: arrived after (B)'s loads, waited on
+// just before the next (A) stores, so it overlaps (B)'s math and the next
+// (A)'s loads and math.
+// ---------------------------------------------------------------------------
+template <typename T, int MINB, bool INV>
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, MINB)
+    k_cluster5(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, cpx<T>* __restrict__ scratch, int64_t batch,
+               T scale, const cpx<T>* __restrict__ tw4, const cpx<T>* __restrict__ twa,
+               const cpx<T>* __restrict__ twb) {
+    constexpr int N1 = 256, N2 = 256, E = 16, LS = pad16c(256) + 1;
+    using Cx = cpx<T>;
+    using F = LineFFT<T, 256, E, INV>;
+    constexpr int64_t N = (int64_t)N1 * N2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Cx* sm = reinterpret_cast<Cx*>(smem_raw);
+    namespace cg = cooperative_groups;
+    const int c = (int)cg::this_cluster().block_rank();
+    const int64_t cid = (int64_t)blockIdx.x / 16, ncl = (int64_t)gridDim.x / 16;
+    const int tid = threadIdx.x;
+    Cx* y = scratch + cid * N;
+    const int64_t iters = (batch - cid + ncl - 1) / ncl;
+    for (int64_t j = 0; j < iters; ++j) {
+        const int64_t b = cid + j * ncl;
+        // ---- (A) + (T): columns n1 = 16 c + t -> Y[k2][n1] in the slot ----
+        {
+            const int t = tid & 15, la = tid >> 4;
+            const int n1 = c * 16 + t;
+            const Cx* src = in + b * N;
+            Cx v[E];
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[F::pos_in(m)] = __ldcs(src + n1 + (int64_t)N1 * (la + 16 * m));
+            F::run(v, sm + t * LS, la, twa);
+            if (j > 0) cluster_wait_acquire();  // the slot's previous readers are done
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int k2 = la + 16 * m;
+                __stcg(y + (int64_t)k2 * N1 + n1,
+                       cmul_dir<INV>(v[F::pos_out(m)], __ldg(tw4 + (int64_t)k2 * N1 + n1)));
+            }
+        }
+        cluster_arrive_release();
+        cluster_wait_acquire();  // Y complete and visible
+        // ---- (B): rows k2 = 16 c + tb, read lane-fastest (coalesced) ----
+        {
+            const int tb = tid >> 4, lb = tid & 15;
+            const int k2 = c * 16 + tb;
+            const Cx* src = y + (int64_t)k2 * N1;
+            Cx v[E];
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[F::pos_in(m)] = __ldcg(src + lb + 16 * m);
+            Cx* line = sm + tb * LS;
+            F::run(v, line, lb, twb);
+            // the loaded values have been consumed, so this CTA's reads of the
+            // slot are complete: peers may overwrite it once all have arrived
+            cluster_arrive_relaxed();
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < E; ++m) line[F::bpos(lb, m)] = cscale(v[F::pos_out(m)], scale);
+            __syncthreads();
+            Cx* dst = out + b * N + c * 16;
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+                const int idx = tid + it * 256;
+                const int l = idx & 15, k1 = idx >> 4;
+                __stcs(dst + (int64_t)N2 * k1 + l, sm[l * LS + pad16(k1)]);
+            }
+            __syncthreads();  // sm is reused by the next (A)
+        }
+    }
+    if (iters > 0) cluster_wait_acquire();  // pair the last arrive before leaving
+}
+
 template <typename T>
 constexpr size_t cluster3_smem() {
     using G = ClusterCfg<T, 256, 256, 16, 16>;

@@ -180,6 +180,43 @@ cudaError_t cluster4_t(const void* in, void* out, int64_t batch, double scale, c
     return cudaGetLastError();
 }
 
+template <typename T, int MINB, bool INV>
+cudaError_t cluster5_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                       cudaStream_t st) {
+    constexpr size_t smem = sizeof(cpx<T>) * 16 * (pad16c(256) + 1);
+    auto kern = k_cluster5<T, MINB, INV>;
+    static int max_clusters = 0;
+    static void* scratch = nullptr;
+    if (!max_clusters) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 16;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(16 * 64, 1, 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        if (e == cudaSuccess) e = cudaMalloc(&scratch, (size_t)(n > 0 ? n : 1) * 65536 * sizeof(cpx<T>));
+        if (e != cudaSuccess) return e;
+        max_clusters = n > 0 ? n : 1;
+    }
+    if (batch <= 0) return cudaSuccess;
+    const int64_t ncl = batch < max_clusters ? batch : max_clusters;
+    const cpx<T>* t = reinterpret_cast<const cpx<T>*>(tw);
+    kern<<<(unsigned)(ncl * 16), 256, smem, st>>>(reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<cpx<T>*>(out),
+                                                 reinterpret_cast<cpx<T>*>(scratch), batch, (T)scale,
+                                                 reinterpret_cast<const cpx<T>*>(tw4), t + tw_base(256),
+                                                 t + tw_base(256));
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2) {
@@ -217,6 +254,7 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 14: return step_ab_t<float, 32, 32, 16, 2, INV>(in, out, batch, scale, tw4, tw, st);
         case 15: return fused_ab_t<float, INV>(in, out, batch, scale, tw4, tw, st);
         case 18: return cluster4_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
+        case 19: return cluster5_t<float, 4, INV>(in, out, batch, scale, tw4, tw, st);
         default: return cudaErrorInvalidValue;
     }
 }
