@@ -52,7 +52,10 @@ struct RowsTmaCfg {
     static constexpr uint32_t ROW_IN_BYTES = (uint32_t)(R * (REAL_IN ? sizeof(float) : sizeof(cpx<T>)));
 };
 
-template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false>
+// TRANS: store the tile transposed, out[v][row] (leading dimension = batch),
+// through the stage buffer so that the W rows of a tile form W-element runs
+// -- the separable pipeline's passes then always read contiguous rows.
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false, bool TRANS = false>
 __global__ void __launch_bounds__(W*(R / E), 1)
     k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
                const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt) {
@@ -107,7 +110,21 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         T sc = scale;
         row_filter_pass<T, R, E, FILT, 0, true>(v, line, lt, tw, rowfilt, sc, bar);
         const int64_t row = tile * W + t;
-        if (row < batch) {
+        if constexpr (TRANS) {
+            F::lsync(bar);
+#pragma unroll
+            for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = cscale(v[F::pos_out(m)], sc);
+            __syncthreads();
+            const C* sg = reinterpret_cast<const C*>(smem_raw + s * G::STAGE_BYTES);
+            const int64_t r0 = tile * W;
+            constexpr int NT = W * F::TPL;
+#pragma unroll 4
+            for (int it = 0; it < (W * R) / NT; ++it) {
+                const int idx = tid + it * NT;
+                const int tt = idx % W, vv = idx / W;
+                if (r0 + tt < batch) out[(int64_t)vv * batch + r0 + tt] = sg[tt * G::LS + pad16(vv)];
+            }
+        } else if (row < batch) {
             C* o = out + row * R + lt;
 #pragma unroll
             for (int m = 0; m < E; ++m) o[F::TPL * m] = cscale(v[F::pos_out(m)], sc);

@@ -20,6 +20,14 @@ cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void*
                         int64_t batch, double scale, const void* tw, cudaStream_t st, int in_sh = -1,
                         int out_sh = -1, const void* rowfilt = nullptr);
 
+// Separable-pipeline pass with a transposed store (complex64, 256 <= R <=
+// 2048): rows of length R -> forward -> * rowfilt[v] * scale -> inverse ->
+// out[v][row] (leading dimension batch).  Two of these (rows, then the rows
+// of the transposed grid) are the whole Gaussian pipeline.
+bool rows_filter_transposed_supported(int prec, int64_t R);
+cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* in, void* out, int64_t batch,
+                                          double scale, const void* tw, const void* rowfilt, cudaStream_t st);
+
 // Kernel family B: column transforms of nimg grids [R][S]; mode 0 fwd, 1 inv,
 // 2 fwd -> filter*scale -> inv.
 cudaError_t launch_cols(int prec, int mode, int64_t R, const void* in, void* out, int64_t S,
