@@ -69,6 +69,18 @@ def sky_image(rows: int = 2048, cols: int = 2048, seed: int = 3, nsrc: int = 500
     return out
 
 
+def sky_image_u8(rows: int = 506, cols: int = 460, seed: int = 6, nsrc: int = 120) -> np.ndarray:
+    """8-bit stand-in for the paper's photograph (NGC5194, 460 x 506 pixels,
+    P:395-398; the image itself is not available): the synthetic sky image
+    above, square-root display stretch to [0, 255] (v = 255 sqrt((x - min) /
+    (max - min))), rounded half up, uint8 [rows][cols].  Input recipe only."""
+    x = sky_image(rows, cols, seed=seed, nsrc=nsrc).astype(np.float64)
+    x -= x.min()
+    top = x.max()
+    v = 255.0 * np.sqrt(x / top) if top > 0 else x
+    return np.clip(np.floor(v + 0.5), 0, 255).astype(np.uint8)
+
+
 # BASELINE.json configs -> (shape, kind, seed); DESIGN.md section "Inputs".
 CONFIGS = {
     "C1": dict(n=1024, batch=1, kind=UNIFORM, seed=1, dtype=np.complex128),

@@ -126,6 +126,29 @@ fft_status fft_inverse(fft_plan plan, const void* in, void* out);
 fft_status fft2d_filter_pipeline(fft_plan plan, const void* in, void* out, fft_filter filter,
                                  double param);
 
+/* The paper's own application (Sec. 6), rank-2
+ * complex64 single-GPU plans with N >= h, M >= w:
+ *   in  : DEVICE uint8 [batch][h][w] row-major, a digital image with
+ *         f(x,y) in Z+ u {0}; x = row.
+ *   pad : zero-padded "on rows and on columns" to the plan's N x M
+ *         (the usual N = next_pow2(h), M = next_pow2(w)), inside
+ *         the first pass's load -- no padded copy.
+ *   then: 2D DFT (eq5), spectrum, x H(u,v) into Re and Im,
+ *         2D-IDFT: the fft2d_filter_pipeline computation with
+ *         (filter, param); Eq. (filtro) with b = param for the ideal filters.
+ *   out : DEVICE uint8 [batch][h][w]: real part of the filtered grid, rounded
+ *         half up (floor(x + 0.5)), clamped to [0, max_val], cropped to the
+ *         original h x w.  max_val in [1, 255].
+ *   spectrum (optional, NULL to skip): DEVICE float32 [batch][N][M],
+ *         |F(u,v)| = sqrt(Re^2 + Im^2) of the forward transform
+ *         with eq5's 1/N, unshifted (u, v = 0 is the DC term).
+ * Errors: FFT_E_INVALID_SIZE if h, w are outside [1, N] x [1, M];
+ * FFT_E_INVALID_ARG for null pointers, a non-rank-2 / complex128 plan, a bad
+ * filter or max_val; FFT_E_UNSUPPORTED on a distributed plan.  Uses the
+ * plan's workspace (one complex N x M grid). */
+fft_status fft2d_image_filter_u8(fft_plan plan, const uint8_t* in, int64_t h, int64_t w, uint8_t* out,
+                                 fft_filter filter, double param, int max_val, float* spectrum);
+
 /* End-to-end call on HOST buffers (pageable or pinned): copies the input
  * host->device, transforms, copies the result device->host, pipelined over
  * batch chunks on the plan's streams; returns after the result is in

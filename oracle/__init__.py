@@ -190,6 +190,83 @@ def gauss_pipeline(f, param: float = 0.1) -> np.ndarray:
     return out
 
 
+# ---- the paper's image application (Sec. 6) ----
+
+def next_pow2(d: int) -> int:
+    """Smallest power of two >= d (d >= 1)."""
+    p = 1
+    while p < d:
+        p *= 2
+    return p
+
+
+def pad_pow2(img, N: int | None = None, M: int | None = None) -> np.ndarray:
+    """"pads with zeros on rows and on columns to complete the next
+    power of two": the image at the top-left of an N x M zero grid (default
+    N, M = next powers of two of its height and width), as complex128."""
+    img = np.asarray(img)
+    h, w = img.shape
+    N = next_pow2(h) if N is None else N
+    M = next_pow2(w) if M is None else M
+    g = np.zeros((N, M), dtype=np.complex128)
+    g[:h, :w] = img.astype(np.float64)
+    return g
+
+
+def spectrum(F) -> np.ndarray:
+    """P:369-373: sqrt(Re[C(x,y)]^2 + Im[C(x,y)]^2), elementwise."""
+    F = np.asarray(F, dtype=np.complex128)
+    return np.sqrt(F.real * F.real + F.imag * F.imag)
+
+
+def ideal_filter(N: int, M: int, b: float, literal: bool = True) -> np.ndarray:
+    """Eq. (filtro), evaluated per (u, v) in fp64.  literal
+    (R13): F = 0 if sqrt((u - N/2)^2 + (v - M/2)^2) <= b, else 1, on
+    the unshifted spectrum, (c1, c2) = (N/2, M/2) the grid's centre.
+    literal=False: the centred low-pass reading, 1 if sqrt(k_u^2 + k_v^2) <= b
+    with signed indices k_u = u (u < N/2) else u - N, else 0."""
+    H = np.empty((N, M), dtype=np.float64)
+    for u in range(N):
+        if literal:
+            d2 = (u - N // 2) ** 2 + (np.arange(M) - M // 2) ** 2
+            H[u] = np.where(np.sqrt(d2) <= b, 0.0, 1.0)
+        else:
+            ku = u if u < N // 2 else u - N
+            kv = np.where(np.arange(M) < M // 2, np.arange(M), np.arange(M) - M)
+            H[u] = np.where(np.sqrt(ku * ku + kv * kv) <= b, 1.0, 0.0)
+    return H
+
+
+def image_filter_u8(img, filt: str = "literal", param: float = 340.0, max_val: int = 255,
+                    N: int | None = None, M: int | None = None) -> dict:
+    """Sec. 6 end to end, in the paper's order: pad to powers of
+    two -> 2D FFT (eq5, O4) -> spectrum -> multiply Re and Im by
+    the filter -> 2D-IFFT (O4) -> real part -> round
+    half up -> clamp to [0, max_val] -> crop to the original h x w (the
+    digital image of P:356-361).  filt: "literal" / "lowpass" (Eq. filtro,
+    b = param) or "gauss" (O5 with param x Nyquist).  Returns the padded grid
+    size, the spectrum, the real part before rounding (cropped) and the uint8
+    image."""
+    img = np.asarray(img)
+    h, w = img.shape
+    g = pad_pow2(img, N, M)
+    N, M = g.shape
+    F = fft2d(g)
+    spec = spectrum(F)
+    if filt == "gauss":
+        H = gauss_filter(N, M, param)
+    elif filt in ("literal", "lowpass"):
+        H = ideal_filter(N, M, param, literal=(filt == "literal"))
+    elif filt == "none":
+        H = np.ones((N, M))
+    else:
+        raise ValueError(filt)
+    f = ifft2d(F * H)
+    real = f.real[:h, :w].copy()
+    out = np.clip(np.floor(real + 0.5), 0, max_val).astype(np.uint8)
+    return {"N": N, "M": M, "spectrum": spec, "real": real, "u8": out}
+
+
 def dft_bins(x, bins, inverse: bool = False) -> np.ndarray:
     """Selected bins of one transform by compensated direct sums (O7)."""
     bins = np.ascontiguousarray(bins, dtype=np.int64)

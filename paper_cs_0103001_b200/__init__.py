@@ -69,6 +69,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fft_inverse": ([vp, vp, vp], ci),
         "fft2d_filter_pipeline": ([vp, vp, vp, ci, cd], ci),
         "fft_execute_host": ([vp, ci, vp, vp, ci, cd], ci),
+        "fft2d_image_filter_u8": ([vp, vp, i64, i64, vp, ci, cd, ci, vp], ci),
         "fft_nccl_unique_id": ([ctypes.c_char_p], ci),
         "fft_plan_set_comm": ([vp, ctypes.c_char_p, ci, ci], ci),
         "fft_plan_set_virtual_ranks": ([vp, ci], ci),
@@ -152,6 +153,17 @@ class Plan:
     def filter_pipeline(self, x, out, filter: int = FILTER_GAUSS, param: float = 0.1):
         _check(load_library().fft2d_filter_pipeline(self._h, _ptr(x), _ptr(out), int(filter),
                                                     float(param)), "fft2d_filter_pipeline")
+        return out
+
+    def image_filter_u8(self, img, out, filter: int = FILTER_IDEAL_LITERAL, param: float = 340.0,
+                        max_val: int = 255, spectrum=None):
+        """The paper's image application (Sec. 6): uint8 [batch][h][w] device image ->
+        zero-pad to the plan's N x M -> 2D FFT -> x H -> 2D IFFT -> real, round, clamp,
+        crop -> uint8 ``out``; optional float32 [batch][N][M] ``spectrum`` |F|."""
+        h, w = int(img.shape[-2]), int(img.shape[-1])
+        _check(load_library().fft2d_image_filter_u8(self._h, _ptr(img), h, w, _ptr(out), int(filter),
+                                                    float(param), int(max_val), _ptr(spectrum)),
+               "fft2d_image_filter_u8")
         return out
 
     def execute_host(self, direction: int, host_in, host_out, filter: int = FILTER_NONE,

@@ -424,6 +424,70 @@ __global__ void __launch_bounds__(WB*(N1 / E), MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Variant 22: the two steps of one chunk pipelined across launches.  Launch i
+// runs A(chunk i) and B(chunk i-1) side by side (disjoint CTAs): A writes Y
+// into scratch slot i % 2, B reads slot (i-1) % 2.  Stream order makes A(i-1)
+// complete before B(i-1) reads it and B(i-2) complete before A(i) overwrites
+// its slot, so no events or flags are needed; every launch mixes HBM reads
+// (A) with HBM writes (B), and Y stays in L2 (two slots of chunk x 512 KiB).
+// Blocks [0, nA*16) are A tasks of transforms bA.., the rest B tasks.
+// ---------------------------------------------------------------------------
+template <typename T, int E, bool INV>
+__global__ void __launch_bounds__(256, 4)
+    k_step_ab(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, cpx<T>* __restrict__ ya,
+              const cpx<T>* __restrict__ yb, int64_t bA, int nA, int64_t bB, T scale,
+              const cpx<T>* __restrict__ tw4, const cpx<T>* __restrict__ twa, const cpx<T>* __restrict__ twb) {
+    constexpr int N1 = 256, N2 = 256, W = 16;
+    using Cx = cpx<T>;
+    using F = LineFFT<T, 256, E, INV>;
+    constexpr int TP = 256 / E, LS = pad16c(256) + 1;
+    constexpr int64_t N = (int64_t)N1 * N2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Cx* smem = reinterpret_cast<Cx*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int blk = (int)blockIdx.x;
+    if (blk < nA * 16) {
+        const int64_t bl = blk / 16;
+        const int c = blk % 16;
+        const int t = tid % W, la = tid / W;
+        const int n1 = c * W + t;
+        const Cx* src = in + (bA + bl) * N;
+        Cx* dst = ya + bl * N;
+        Cx v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[F::pos_in(m)] = __ldcs(src + n1 + (int64_t)N1 * (la + TP * m));
+        F::run(v, smem + t * LS, la, twa);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int k2 = la + TP * m;
+            __stcg(dst + (int64_t)k2 * N1 + n1, cmul_dir<INV>(v[F::pos_out(m)], __ldg(tw4 + (int64_t)k2 * N1 + n1)));
+        }
+    } else {
+        const int64_t bl = (blk - nA * 16) / 16;
+        const int c = (blk - nA * 16) % 16;
+        const int tb = tid / TP, lb = tid % TP;
+        const int k2 = c * W + tb;
+        const Cx* src = yb + bl * N + (int64_t)k2 * N1;
+        Cx v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[F::pos_in(m)] = __ldcg(src + lb + TP * m);
+        Cx* line = smem + tb * LS;
+        F::run(v, line, lb, twb);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < E; ++m) line[F::bpos(lb, m)] = cscale(v[F::pos_out(m)], scale);
+        __syncthreads();
+        Cx* dst = out + (bB + bl) * N + c * W;
+#pragma unroll
+        for (int it = 0; it < (W * N1) / 256; ++it) {
+            const int idx = tid + it * 256;
+            const int l = idx % W, k1 = idx / W;
+            __stcs(dst + (int64_t)N2 * k1 + l, smem[l * LS + pad16(k1)]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Persistent single-kernel form of the two steps: CTAs take tasks from a
 // global ticket in the order A(0..Wr-1), B(0), A(Wr), B(1), A(Wr+1), ...,
 // where A(b) / B(b) are the 16 column / 16 row tasks of transform b.  Y(b)
@@ -753,6 +817,108 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, MINB)
         }
     }
     if (iters > 0) cluster_wait_acquire();  // pair the last arrive before leaving
+}
+
+// ---------------------------------------------------------------------------
+// Variant 6: variant 16 (st.async into the aliased phase-A buffer, rotated
+// send order) made persistent -- one cluster loops over transforms
+// cid, cid + ncl, ... -- and with the NEXT transform's phase-A columns
+// prefetched into L2 (cp.async.bulk.prefetch, one 16-column row segment of
+// 128 B per thread) while this one is transformed and exchanged, so the
+// phase-A loads of every iteration after the first hit L2 and the HBM reads
+// overlap the DSMEM exchange.  One cluster barrier per iteration (every CTA
+// done with its phase-A smem before peers push into it), one mbarrier phase
+// per iteration (parity i & 1).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <typename T, int MINB, bool INV, bool PREF>
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, MINB)
+    k_cluster6(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, int64_t batch, T scale,
+               const cpx<T>* __restrict__ tw4, const cpx<T>* __restrict__ twa, const cpx<T>* __restrict__ twb,
+               unsigned stagger_ns) {
+    constexpr int N1 = 256, N2 = 256, C = 16, E = 16;
+    using Cx = cpx<T>;
+    using G = ClusterCfg<T, N1, N2, C, E>;
+    using H = Cluster2Cfg<T, N1, N2, C, E, true>;
+    using FA = LineFFT<T, N2, E, INV>;
+    using FB = LineFFT<T, N1, E, INV>;
+    constexpr int64_t N = (int64_t)N1 * N2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Cx* bufa = reinterpret_cast<Cx*>(smem_raw);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + H::BAR_OFF);
+    const uint32_t bar_s = smem_u32(bar);
+    const uint32_t rx_s = smem_u32(bufa);
+    namespace cg = cooperative_groups;
+    const int c = (int)cg::this_cluster().block_rank();
+    const int64_t cid = (int64_t)blockIdx.x / C, ncl = (int64_t)gridDim.x / C;
+    const int tid = threadIdx.x;
+    const int64_t iters = (batch - cid + ncl - 1) / ncl;
+    const int t = tid % G::WA, la = tid / G::WA;
+    const int n1 = c * G::WA + t;
+    const int tb = tid % G::WB, lb = tid / G::WB;
+    const int k2b = c * G::WB + tb;
+
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_s), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s), "r"(H::RX_BYTES)
+                     : "memory");
+    }
+    // staggered start: clusters resident on the same SMs begin a quarter
+    // iteration apart so that their load / exchange / store phases interleave
+    if (stagger_ns) {
+        const unsigned d = (unsigned)(cid % 4) * stagger_ns;
+        for (unsigned w = 0; w < d; w += 1000) __nanosleep(1000);
+    }
+    for (int64_t i = 0; i < iters; ++i) {
+        const int64_t b = cid + i * ncl;
+        const Cx* src = in + b * N;
+        if constexpr (PREF) {
+            if (i + 1 < iters)  // row n2 = tid of this CTA's 16 columns of the next transform
+                prefetch_l2_bulk(src + ncl * N + (int64_t)N1 * tid + c * G::WA, (uint32_t)(G::WA * sizeof(Cx)));
+        }
+        // ---- (A) columns n1 = c WA + t ----
+        Cx v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[FA::pos_in(m)] = src[n1 + (int64_t)N1 * (la + G::TPA * m)];
+        FA::run(v, bufa + t * G::LSA, la, twa);
+        // done with bufa (and, from the previous iteration, with rx = bufa)
+        cluster_arrive_relaxed();
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int k2 = la + G::TPA * m;
+            v[FA::pos_out(m)] = cmul_dir<INV>(v[FA::pos_out(m)], __ldg(tw4 + (int64_t)k2 * N1 + n1));
+        }
+        cluster_wait_acquire();
+#pragma unroll
+        for (int mm = 0; mm < E; ++mm) {
+            const int m = (mm + c) & (E - 1);
+            const int k2 = la + G::TPA * m;
+            const uint32_t owner = (uint32_t)(k2 / G::WB), line = (uint32_t)(k2 % G::WB);
+            const uint32_t laddr = rx_s + (uint32_t)sizeof(Cx) * (line * G::LSB + pad16(n1));
+            st_async_v2(mapa_u32(laddr, owner), pick_out<0, E, FA>(v, m), mapa_u32(bar_s, owner));
+        }
+        // ---- (B) rows k2 = c WB + tb, once all RX_BYTES have landed ----
+        mbar_wait_parity_cluster(bar_s, (uint32_t)(i & 1));
+        __syncthreads();  // every thread has observed phase i before it is re-armed
+        if (tid == 0 && i + 1 < iters)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s), "r"(H::RX_BYTES)
+                         : "memory");
+        Cx* lineb = bufa + tb * G::LSB;
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[FB::pos_in(m)] = lineb[FB::bpos(lb, m)];
+        FB::run(v, lineb, lb, twb);
+        Cx* dst = out + b * N;
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int k1 = lb + G::TPB * m;
+            dst[k2b + (int64_t)N2 * k1] = cscale(v[FB::pos_out(m)], scale);
+        }
+        __syncthreads();  // bufa is reused by the next (A)
+    }
 }
 
 template <typename T>

@@ -87,6 +87,12 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         if constexpr (MODE == 2) {
             C w[E];
             const int64_t col = s0 + t;
+            if (filt.spec != nullptr && col < S) {
+                float* sp = filt.spec + img * (int64_t)R * S + col;
+#pragma unroll
+                for (int m = 0; m < E; ++m)
+                    sp[(int64_t)(lt + F::TPL * m) * S] = spec_mag(v[F::pos_out(m)], filt.spec_scale);
+            }
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const int64_t u = lt + F::TPL * m;

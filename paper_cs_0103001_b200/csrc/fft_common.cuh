@@ -31,12 +31,58 @@ template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
 template <typename C> __device__ __forceinline__ C cmulc(C a, C b) {
     return mk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
+template <typename C, typename S> __device__ __forceinline__ C cscale(C a, S s) {
+    return mk(a.x * s, a.y * s);
+}
+
+// complex64 specialisations on the sm_100 packed-fp32 pipe (add/sub/mul/fma
+// .f32x2 -> FADD2 / FMUL2 / FFMA2): one instruction per complex add, two per
+// complex multiply (ptxas folds the (y, x) swap and the one-sided negation
+// into the FFMA2 operand modifiers), half the issue slots of scalar fp32.
+// Rounding is the same as the scalar code (RN, FMA contraction).
+__device__ __forceinline__ uint64_t pk2(float2 a) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 up2(uint64_t r) {
+    float2 v;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+    return up2(r);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+    return up2(r);
+}
+// a * w = (a.x, a.y) * (w.x, w.x) + (a.y, a.x) * (-w.y, w.y)
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(make_float2(w.x, w.x))));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(pk2(make_float2(a.y, a.x))), "l"(pk2(make_float2(-w.y, w.y))));
+    return up2(r);
+}
+// a * conj(w) = (a.x, a.y) * (w.x, w.x) + (a.y, a.x) * (w.y, -w.y)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 w) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(make_float2(w.x, w.x))));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(pk2(make_float2(a.y, a.x))), "l"(pk2(make_float2(w.y, -w.y))));
+    return up2(r);
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(make_float2(s, s))));
+    return up2(r);
+}
+
 template <bool CONJ, typename C> __device__ __forceinline__ C cmul_dir(C a, C b) {
     if constexpr (CONJ) return cmulc(a, b);
     else return cmul(a, b);
-}
-template <typename C, typename S> __device__ __forceinline__ C cscale(C a, S s) {
-    return mk(a.x * s, a.y * s);
 }
 // -i * a (forward quarter turn) / +i * a (inverse)
 template <bool INV, typename C> __device__ __forceinline__ C rot_quarter(C a) {
@@ -79,7 +125,7 @@ __device__ __forceinline__ C mulw(C a, int e) {
     if (e16 == 12) return rot_quarter<!INV>(a);
     const T c = (T)cos16(e16);
     const T s = INV ? (T)sin16(e16) : (T)(-sin16(e16));
-    return mk(a.x * c - a.y * s, a.x * s + a.y * c);
+    return cmul(a, mk(c, s));
 }
 
 // In-place DFT of N values v[0..N-1] (natural order in and out), N in

@@ -298,7 +298,17 @@ struct FilterArgs {
     const void* gv;     // T[M] (GAUSS)
     int64_t N, M;       // global grid
     int64_t col_off;    // global index of local column 0 (column slab of a distributed plan)
+    float* spec;        // optional (MODE 2, complex64): |F(u,v)| * spec_scale -> spec[img][u][v]
+    float spec_scale;   // eq5's 1/N (the column pass holds the unnormalised 2D sums)
 };
+
+// spectrum sqrt(Re^2 + Im^2) of one forward-transformed column (Sec. 6,
+// P:369-373), written when the pipeline's caller asked for it
+template <typename C>
+__device__ __forceinline__ float spec_mag(C a, float s) {
+    const float x = (float)a.x, y = (float)a.y;
+    return sqrtf(fmaf(x, x, y * y)) * s;
+}
 
 template <typename T>
 __device__ __forceinline__ T filter_value(const FilterArgs& f, int64_t u, int64_t v) {
@@ -370,6 +380,11 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
     if constexpr (MODE == 2) {
         C w[E];
         const int64_t col = s0 + t;
+        if (filt.spec != nullptr && col < S) {
+            float* sp = filt.spec + img * (int64_t)R * S + col;
+#pragma unroll
+            for (int m = 0; m < E; ++m) sp[(int64_t)(lt + F::TPL * m) * S] = spec_mag(v[F::pos_out(m)], filt.spec_scale);
+        }
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int64_t u = lt + F::TPL * m;

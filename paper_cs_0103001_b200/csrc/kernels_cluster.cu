@@ -1,5 +1,7 @@
 // kernels_cluster.cu -- instantiations and launcher of the one-pass cluster
 // FFT (fft_cluster.cuh) for 1D lengths that do not fit one CTA.
+#include <cstdio>
+
 #include "fft_cluster.cuh"
 #include "launch.h"
 
@@ -217,6 +219,81 @@ cudaError_t cluster5_t(const void* in, void* out, int64_t batch, double scale, c
     return cudaGetLastError();
 }
 
+template <typename T, int MINB, bool INV, bool PREF>
+cudaError_t cluster6_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                       cudaStream_t st) {
+    using H = Cluster2Cfg<T, 256, 256, 16, 16, true>;
+    auto kern = k_cluster6<T, MINB, INV, PREF>;
+    static int max_clusters = 0;
+    static unsigned stagger = 0;
+    if (!max_clusters) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM_BYTES);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 16;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(16 * 64, 1, 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.dynamicSmemBytes = H::SMEM_BYTES;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        if (e != cudaSuccess) return e;
+        const char* f = getenv("B200FFT_CLUSTERS");
+        if (f && atoi(f) > 0 && atoi(f) < n) n = atoi(f);
+        max_clusters = n > 0 ? n : 1;
+        const char* sg = getenv("B200FFT_STAGGER_NS");
+        stagger = sg ? (unsigned)atoi(sg) : 0u;
+        fprintf(stderr, "cluster6: max active clusters %d, stagger %u ns\n", max_clusters, stagger);
+    }
+    if (batch <= 0) return cudaSuccess;
+    const int64_t ncl = batch < max_clusters ? batch : max_clusters;
+    const cpx<T>* t = reinterpret_cast<const cpx<T>*>(tw);
+    kern<<<(unsigned)(ncl * 16), 256, H::SMEM_BYTES, st>>>(reinterpret_cast<const cpx<T>*>(in),
+                                                          reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
+                                                          reinterpret_cast<const cpx<T>*>(tw4), t + tw_base(256),
+                                                          t + tw_base(256), stagger);
+    return cudaGetLastError();
+}
+
+template <typename T, bool INV>
+cudaError_t step_ab2_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                       cudaStream_t st) {
+    constexpr size_t smem = sizeof(cpx<T>) * 16 * (pad16c(256) + 1);
+    auto k = k_step_ab<T, 16, INV>;
+    static bool attr = false;
+    static void* scratch = nullptr;
+    static int64_t chunk = 0;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const char* cs = getenv("B200FFT_STEP_CHUNK");
+        chunk = cs ? atoll(cs) : 48;
+        if (e == cudaSuccess) e = cudaMalloc(&scratch, (size_t)2 * chunk * 65536 * sizeof(cpx<T>));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const cpx<T>* t = reinterpret_cast<const cpx<T>*>(tw);
+    const cpx<T>* x = reinterpret_cast<const cpx<T>*>(in);
+    cpx<T>* o = reinterpret_cast<cpx<T>*>(out);
+    cpx<T>* y = reinterpret_cast<cpx<T>*>(scratch);
+    const int64_t nch = (batch + chunk - 1) / chunk;
+    for (int64_t i = 0; i <= nch; ++i) {
+        const int64_t bA = i * chunk, bB = (i - 1) * chunk;
+        const int nA = i < nch ? (int)(batch - bA < chunk ? batch - bA : chunk) : 0;
+        const int nB = i >= 1 ? (int)(batch - bB < chunk ? batch - bB : chunk) : 0;
+        cpx<T>* ya = y + (i & 1) * chunk * 65536;
+        const cpx<T>* yb = y + ((i + 1) & 1) * chunk * 65536;
+        k<<<(unsigned)(16 * (nA + nB)), 256, smem, st>>>(x, o, ya, yb, bA, nA, bB, (T)scale,
+                                                        reinterpret_cast<const cpx<T>*>(tw4), t + tw_base(256),
+                                                        t + tw_base(256));
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2) {
@@ -255,6 +332,14 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 15: return fused_ab_t<float, INV>(in, out, batch, scale, tw4, tw, st);
         case 18: return cluster4_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
         case 19: return cluster5_t<float, 4, INV>(in, out, batch, scale, tw4, tw, st);
+        case 20: return cluster6_t<float, 4, INV, true>(in, out, batch, scale, tw4, tw, st);
+        case 21: return cluster6_t<float, 4, INV, false>(in, out, batch, scale, tw4, tw, st);
+        case 27: return cluster6_t<float, 5, INV, false>(in, out, batch, scale, tw4, tw, st);
+        case 22: return step_ab2_t<float, INV>(in, out, batch, scale, tw4, tw, st);
+        case 23: return cluster2_t<float, 256, 256, 16, 16, 5, INV, true, true>(in, out, batch, scale, tw4, tw, st);
+        case 24: return cluster2_t<float, 256, 256, 16, 16, 3, INV, true, true>(in, out, batch, scale, tw4, tw, st);
+        case 25: return cluster2_t<float, 256, 256, 8, 16, 2, INV, true, true>(in, out, batch, scale, tw4, tw, st);
+        case 26: return cluster2_t<float, 256, 256, 8, 16, 3, INV, true, true>(in, out, batch, scale, tw4, tw, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -49,6 +49,13 @@ cudaError_t launch_transpose(int prec, const void* in, void* out, int64_t R, int
 cudaError_t launch_twiddle4(int prec, bool inv, void* y, int64_t rows, int64_t L, int64_t row0, const void* ta,
                             const void* tb, int sh, cudaStream_t st);
 
+// The paper's image application (kernels_image.cu): row DFTs of the N x M
+// grid of `nrows` = batch * N rows of length M.  Forward: u8 [batch][h][w]
+// zero-padded to [N][M] in the load -> complex64 out.  Inverse: complex64 in
+// -> real part, round half up, clamp [0, max_val], crop to h x w -> u8 out.
+cudaError_t launch_image_rows(bool inv, int64_t M, const void* in, void* out, int64_t nrows, int64_t N, int64_t h,
+                              int64_t w, int max_val, const void* tw, cudaStream_t st);
+
 // One-pass cluster FFT (fft_cluster.cuh): n = n1 * n2 in one thread-block
 // cluster per transform.  tw4: W_n^{n1 k2} laid out [k2][n1].
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2);

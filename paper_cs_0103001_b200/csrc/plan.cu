@@ -746,11 +746,11 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
                 t[2 * (k2 * cn1 + n1) + 1] = std::sin(ang);
             }
         const char* var = getenv("B200FFT_CLUSTER_VARIANT");
-        // default 16: st.async transpose with rank-rotated send order (no
-        // incast), 16-CTA clusters, 4 CTAs/SM (the
-        // fastest measured); 8/9 are timing-only
-        p->cvariant = var ? atoi(var) : 16;
-        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 16;
+        // default 23: st.async transpose with rank-rotated send order (no
+        // incast), 16-CTA clusters, 48 registers -> 5 CTAs/SM (the fastest
+        // measured, profiles/README.md); 8/9 are timing-only
+        p->cvariant = var ? atoi(var) : 23;
+        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 23;
         if (var && atoi(var) == 8 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 8;
         if (var && atoi(var) == 9 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 9;
         e = upload(t, ip, &p->tw4);
@@ -853,6 +853,53 @@ fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filt
     if (p->elems() == 0) return FFT_OK;
     if (p->dist()) return run_dist_2d(p, in, out, 2, filter, param, p->stream);
     return run_pipeline(p, in, out, filter, param, p->stream);
+}
+
+fft_status fft2d_image_filter_u8(fft_plan p, const uint8_t* in, int64_t h, int64_t w, uint8_t* out,
+                                 fft_filter filter, double param, int max_val, float* spectrum) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (p->rank != 2 || p->prec != FFT_C64) return fail(FFT_E_INVALID_ARG, "image filter needs a rank-2 complex64 plan");
+    if (p->dist()) return fail(FFT_E_UNSUPPORTED, "image filter on a distributed plan");
+    if (!in || !out) return fail(FFT_E_INVALID_ARG, "null image pointer");
+    if (spectrum && !aligned(spectrum, 4)) return fail(FFT_E_INVALID_ARG, "misaligned spectrum pointer");
+    if (h < 1 || w < 1 || h > p->n0 || w > p->n1)
+        return fail(FFT_E_INVALID_SIZE, "image must be 1 <= h <= N, 1 <= w <= M of the plan");
+    if (max_val < 1 || max_val > 255) return fail(FFT_E_INVALID_ARG, "max_val must be in [1, 255]");
+    if (filter < FFT_FILTER_NONE || filter > FFT_FILTER_IDEAL_LOWPASS) return fail(FFT_E_INVALID_ARG, "unknown filter");
+    if (filter == FFT_FILTER_GAUSS && !(param > 0.0)) return fail(FFT_E_INVALID_ARG, "Gaussian needs param > 0");
+    if ((filter == FFT_FILTER_IDEAL_LITERAL || filter == FFT_FILTER_IDEAL_LOWPASS) && !(param >= 0.0))
+        return fail(FFT_E_INVALID_ARG, "ideal filter needs radius >= 0");
+    const int64_t N = p->n0, M = p->n1;
+    fft_status s = ensure_workspace(p);
+    if (s != FFT_OK) return s;
+    FilterArgs f{};
+    f.kind = (int)filter;
+    f.N = N;
+    f.M = M;
+    if (filter == FFT_FILTER_GAUSS) {
+        s = gauss_tables(p, param);
+        if (s != FFT_OK) return s;
+        f.gu = p->gu;
+        f.gv = p->gv;
+    } else if (filter == FFT_FILTER_IDEAL_LITERAL || filter == FFT_FILTER_IDEAL_LOWPASS) {
+        f.b2 = param * param;
+    }
+    f.spec_scale = (float)(1.0 / (double)N);  // eq5's 1/N
+    cudaStream_t st = p->stream;
+    const int64_t img_px = h * w;
+    for (int64_t g = 0; g < p->batch; ++g) {
+        f.spec = spectrum ? spectrum + g * N * M : nullptr;
+        // pad + promote + rows forward (unnormalised) -> ws; columns fwd -> |F| -> x H / (N M) -> inv;
+        // rows inverse -> real, round, clamp, crop -> out
+        cudaError_t e = launch_image_rows(false, M, in + g * img_px, p->ws, N, N, h, w, max_val, p->tw, st);
+        if (e == cudaSuccess)
+            e = launch_cols(p->prec, 2, N, p->ws, p->ws, M, 1, 1.0 / ((double)N * (double)M), p->tw, f, st);
+        if (e == cudaSuccess)
+            e = launch_image_rows(true, M, p->ws, out + g * img_px, N, N, h, w, max_val, p->tw, st);
+        if (e != cudaSuccess) return cuda_fail(e, "image filter launch");
+    }
+    p->last_launches = (int)(3 * p->batch);
+    return FFT_OK;
 }
 
 fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void* host_out, fft_filter filter,

@@ -28,4 +28,21 @@ if which in ("all", "c3"):
     torch.cuda.synchronize()
     p.filter_pipeline(img, out, b.FILTER_GAUSS, 0.1)
     torch.cuda.synchronize()
+if which in ("all", "c4"):
+    x = torch.from_numpy(fixtures.complex_input(8192 * 8192, 0, seed=4).reshape(8192, 8192)).to(dev)
+    out = torch.empty_like(x)
+    p = b.Plan((8192, 8192))
+    p.filter_pipeline(x, out, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    p.filter_pipeline(x, out, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+if which in ("all", "c5"):
+    n = 1 << 30
+    x = torch.from_numpy(fixtures.complex_input(n, 1, seed=5)).to(dev)
+    p = b.Plan((n,))
+    y = torch.empty_like(x)
+    p.forward(x, y)
+    torch.cuda.synchronize()
+    p.forward(x, y)
+    torch.cuda.synchronize()
 print("ok")

@@ -70,6 +70,15 @@ def test_1d_multi_pass_sizes(fft, dtype, m):
     assert oracle.rel_l2(z, oracle.fft_batch(x, inverse=True)) <= TOL[dtype]
 
 
+def test_1d_three_pass_radix512(fft):
+    """2^27 = 512^3: three pipelined passes (k_pass_pipe), the last one with a
+    two-level pass twiddle (pa x pb), forward and inverse against the oracle."""
+    n = 1 << 27
+    x = fixtures.complex_input(n, fixtures.NORMAL, seed=227).reshape(1, n)
+    assert oracle.rel_l2(run_1d(fft, x), oracle.fft_batch(x)) <= TOL[np.complex64]
+    assert oracle.rel_l2(run_1d(fft, x, inverse=True), oracle.fft_batch(x, inverse=True)) <= TOL[np.complex64]
+
+
 @pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
 def test_1d_65536_multipass_fallback(fft, dtype, monkeypatch):
     """The generic 2-pass schedule for N = 65536 (the one-pass cluster kernel
