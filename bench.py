@@ -325,6 +325,43 @@ def bench_c3(args, local):
             "hbm_frac": round(alg / (med / 1e3) / 1e9 / peak, 4)}
 
 
+def bench_next1(args, local):
+    """SURVEY NEXT-1, the paper's own application (Sec. 6): an
+    8-bit 506 x 460 image (synthetic stand-in for NGC5194) zero-padded to
+    512^2 -> 2D FFT -> Eq. (filtro) b = 340 -> 2D IFFT -> real, round, clamp,
+    crop to uint8, spectrum written; cold L2, latency per image."""
+    import torch
+
+    import paper_cs_0103001_b200 as b
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    img = fixtures.sky_image_u8(506, 460, seed=6)
+    idev = torch.from_numpy(img).to(dev)
+    out = torch.empty_like(idev)
+    spec = torch.empty((512, 512), dtype=torch.float32, device=dev)
+    plan = b.Plan((512, 512), batch=1, precision=b.C64, stream=stream)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        plan.image_filter_u8(idev, out, b.FILTER_IDEAL_LITERAL, 340.0, 255, spec)
+    times = []
+    for _ in range(max(args.steps, 20)):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            s.record(stream)
+            plan.image_filter_u8(idev, out, b.FILTER_IDEAL_LITERAL, 340.0, 255, spec)
+            e.record(stream)
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    med = statistics.median(times)
+    n = 512 * 512
+    plan.destroy()
+    return {"workload": "NEXT-1: 506x460 uint8 image -> pad 512^2 -> FFT2 -> Eq. filtro b=340 -> IFFT2 -> uint8 "
+                        "(+ spectrum), cold L2", "us_median": round(med * 1e3, 2), "us_min": round(min(times) * 1e3, 2),
+            "GFLOP/s": round(2 * 5 * n * math.log2(n) / (med / 1e3) / 1e9, 1), "launches": 3}
+
+
 def bench_c1(args, local):
     import torch
 
@@ -474,7 +511,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--extra", action="store_true", help="also time C1 and C3 (rank 0)")
+    ap.add_argument("--extra", action="store_true", help="also time C1, C3 and NEXT-1 (rank 0)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -499,7 +536,8 @@ def main():
         if ws == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = cpu_baseline_c2()
         if args.extra:
-            res["extra"] = {"C1": bench_c1(args, local), "C3": bench_c3(args, local)}
+            res["extra"] = {"C1": bench_c1(args, local), "C3": bench_c3(args, local),
+                            "NEXT1": bench_next1(args, local)}
         print(json.dumps(res), flush=True)
     if ws > 1:
         import torch.distributed as dist

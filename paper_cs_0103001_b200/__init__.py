@@ -33,7 +33,7 @@ IN_REAL_F32 = 1 << 1
 
 EXPORTS = [
     "fft_plan_create", "fft_plan_create_ex", "fft_plan_set_stream", "fft_plan_workspace_bytes",
-    "fft_plan_set_workspace", "fft_forward", "fft_inverse", "fft2d_filter_pipeline",
+    "fft_plan_set_workspace", "fft_forward", "fft_inverse", "fft2d_filter_pipeline", "fft2d_image_filter_u8",
     "fft_execute_host", "fft_nccl_unique_id", "fft_plan_set_comm", "fft_plan_set_virtual_ranks",
     "fft_plan_destroy",
     "fft_status_string", "fft_last_error", "fft_plan_last_launch_count", "fft_build_info",
