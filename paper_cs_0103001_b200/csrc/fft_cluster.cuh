@@ -21,6 +21,7 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include "fft_cols_pipe.cuh"
 #include "fft_engine.cuh"
 
 namespace b200fft {
@@ -919,6 +920,151 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, MINB)
         }
         __syncthreads();  // bufa is reused by the next (A)
     }
+}
+
+// ---------------------------------------------------------------------------
+// Variant 28: the four-step split into independent 16-line tasks -- A(b, p):
+// columns n1 in [16p, 16p+16) of transform b, (A)+(T), Y rows to an
+// L2-resident ring slot; B(b, p): rows k2 in [16p, 16p+16) of Y(b), (B),
+// X to HBM -- run by a persistent, software-pipelined grid.  Every CTA walks
+// the global task sequence
+//     A(0..D-1) | A(D) B(0) | A(D+1) B(1) | ... | B(batch-D..batch-1)
+// (16 tasks per letter) with stride gridDim.x and prefetches its NEXT task's
+// 16 x 256 input into the second smem stage with cp.async while it computes
+// the current one, so HBM / L2 latency hides behind the math.  A B task's
+// input waits on a counter (done_a[b] == 16) that was filled D transforms
+// earlier in the sequence; an A task's ring slot waits on done_b of the
+// transform RING slots back.  With 16 D >= gridDim.x every wait is on a
+// task strictly earlier than the waiter's current one, so co-resident CTAs
+// (cooperative launch) cannot deadlock.
+// ---------------------------------------------------------------------------
+struct AbCtl {
+    int* done_a;  // [batch]
+    int* done_b;  // [batch]
+    int D, ring;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename T, int MINB, bool INV>
+__global__ void __launch_bounds__(256, MINB)
+    k_ab_pipe(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, cpx<T>* __restrict__ ring, int64_t batch,
+              T scale, const cpx<T>* __restrict__ tw4, const cpx<T>* __restrict__ tw256, AbCtl ctl) {
+    constexpr int N1 = 256, W = 16, E = 16, LS = pad16c(256) + 1;
+    constexpr int64_t N = 65536;
+    constexpr int STAGE = W * LS;
+    using Cx = cpx<T>;
+    using F = LineFFT<T, 256, E, INV>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Cx* stage0 = reinterpret_cast<Cx*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int t = tid % W, l = tid / W;  // line t (column n1 / row k2), lane l
+    const int64_t Dp = batch < ctl.D ? batch : ctl.D;
+    const int64_t n1t = 16 * Dp, n2t = 32 * (batch - Dp);
+    const int64_t ntasks = 32 * batch;
+
+    // task i -> (is_b, transform, part)
+    auto decode = [&](int64_t i, bool& isb, int64_t& b, int& part) {
+        if (i < n1t) {
+            isb = false;
+            b = i / 16;
+            part = (int)(i % 16);
+        } else if (i < n1t + n2t) {
+            const int64_t j = i - n1t, r = j % 32;
+            isb = r >= 16;
+            b = Dp + j / 32 - (isb ? Dp : 0);
+            part = (int)(r % 16);
+        } else {
+            const int64_t j = i - n1t - n2t;
+            isb = true;
+            b = batch - Dp + j / 16;
+            part = (int)(j % 16);
+        }
+    };
+    // this thread's cp.async copies of a task's 16 x 256 tile into stage buf
+    auto prefetch = [&](int64_t i, int buf) {
+        if (i < ntasks) {
+            bool isb;
+            int64_t b;
+            int part;
+            decode(i, isb, b, part);
+            Cx* sm = stage0 + buf * STAGE;
+            if (!isb) {  // columns n1 = 16 part + tt, rows n2: 128-B runs
+                const Cx* src = in + b * N + part * W;
+#pragma unroll
+                for (int it = 0; it < 16; ++it) {
+                    const int idx = tid + it * 256;
+                    const int tt = idx % W, r = idx / W;
+                    cp_async8(sm + tt * LS + pad16(r), src + (int64_t)r * N1 + tt, true);
+                }
+            } else {  // rows k2 = 16 part + tt of Y (contiguous 2 KiB each)
+                if (tid == 0) {
+                    while (ld_acquire_gpu(ctl.done_a + b) < 16) __nanosleep(32);
+                }
+                __syncthreads();
+                const Cx* src = ring + (b % ctl.ring) * N + (int64_t)part * W * N1;
+#pragma unroll
+                for (int it = 0; it < 16; ++it) {
+                    const int idx = tid + it * 256;
+                    const int tt = idx / N1, r = idx % N1;
+                    cp_async8(sm + tt * LS + pad16(r), src + idx, true);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+
+    int64_t i = blockIdx.x;
+    prefetch(i, 0);
+    for (int k = 0; i < ntasks; ++k, i += gridDim.x) {
+        const int buf = k & 1;
+        prefetch(i + gridDim.x, buf ^ 1);
+        cp_async_wait<1>();
+        __syncthreads();
+        bool isb;
+        int64_t b;
+        int part;
+        decode(i, isb, b, part);
+        if (isb && tid == 0) {  // this task's reads of ring slot b are complete
+            __threadfence();
+            atomicAdd(ctl.done_b + b, 1);
+        }
+        Cx* line = stage0 + buf * STAGE + t * LS;
+        Cx v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(l, m)];
+        F::run(v, line, l, tw256);
+        if (!isb) {
+            const int n1 = part * W + t;
+            if (b >= ctl.ring) {
+                if (tid == 0) {
+                    while (ld_acquire_gpu(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
+                }
+                __syncthreads();
+            }
+            Cx* y = ring + (b % ctl.ring) * N;
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int k2 = l + 16 * m;
+                __stcg(y + (int64_t)k2 * N1 + n1,
+                       cmul_dir<INV>(v[F::pos_out(m)], __ldg(tw4 + (int64_t)k2 * N1 + n1)));
+            }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicAdd(ctl.done_a + b, 1);
+        } else {
+            const int k2 = part * W + t;
+            Cx* dst = out + b * N + k2;
+#pragma unroll
+            for (int m = 0; m < E; ++m) __stcs(dst + (int64_t)N1 * (l + 16 * m), cscale(v[F::pos_out(m)], scale));
+            __syncthreads();  // stage buf is free for the prefetch two tasks ahead
+        }
+    }
+    cp_async_wait<0>();
 }
 
 template <typename T>

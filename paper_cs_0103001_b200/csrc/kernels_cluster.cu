@@ -294,6 +294,64 @@ cudaError_t step_ab2_t(const void* in, void* out, int64_t batch, double scale, c
     return cudaGetLastError();
 }
 
+template <typename T, int MINB, bool INV>
+cudaError_t ab_pipe_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                      cudaStream_t st) {
+    constexpr size_t smem = 2 * sizeof(cpx<T>) * 16 * (pad16c(256) + 1);
+    auto k = k_ab_pipe<T, MINB, INV>;
+    static int grid = 0, D = 0, ring_slots = 0;
+    static void* ring = nullptr;
+    static int* ctl = nullptr;
+    static int64_t ctl_n = 0;
+    if (!grid) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
+        if (e != cudaSuccess) return e;
+        grid = sms * (occ > 0 ? occ : 1);
+        const char* dv = getenv("B200FFT_AB_D");
+        D = (grid + 15) / 16 + (dv ? atoi(dv) : 8);
+        const char* rv = getenv("B200FFT_AB_RING");
+        ring_slots = D + (rv ? atoi(rv) : 16);
+        e = cudaMalloc(&ring, (size_t)ring_slots * 65536 * sizeof(cpx<T>));
+        if (e != cudaSuccess) return e;
+        fprintf(stderr, "ab_pipe: grid %d (occ %d), D %d, ring %d\n", grid, occ, D, ring_slots);
+    }
+    if (batch <= 0) return cudaSuccess;
+    if (ctl_n < 2 * batch) {
+        if (ctl) cudaFree(ctl);
+        cudaError_t e = cudaMalloc(&ctl, sizeof(int) * 2 * batch);
+        if (e != cudaSuccess) return e;
+        ctl_n = 2 * batch;
+    }
+    cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
+    if (e != cudaSuccess) return e;
+    AbCtl c{ctl, ctl + batch, D, ring_slots};
+    const cpx<T>* t = reinterpret_cast<const cpx<T>*>(tw);
+    const int64_t tasks = 32 * batch;
+    const int g = (int)(tasks < grid ? tasks : grid);
+    const cpx<T>* a_in = reinterpret_cast<const cpx<T>*>(in);
+    cpx<T>* a_out = reinterpret_cast<cpx<T>*>(out);
+    cpx<T>* a_ring = reinterpret_cast<cpx<T>*>(ring);
+    T a_scale = (T)scale;
+    const cpx<T>* a_tw4 = reinterpret_cast<const cpx<T>*>(tw4);
+    const cpx<T>* a_tw = t + tw_base(256);
+    void* args[] = {&a_in, &a_out, &a_ring, &batch, &a_scale, &a_tw4, &a_tw, &c};
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3(g, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, (const void*)k, args);
+}
+
 }  // namespace
 
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2) {
@@ -335,6 +393,10 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 20: return cluster6_t<float, 4, INV, true>(in, out, batch, scale, tw4, tw, st);
         case 21: return cluster6_t<float, 4, INV, false>(in, out, batch, scale, tw4, tw, st);
         case 27: return cluster6_t<float, 5, INV, false>(in, out, batch, scale, tw4, tw, st);
+        case 28: return ab_pipe_t<float, 3, INV>(in, out, batch, scale, tw4, tw, st);
+        case 31: return cluster2_t<float, 256, 256, 16, 16, 6, INV, true, true>(in, out, batch, scale, tw4, tw, st);
+        case 29: return ab_pipe_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
+        case 30: return ab_pipe_t<float, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 22: return step_ab2_t<float, INV>(in, out, batch, scale, tw4, tw, st);
         case 23: return cluster2_t<float, 256, 256, 16, 16, 5, INV, true, true>(in, out, batch, scale, tw4, tw, st);
         case 24: return cluster2_t<float, 256, 256, 16, 16, 3, INV, true, true>(in, out, batch, scale, tw4, tw, st);
