@@ -90,7 +90,16 @@ enum {
      * transposed order -- X[k2 + N2 k1] for k2 in [r N2/P, (r+1) N2/P) at
      * local index (k2 - r N2/P) N1 + k1 -- one all-to-all less.  Ignored by
      * fft_inverse (its input is always in natural order). */
-    FFT_OUT_TRANSPOSED = 1u << 0
+    FFT_OUT_TRANSPOSED = 1u << 0,
+    /* NEXT-3 (with FFT_IN_REAL_F32, FFT_FILTER_GAUSS, even N and M,
+     * 256 <= N, M <= 2048, single GPU): fft2d_filter_pipeline writes float32
+     * real [N][M] -- the pipeline's real part.  For real input and the real,
+     * even Gaussian H the pipeline preserves Hermitian symmetry, so its
+     * imaginary part is zero in exact arithmetic (nothing is dropped).  Runs
+     * as two real-to-real row passes that transform two real rows per
+     * complex row: half the bytes and flops of the complex pipeline.  Other
+     * filters / sizes: FFT_E_UNSUPPORTED. */
+    FFT_OUT_REAL_F32 = 1u << 2
 };
 
 /* Short form from BASELINE.json's north_star: rank = transform

@@ -30,6 +30,7 @@ FILTER_NONE, FILTER_GAUSS, FILTER_IDEAL_LITERAL, FILTER_IDEAL_LOWPASS = 0, 1, 2,
 # flags
 OUT_TRANSPOSED = 1 << 0
 IN_REAL_F32 = 1 << 1
+OUT_REAL_F32 = 1 << 2  # NEXT-3 real-to-real Gaussian pipeline (with IN_REAL_F32)
 
 EXPORTS = [
     "fft_plan_create", "fft_plan_create_ex", "fft_plan_set_stream", "fft_plan_workspace_bytes",

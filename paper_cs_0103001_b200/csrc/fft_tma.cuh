@@ -55,7 +55,16 @@ struct RowsTmaCfg {
 // TRANS: store the tile transposed, out[v][row] (leading dimension = batch),
 // through the stage buffer so that the W rows of a tile form W-element runs
 // -- the separable pipeline's passes then always read contiguous rows.
-template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false, bool TRANS = false>
+// PAIR (NEXT-3, real-to-real separable pipeline): each line is TWO real
+// float32 rows a, b (the 2R floats a bulk copy of one complex row brings in)
+// transformed as the complex row a + i b.  The row filter pass is a real
+// operator when its filter is real and even (g[v] = g[R - v]: the Gaussian),
+// so the result is L(a) + i L(b) exactly: real part = filtered a, imaginary
+// part = filtered b, stored as the float pair (a', b') -- which, with TRANS,
+// is the transposed real grid.  Half the lines, half the bytes of promoting
+// each real row to complex.
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false, bool TRANS = false,
+          bool PAIR = false>
 __global__ void __launch_bounds__(W*(R / E), 1)
     k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
                const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt) {
@@ -101,6 +110,10 @@ __global__ void __launch_bounds__(W*(R / E), 1)
             const float* fl = reinterpret_cast<const float*>(line);
 #pragma unroll
             for (int m = 0; m < E; ++m) v[F::pos_in(m)] = mk((T)fl[lt + F::TPL * m], (T)0);
+        } else if constexpr (PAIR) {
+            const float* fl = reinterpret_cast<const float*>(line);
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[F::pos_in(m)] = mk((T)fl[lt + F::TPL * m], (T)fl[R + lt + F::TPL * m]);
         } else {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[lt + F::TPL * m];

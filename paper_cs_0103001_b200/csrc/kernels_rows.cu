@@ -50,14 +50,14 @@ cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double s
 }
 
 // persistent TMA-fed variant (fft_tma.cuh): 3 stages of ~64 KiB, 512 threads
-template <typename T, int R, bool INV, bool REAL_IN, bool FILT, bool TRANS = false>
+template <typename T, int R, bool INV, bool REAL_IN, bool FILT, bool TRANS = false, bool PAIR = false>
 cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw, const void* rowfilt,
                        cudaStream_t st) {
     constexpr int E = 16;
     constexpr int W = (int)((64 * 1024) / (R * sizeof(cpx<T>))) < 1 ? 1 : (int)((64 * 1024) / (R * sizeof(cpx<T>)));
     constexpr int STAGES = 3;
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
-    auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS>;
+    auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS, PAIR>;
     static int grid_max = 0;
     if (!grid_max) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
@@ -99,14 +99,18 @@ bool use_tma_rows(int prec, int64_t R, int in_sh, int out_sh) {
     return !off && prec == 0 && R >= 256 && R <= 8192 && in_sh < 0 && out_sh < 0;
 }
 
-template <bool REAL_IN>
+template <bool REAL_IN, bool PAIR = false>
 cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw,
                                 const void* rowfilt, cudaStream_t st) {
     switch (R) {
-        case 256: return rows_tma_t<float, 256, false, REAL_IN, true, true>(in, out, batch, scale, tw, rowfilt, st);
-        case 512: return rows_tma_t<float, 512, false, REAL_IN, true, true>(in, out, batch, scale, tw, rowfilt, st);
-        case 1024: return rows_tma_t<float, 1024, false, REAL_IN, true, true>(in, out, batch, scale, tw, rowfilt, st);
-        case 2048: return rows_tma_t<float, 2048, false, REAL_IN, true, true>(in, out, batch, scale, tw, rowfilt, st);
+        case 256:
+            return rows_tma_t<float, 256, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
+        case 512:
+            return rows_tma_t<float, 512, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
+        case 1024:
+            return rows_tma_t<float, 1024, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
+        case 2048:
+            return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -118,7 +122,9 @@ bool rows_filter_transposed_supported(int prec, int64_t R) {
 }
 
 cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* in, void* out, int64_t batch,
-                                          double scale, const void* tw, const void* rowfilt, cudaStream_t st) {
+                                          double scale, const void* tw, const void* rowfilt, cudaStream_t st,
+                                          bool pair) {
+    if (pair) return rows_filter_trans_r<false, true>(R, in, out, batch, scale, tw, rowfilt, st);
     return real_in ? rows_filter_trans_r<true>(R, in, out, batch, scale, tw, rowfilt, st)
                    : rows_filter_trans_r<false>(R, in, out, batch, scale, tw, rowfilt, st);
 }

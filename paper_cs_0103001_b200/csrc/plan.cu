@@ -340,6 +340,26 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
     // DFT_r] f exactly -- two fused passes (rows fwd*g*inv, then columns
     // fwd*g*inv), 32 B/point of HBM instead of 48 (DESIGN.md "Separable
     // pipeline").  B200FFT_PIPE_LITERAL=1 keeps the three-pass order.
+    if (p->flags & FFT_OUT_REAL_F32) {
+        // NEXT-3: real in, real out; two real rows per complex line in both
+        // passes (the Gaussian row / column operators are real and even)
+        if (!real_in || filter != FFT_FILTER_GAUSS || N % 2 || M % 2 || !rows_filter_transposed_supported(p->prec, M) ||
+            !rows_filter_transposed_supported(p->prec, N))
+            return fail(FFT_E_UNSUPPORTED, "real-output pipeline needs real input, the Gaussian, even 256..2048 sides");
+        fft_status s = ensure_workspace(p);
+        if (s != FFT_OK) return s;
+        const size_t grid = (size_t)N * M * sizeof(float);
+        for (int64_t g = 0; g < p->batch; ++g) {
+            e = launch_rows_filter_transposed(false, M, (const char*)in + g * grid, p->ws, N / 2, 1.0 / (double)M, p->tw,
+                                              p->gv, st, true);
+            if (e == cudaSuccess)
+                e = launch_rows_filter_transposed(false, N, p->ws, (char*)out + g * grid, M / 2, 1.0 / (double)N,
+                                                  p->tw, p->gu, st, true);
+            if (e != cudaSuccess) return cuda_fail(e, "k_rows_tma (real pairs) launch");
+        }
+        p->last_launches = (int)(2 * p->batch);
+        return FFT_OK;
+    }
     const char* lit_env = getenv("B200FFT_PIPE_LITERAL");
     const bool literal = lit_env && lit_env[0] == '1';
     if (filter == FFT_FILTER_GAUSS && !literal && rows_filter_transposed_supported(p->prec, M) &&
@@ -702,7 +722,10 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
     if (rank != 1 && rank != 2) return fail(FFT_E_INVALID_ARG, "rank must be 1 or 2");
     if (prec != FFT_C64 && prec != FFT_C128) return fail(FFT_E_INVALID_ARG, "bad precision");
     if (batch < 0) return fail(FFT_E_INVALID_SIZE, "negative batch");
-    if (flags & ~(unsigned)(FFT_IN_REAL_F32 | FFT_OUT_TRANSPOSED)) return fail(FFT_E_INVALID_ARG, "unknown flag");
+    if (flags & ~(unsigned)(FFT_IN_REAL_F32 | FFT_OUT_TRANSPOSED | FFT_OUT_REAL_F32))
+        return fail(FFT_E_INVALID_ARG, "unknown flag");
+    if ((flags & FFT_OUT_REAL_F32) && (rank != 2 || !(flags & FFT_IN_REAL_F32) || prec != FFT_C64))
+        return fail(FFT_E_INVALID_ARG, "FFT_OUT_REAL_F32 needs a rank-2 complex64 plan with FFT_IN_REAL_F32");
     const int ip = (int)prec;
     for (int d = 0; d < rank; ++d)
         if (!is_pow2(dims[d])) return fail(FFT_E_INVALID_SIZE, "transform sizes must be powers of two >= 1");
@@ -851,6 +874,8 @@ fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filt
         return fail(FFT_E_INVALID_ARG, "ideal filter needs radius >= 0");
     if (real_in && in == out) return fail(FFT_E_INVALID_ARG, "real input cannot alias the complex output");
     if (p->elems() == 0) return FFT_OK;
+    if (p->dist() && (p->flags & FFT_OUT_REAL_F32))
+        return fail(FFT_E_UNSUPPORTED, "real-output pipeline on a distributed plan");
     if (p->dist()) return run_dist_2d(p, in, out, 2, filter, param, p->stream);
     return run_pipeline(p, in, out, filter, param, p->stream);
 }
@@ -909,6 +934,7 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
     if (direction == 0 && p->rank != 2) return fail(FFT_E_INVALID_ARG, "pipeline needs a rank-2 plan");
     if (direction < -1 || direction > 1) return fail(FFT_E_INVALID_ARG, "direction must be -1, 0 or +1");
     if (p->dist()) return fail(FFT_E_UNSUPPORTED, "host execution of a distributed plan");
+    if (p->flags & FFT_OUT_REAL_F32) return fail(FFT_E_UNSUPPORTED, "host execution of a real-output plan");
     const int64_t total = p->elems();
     if (total == 0) return FFT_OK;
     const bool real_in = direction == 0 && (p->flags & FFT_IN_REAL_F32);

@@ -103,3 +103,29 @@ def test_batched_image_filter(b):
         amb = np.abs(frac - 0.5) < 2e-3
         assert d[~amb].max(initial=0) == 0 and d.max() <= 1
         assert oracle.rel_l2(sp[i], ref["spectrum"]) <= 1e-5
+
+
+@pytest.mark.parametrize("batch,N,M", [(1, 2048, 2048), (2, 256, 512), (3, 1024, 256), (1, 512, 2048)])
+def test_real_to_real_gauss_pipeline(b, batch, N, M):
+    """NEXT-3: FFT_IN_REAL_F32 | FFT_OUT_REAL_F32 -- two real rows per complex
+    line in both passes; float32 output against the real part of the
+    oracle's complex pipeline (whose imaginary part is ~0, pinned on CPU)."""
+    imgs = np.stack([fixtures.sky_image(N, M, seed=700 + i, nsrc=60) for i in range(batch)])
+    p = b.Plan((N, M), batch=batch, flags=b.IN_REAL_F32 | b.OUT_REAL_F32)
+    x = torch.from_numpy(imgs).cuda()
+    o = torch.empty_like(x)
+    p.filter_pipeline(x, o, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    assert p.last_launch_count() == 2 * batch
+    p.destroy()
+    ref = np.stack([oracle.gauss_pipeline(imgs[i].astype(np.complex128), 0.1).real for i in range(batch)])
+    assert oracle.rel_l2(o.cpu().numpy(), ref) <= 1e-5
+
+
+def test_real_to_real_rejects_other_filters(b):
+    p = b.Plan((256, 256), flags=b.IN_REAL_F32 | b.OUT_REAL_F32)
+    x = torch.zeros((256, 256), dtype=torch.float32, device="cuda")
+    o = torch.empty_like(x)
+    with pytest.raises(b.FFTError):
+        p.filter_pipeline(x, o, b.FILTER_IDEAL_LOWPASS, 10.0)
+    p.destroy()

@@ -115,3 +115,21 @@ def test_image_energy_monotone():
         assert abs(float(np.sum(r["real"] ** 2)) - kept) <= 1e-9 * kept
         e.append(kept)
     assert e[0] < e[1] < e[2]
+
+
+@pytest.mark.parametrize("N,M", [(64, 64), (32, 128)])
+def test_real_gauss_pipeline_stays_real(N, M):
+    """NEXT-3's premise (R19): for a real image and the real, even
+    Gaussian H, the pipeline preserves Hermitian symmetry, so its output is
+    real -- the imaginary part of the oracle's complex result vanishes to
+    fp64 rounding -- and equals the separable row-then-column application of
+    the 1D operators (rows filtered, then columns) on real data."""
+    img = fixtures.sky_image(N, M, seed=21, nsrc=10).astype(np.float64)
+    out = oracle.gauss_pipeline(img.astype(np.complex128), 0.1)
+    assert np.abs(out.imag).max() <= 1e-12 * np.abs(out.real).max()
+    H = oracle.gauss_filter(N, M, 0.1)
+    g_v = H[0] / H[0, 0]  # row factor g_M(v): H(0, v) = g_N(0) g_M(v), g_N(0) = 1
+    g_u = H[:, 0] / H[0, 0]
+    rows = np.real(np.fft.ifft(np.fft.fft(img, axis=1) * g_v[None, :], axis=1))
+    both = np.real(np.fft.ifft(np.fft.fft(rows, axis=0) * g_u[:, None], axis=0))
+    assert oracle.rel_l2(out.real, both) <= 1e-12
