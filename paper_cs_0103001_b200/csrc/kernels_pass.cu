@@ -65,6 +65,37 @@ cudaError_t pass_pipe_t(const void* in, void* out, int64_t L, int64_t Ns, int64_
     return cudaGetLastError();
 }
 
+// TMA-bulk-fed form (fft_pass_pipe.cuh k_pass_tma); complex64
+template <typename T, int R, int W, bool INV>
+cudaError_t pass_tma_t(const void* in, void* out, int64_t L, int64_t Ns, int64_t batch, double scale,
+                       const void* tw, const void* pa, const void* pb, int klo_sh, cudaStream_t st) {
+    constexpr int E = 16;
+    constexpr int TPL = R / E;
+    using G = PassTmaCfg<T, R, W>;
+    auto kern = k_pass_tma<T, R, E, W, INV>;
+    static int grid_max = 0;
+    if (!grid_max) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * TPL, G::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        grid_max = sms * (occ > 0 ? occ : 1);
+    }
+    if (batch <= 0) return cudaSuccess;
+    const int64_t LR = L / R;
+    if (LR % W != 0 || (Ns > 1 && Ns < W)) return cudaErrorInvalidValue;
+    const int64_t nlines = batch * LR;
+    const int64_t ntiles = nlines / W;
+    const int64_t grid = ntiles < grid_max ? ntiles : grid_max;
+    kern<<<(unsigned)grid, W * TPL, G::SMEM_BYTES, st>>>(
+        reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<cpx<T>*>(out), L, Ns, nlines, (T)scale,
+        reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), reinterpret_cast<const cpx<T>*>(pa),
+        reinterpret_cast<const cpx<T>*>(pb), klo_sh);
+    return cudaGetLastError();
+}
+
 template <typename T, bool INV>
 cudaError_t pass_r(int64_t R, const void* in, void* out, int64_t L, int64_t Ns, int64_t batch,
                    double scale, const void* tw, const void* pa, const void* pb, int klo_sh,
@@ -74,6 +105,23 @@ cudaError_t pass_r(int64_t R, const void* in, void* out, int64_t L, int64_t Ns, 
         return v ? atoi(v) : 0;  // 0: k_pass (measured faster, profiles/README.md)
     }();
     if constexpr (sizeof(T) == 4) {
+        if (pipe == 5) {  // TMA-bulk-fed tiles
+            switch (R) {
+                case 256: return pass_tma_t<T, 256, 32, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                case 512: return pass_tma_t<T, 512, 16, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                case 1024: return pass_tma_t<T, 1024, 8, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                default: break;
+            }
+        }
+        // radix <= 256 passes: pipelined, 32 / 64 lines per tile (256-B / 512-B runs)
+        if (pipe != 4) {
+            switch (R) {
+                case 128: return pass_pipe_t<T, 128, 64, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                case 256: return pass_pipe_t<T, 256, 32, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                case 512: return pass_pipe_t<T, 512, 16, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                default: break;
+            }
+        }
         if (pipe == 1) {
             switch (R) {
                 case 512: return pass_pipe_t<T, 512, 16, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);

@@ -184,7 +184,7 @@ size_t workspace_need(const fft_plan_s* p) {
         return (size_t)p->n0 * p->n1 * p->elem_bytes();
     if (p->rank == 1 && !p->radices.empty()) {
         size_t one = (size_t)p->elems() * p->elem_bytes();
-        return p->radices.size() >= 3 ? 2 * one : one;
+        return p->radices.size() % 2 == 1 ? 2 * one : one;  // odd pass counts may need ws1 (run_1d)
     }
     return 0;
 }
@@ -207,11 +207,20 @@ fft_status ensure_workspace(fft_plan_s* p) {
 
 bool aligned(const void* ptr, size_t a) { return ((uintptr_t)ptr % a) == 0; }
 
-// radix split of a multi-pass length L = 2^m (m >= 14): 2 or 3 passes of
-// radix 2^7 .. 2^10, as even as possible (largest first).
-std::vector<int64_t> split_radices(int64_t L) {
+// radix split of a multi-pass length L = 2^m (m >= 14): passes of radix
+// <= 2^rmax, as even as possible (largest first).  rmax = 10 (2 or 3 passes
+// of 128..1024) by default; complex64 transforms whose pass strides reach
+// 2^21 elements (16 MiB) use rmax = 8 so that the pipelined pass kernel's
+// tiles are 32 lines wide: 256-B runs instead of 64-B ones, which DRAM
+// serves at 6.6 vs 2.9 TB/s at such strides (scripts/strided.cu,
+// profiles/README.md) -- one pass more, each ~2x faster.
+std::vector<int64_t> split_radices(int64_t L, int prec) {
     int m = ilog2(L);
-    int P = (m + 9) / 10;
+    int rmax = 10;
+    const char* rv = getenv("B200FFT_PASS_RMAX");
+    if (rv) rmax = atoi(rv);
+    (void)prec;  // rmax = 8 for m >= 29 measured slower (4 passes at 2.8 TB/s, profiles/README.md)
+    int P = (m + rmax - 1) / rmax;
     std::vector<int64_t> r;
     for (int i = 0; i < P; ++i) {
         int mi = m / P + (i < m % P ? 1 : 0);
@@ -247,12 +256,11 @@ fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream
     std::vector<const void*> src(P);
     std::vector<void*> dst(P);
     dst[P - 1] = out;
-    if (P == 2) {
-        dst[0] = ws0;
-    } else {  // P == 3
-        dst[1] = ws0;
-        dst[0] = (in == out) ? (void*)ws1 : out;
-    }
+    // passes alternate between ws0 and out, ending in out; with an odd count
+    // pass 0 would write out, which must not alias in (passes are not
+    // in-place safe): then it writes ws1
+    for (int i = 0; i < P - 1; ++i) dst[i] = ((P - 1 - i) % 2 == 0) ? out : (void*)ws0;
+    if (P % 2 == 1 && in == out) dst[0] = ws1;
     src[0] = in;
     for (int i = 1; i < P; ++i) src[i] = dst[i - 1];
     int64_t Ns = 1;
@@ -782,7 +790,7 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
             return cuda_fail(e, "four-step twiddle upload");
         }
     } else if (rank == 1 && p->n0 > kRowsMax) {
-        p->radices = split_radices(p->n0);
+        p->radices = split_radices(p->n0, ip);
         // pass i (span Ns, radix R): W_{Ns R}^{k r} = pa[r][k mod KLO] * pb[r][k / KLO]
         int64_t Ns = 1;
         for (size_t i = 0; i < p->radices.size(); ++i) {
