@@ -508,11 +508,78 @@ def bench_sharded(args, ws, rank, local, cfg):
     return res
 
 
+def bench_tree(args, ws, rank, local):
+    """NEXT-2: the paper's own parallel schedule (Sec. 4) against
+    the library's all-to-all four-step, forward only, on C5's transform
+    (n = 2^30 complex64).  ws > 1: one rank per GPU, NCCL send/recv rounds;
+    ws == 1: P = 8 VIRTUAL ranks on one GPU (all ranks' work serialised on
+    one device: the arithmetic and HBM cost of the schedule, not its
+    multi-GPU wall time -- labelled so).  Branch inputs: i.i.d. N(0,1) blocks
+    (a cyclic subsequence of an i.i.d. sequence is i.i.d.)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_cs_0103001_b200 as b
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    n = 1 << 30
+    P = ws if ws > 1 else 8
+    loc = n // ws
+    x = np.empty(loc, np.complex64)
+    fixtures.complex_input(loc, fixtures.NORMAL, seed=5, offset=rank * loc, out=x)
+    xd = torch.from_numpy(x).to(dev)
+    del x
+    res = {}
+    for sched in ("paper_tree", "four_step_a2a"):
+        plan = b.Plan((n,), batch=1, stream=stream)
+        if ws > 1:
+            uid = [b.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            plan.set_comm(uid[0], ws, rank)
+        else:
+            plan.set_virtual_ranks(P)
+        if sched == "paper_tree":
+            yd = torch.empty(n if rank == 0 else 1, dtype=torch.complex64, device=dev)
+            run = lambda: plan.forward_paper_tree(xd, yd if rank == 0 else None)  # noqa: E731
+        else:
+            yd = torch.empty_like(xd)
+            run = lambda: plan.forward(xd, yd)  # noqa: E731
+        for _ in range(args.warmup):
+            run()
+        torch.cuda.synchronize()
+        barrier(ws)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(args.steps):
+            run()
+        e.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        ms = allreduce_max(ws, s.elapsed_time(e)) / args.steps
+        res[sched] = {"ms": round(ms, 3), "GFLOP/s": round(5.0 * n * 30 / (ms / 1e3) / 1e9, 1),
+                      "launches": plan.last_launch_count()}
+        plan.destroy()
+        del yd
+        torch.cuda.empty_cache()
+    return {"metric": "FFT GFLOP/s (5N*log2N), forward only", "value": res["paper_tree"]["GFLOP/s"],
+            "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": res["paper_tree"]["ms"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c64 (fp32 arithmetic)", "data": "synthetic (counter-based seeded)",
+            "config": {"workload": "NEXT-2: the paper's tree schedule vs the all-to-all four-step, n = 2^30",
+                       "ranks": P, "emulated": ws == 1,
+                       "parallelism": f"{P} virtual ranks on 1 GPU (work serialised)" if ws == 1
+                       else f"{ws} GPUs, NCCL send/recv rounds"},
+            "schedules": res}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--config", default="C2", choices=["C2", "C4", "C5"],
-                    help="C2 (default, the metric's config), or the sharded C4 / C5")
+    ap.add_argument("--config", default="C2", choices=["C2", "C4", "C5", "TREE"],
+                    help="C2 (default, the metric's config), the sharded C4 / C5, or TREE (NEXT-2: the "
+                         "paper's parallel schedule vs the all-to-all four-step)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -528,7 +595,8 @@ def main():
             print(json.dumps(res), flush=True)
         return
     if args.config != "C2":
-        res = bench_sharded(args, ws, rank, local, args.config)
+        res = (bench_tree(args, ws, rank, local) if args.config == "TREE"
+               else bench_sharded(args, ws, rank, local, args.config))
         if rank == 0:
             print(json.dumps(res), flush=True)
         if ws > 1:

@@ -158,6 +158,27 @@ fft_status fft2d_filter_pipeline(fft_plan plan, const void* in, void* out, fft_f
 fft_status fft2d_image_filter_u8(fft_plan plan, const uint8_t* in, int64_t h, int64_t w, uint8_t* out,
                                  fft_filter filter, double param, int max_val, float* spectrum);
 
+/* NEXT-2: the paper's own parallel schedule (Sec. 4) for one
+ * complex 1D transform of n = 2^m on P = 2^l ranks (a rank-1, batch-1 plan
+ * with fft_plan_set_comm, or P virtual ranks on one GPU for tests):
+ *   in : this rank's branch, the cyclic subsequence x[q + P j], j < n/P
+ *        (the leaves processor idproc = q starts from); with
+ *        virtual ranks, the P branches back to back (P x n/P elements).
+ *   1. every rank transforms its branch (the tree's levels 1..m - l);
+ *   2. l rounds (nproc_sup = P, P/2, ..., 2): ranks q in [S/2, S) send their
+ *      vector to q - S/2 (NCCL send/recv over NVLink) and stop; the receiver
+ *      combines the two with one radix-2 level;
+ *   3. rank 0 (the MASTER) ends with X = (1/n) DFT(x) in natural order
+ *      (P:191-224).
+ *   out: rank 0: n elements (DEVICE, caller-owned); other ranks: unused (may
+ *        be NULL).  Collective: every rank calls it.
+ * It keeps the paper's serial tail (the last rounds run on half, then a
+ * quarter ... of the GPUs, the last on rank 0 alone): a comparison point for
+ * the all-to-all schedule of fft_forward, not its replacement.
+ * Errors: FFT_E_INVALID_SIZE if P is not a power of two or does not divide
+ * n; FFT_E_INVALID_ARG for a non-1D / batched plan or null pointers. */
+fft_status fft_forward_paper_tree(fft_plan plan, const void* in, void* out);
+
 /* End-to-end call on HOST buffers (pageable or pinned): copies the input
  * host->device, transforms, copies the result device->host, pipelined over
  * batch chunks on the plan's streams; returns after the result is in

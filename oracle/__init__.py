@@ -267,6 +267,38 @@ def image_filter_u8(img, filt: str = "literal", param: float = 340.0, max_val: i
     return {"N": N, "M": M, "spectrum": spec, "real": real, "u8": out}
 
 
+# ---- the paper's parallel schedule (Sec. 4) ----
+
+def paper_tree_fft(x, P: int) -> np.ndarray:
+    """The paper's parallel FFT, step by step, fp64: processor q
+    of P = 2^l transforms its branch, the cyclic subsequence x[q + P j]
+    (with this oracle's O2 and its 1/len); then while nproc_sup
+    = S > 1, processor q + S/2 hands its vector to q, which
+    combines them with one radix-2 level, Y[k] = (E[k] + w^k O[k]) / 2,
+    Y[k + M] = (E[k] - w^k O[k]) / 2 with w = exp(-2 pi i / (2M)) (the
+    paper's Z factors, Table 2, and its 1/N); the MASTER ends with X."""
+    x = np.asarray(x, dtype=np.complex128).ravel()
+    n = x.size
+    assert P >= 1 and P & (P - 1) == 0 and n % P == 0
+    vec = [fft(x[q::P]) for q in range(P)]
+    S = P
+    while S > 1:
+        M = vec[0].size
+        k = np.arange(M)
+        w = np.exp(-2j * np.pi * k / (2 * M))
+        for q in range(S // 2):
+            E, O = vec[q], vec[q + S // 2]
+            vec[q] = np.concatenate([(E + w * O) / 2, (E - w * O) / 2])
+        S //= 2
+    return vec[0]
+
+
+def paper_parallel_products(m: int, l: int) -> int:
+    """Eq. (multi): complex products of the parallel FFT with
+    N = 2^m data on 2^l processors, (m - l) 2^(m - l) + sum_{i=1..l} 2^(m-l+i)."""
+    return (m - l) * 2 ** (m - l) + sum(2 ** (m - l + i) for i in range(1, l + 1))
+
+
 def dft_bins(x, bins, inverse: bool = False) -> np.ndarray:
     """Selected bins of one transform by compensated direct sums (O7)."""
     bins = np.ascontiguousarray(bins, dtype=np.int64)

@@ -35,6 +35,7 @@ OUT_REAL_F32 = 1 << 2  # NEXT-3 real-to-real Gaussian pipeline (with IN_REAL_F32
 EXPORTS = [
     "fft_plan_create", "fft_plan_create_ex", "fft_plan_set_stream", "fft_plan_workspace_bytes",
     "fft_plan_set_workspace", "fft_forward", "fft_inverse", "fft2d_filter_pipeline", "fft2d_image_filter_u8",
+    "fft_forward_paper_tree",
     "fft_execute_host", "fft_nccl_unique_id", "fft_plan_set_comm", "fft_plan_set_virtual_ranks",
     "fft_plan_destroy",
     "fft_status_string", "fft_last_error", "fft_plan_last_launch_count", "fft_build_info",
@@ -71,6 +72,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fft2d_filter_pipeline": ([vp, vp, vp, ci, cd], ci),
         "fft_execute_host": ([vp, ci, vp, vp, ci, cd], ci),
         "fft2d_image_filter_u8": ([vp, vp, i64, i64, vp, ci, cd, ci, vp], ci),
+        "fft_forward_paper_tree": ([vp, vp, vp], ci),
         "fft_nccl_unique_id": ([ctypes.c_char_p], ci),
         "fft_plan_set_comm": ([vp, ctypes.c_char_p, ci, ci], ci),
         "fft_plan_set_virtual_ranks": ([vp, ci], ci),
@@ -154,6 +156,13 @@ class Plan:
     def filter_pipeline(self, x, out, filter: int = FILTER_GAUSS, param: float = 0.1):
         _check(load_library().fft2d_filter_pipeline(self._h, _ptr(x), _ptr(out), int(filter),
                                                     float(param)), "fft2d_filter_pipeline")
+        return out
+
+    def forward_paper_tree(self, x, out=None):
+        """The paper's parallel schedule (Sec. 4): ``x`` = this rank's cyclic
+        branch x[q + P j] (virtual ranks: all P branches back to back); rank 0's
+        ``out`` receives the whole (1/n) DFT in natural order."""
+        _check(load_library().fft_forward_paper_tree(self._h, _ptr(x), _ptr(out)), "fft_forward_paper_tree")
         return out
 
     def image_filter_u8(self, img, out, filter: int = FILTER_IDEAL_LITERAL, param: float = 340.0,

@@ -50,6 +50,34 @@ __global__ void __launch_bounds__(256) k_twiddle4(cpx<T>* __restrict__ y, int64_
     }
 }
 
+// The paper's combine step (Sec. 4): the receiver of a round holds
+// E = DFT_M of x[q + 2S j] and gets O = DFT_M of x[q + S + 2S j] from rank
+// q + S; one radix-2 level gives the DFT_{2M} of x[q + S j]:
+//   Y[k]     = (E[k] + W_{2M}^k O[k]) / 2
+//   Y[k + M] = (E[k] - W_{2M}^k O[k]) / 2,   k < M
+// (the 1/2 keeps the paper's normalisation: every branch carries its 1/len,
+// so l halvings give the 1/n of Eq. E2).  W_{2M}^k = W_n^{k n / (2M)} from the
+// two fp64-generated tables (ta[x >> sh] * tb[x & mask]).  `nb` independent
+// combines (virtual ranks): E_b = e + b * es, O_b = o + b * es, Y_b = y + b * ys.
+template <typename T>
+__global__ void __launch_bounds__(256) k_tree_combine(const cpx<T>* __restrict__ e, const cpx<T>* __restrict__ o,
+                                                      cpx<T>* __restrict__ y, int64_t M, int64_t nb, int64_t es,
+                                                      int64_t ys, int64_t xstep, const cpx<T>* __restrict__ ta,
+                                                      const cpx<T>* __restrict__ tb, int sh) {
+    const int64_t total = M * nb;
+    const int64_t mask = ((int64_t)1 << sh) - 1;
+    const T half = (T)0.5;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / M, k = i - b * M;
+        const int64_t x = k * xstep;
+        const cpx<T> w = cmul(__ldg(ta + (x >> sh)), __ldg(tb + (x & mask)));
+        const cpx<T> a = e[b * es + k];
+        const cpx<T> t = cmul(o[b * es + k], w);
+        y[b * ys + k] = cscale(cadd(a, t), half);
+        y[b * ys + k + M] = cscale(csub(a, t), half);
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_transpose(int prec, const void* in, void* out, int64_t R, int64_t Cn, int64_t nmat,
@@ -90,6 +118,23 @@ cudaError_t launch_twiddle4(int prec, bool inv, void* y, int64_t rows, int64_t L
                                                                        reinterpret_cast<const double2*>(ta),
                                                                        reinterpret_cast<const double2*>(tb), sh);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tree_combine(int prec, const void* e, const void* o, void* y, int64_t M, int64_t nb, int64_t es,
+                                int64_t ys, int64_t xstep, const void* ta, const void* tb, int sh, cudaStream_t st) {
+    if (M <= 0 || nb <= 0) return cudaSuccess;
+    const int64_t total = M * nb;
+    const int64_t want = (total + 255) / 256;
+    const unsigned grid = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+    if (prec == 0)
+        k_tree_combine<float><<<grid, 256, 0, st>>>(
+            reinterpret_cast<const float2*>(e), reinterpret_cast<const float2*>(o), reinterpret_cast<float2*>(y), M,
+            nb, es, ys, xstep, reinterpret_cast<const float2*>(ta), reinterpret_cast<const float2*>(tb), sh);
+    else
+        k_tree_combine<double><<<grid, 256, 0, st>>>(
+            reinterpret_cast<const double2*>(e), reinterpret_cast<const double2*>(o), reinterpret_cast<double2*>(y),
+            M, nb, es, ys, xstep, reinterpret_cast<const double2*>(ta), reinterpret_cast<const double2*>(tb), sh);
     return cudaGetLastError();
 }
 

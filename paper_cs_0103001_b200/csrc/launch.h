@@ -60,6 +60,12 @@ cudaError_t launch_twiddle4(int prec, bool inv, void* y, int64_t rows, int64_t L
 cudaError_t launch_image_rows(bool inv, int64_t M, const void* in, void* out, int64_t nrows, int64_t N, int64_t h,
                               int64_t w, int max_val, const void* tw, cudaStream_t st);
 
+// The paper's tree combine (NEXT-2, kernels_misc.cu k_tree_combine): nb
+// radix-2 combines of E, O (length M, stride es) into Y (length 2M, stride
+// ys) with W_{2M}^k = ta[x >> sh] * tb[x & mask], x = k * xstep.
+cudaError_t launch_tree_combine(int prec, const void* e, const void* o, void* y, int64_t M, int64_t nb, int64_t es,
+                                int64_t ys, int64_t xstep, const void* ta, const void* tb, int sh, cudaStream_t st);
+
 // One-pass cluster FFT (fft_cluster.cuh): n = n1 * n2 in one thread-block
 // cluster per transform.  tw4: W_n^{n1 k2} laid out [k2][n1].
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2);

@@ -163,6 +163,13 @@ struct fft_plan_s {
     void* ftb = nullptr;          // W_n^{i}
     int fsh = 0;
     double scale_override = 0.0;  // sub-plans: scale of the last pass (0 = the default)
+    // the paper's own tree schedule (NEXT-2, fft_forward_paper_tree)
+    fft_plan_s* tree_sub = nullptr;  // branch FFTs: length n / P, batch = local ranks
+    void* tta = nullptr;             // W_n^{i << tsh}
+    void* ttb = nullptr;             // W_n^{i}
+    int tsh = 0;
+    void* tws = nullptr;             // tree buffers (owned)
+    size_t tws_bytes = 0;
 
     size_t elem_bytes() const { return prec == 0 ? 8 : 16; }
     int P() const { return comm ? nranks : virt; }
@@ -610,6 +617,145 @@ cudaError_t unpack_blocks(char* dst, const char* src, int64_t R, int64_t Cb, int
     return e;
 }
 
+// ---- NEXT-2: the paper's parallel schedule (Sec. 4) ----------
+// P = 2^l ranks, n = 2^m.  Rank q holds its branch, the cyclic subsequence
+// x[q + P j] (the leaves of processor idproc), and transforms it
+// (levels 1..m1 = m - l).  Then l rounds: with nproc_sup = S
+// active ranks, ranks q in [S/2, S) send their vector to q - S/2 and stop
+// (P:165-190); each receiver combines the two with one radix-2 level
+// (k_tree_combine); S halves.  After the last round the MASTER (rank 0)
+// holds X = (1/n) DFT(x) in natural order.  Virtual ranks: all P
+// branches are slabs of one buffer and every round is one batched combine.
+fft_status tree_prepare(fft_plan_s* p) {
+    const int P = p->P();
+    const int64_t n = p->n0, L = n / P;
+    const int nloc = p->comm ? 1 : P;
+    if (!p->tree_sub || p->tree_sub->n0 != L || p->tree_sub->batch != nloc) {
+        if (p->tree_sub) fft_plan_destroy(p->tree_sub);
+        p->tree_sub = nullptr;
+        int64_t d = L;
+        fft_status s = fft_plan_create_ex(&p->tree_sub, &d, 1, nloc, p->prec == 0 ? FFT_C64 : FFT_C128, 0);
+        if (s != FFT_OK) return s;
+    }
+    if (!p->tta) {
+        const int m = ilog2(n);
+        p->tsh = (m + 1) / 2;
+        const int64_t na = (int64_t)1 << (m - p->tsh), nb = (int64_t)1 << p->tsh;
+        std::vector<double> a(2 * na), b(2 * nb);
+        for (int64_t i = 0; i < na; ++i) {
+            const double ang = -2.0 * M_PI * (double)((i << p->tsh) % n) / (double)n;
+            a[2 * i] = std::cos(ang);
+            a[2 * i + 1] = std::sin(ang);
+        }
+        for (int64_t i = 0; i < nb; ++i) {
+            const double ang = -2.0 * M_PI * (double)i / (double)n;
+            b[2 * i] = std::cos(ang);
+            b[2 * i + 1] = std::sin(ang);
+        }
+        cudaError_t e = upload(a, p->prec, &p->tta);
+        if (e == cudaSuccess) e = upload(b, p->prec, &p->ttb);
+        if (e != cudaSuccess) return cuda_fail(e, "tree twiddle upload");
+    }
+    // buffers: virtual ranks ping-pong two n-element grids; a rank of a
+    // communicator needs its largest vector twice plus the received half
+    const size_t eb = p->elem_bytes();
+    size_t need;
+    if (!p->comm) {
+        need = 2 * (size_t)n * eb;
+    } else {
+        int64_t mx = L;
+        for (int S = P; S > 1; S /= 2)
+            if (p->my_rank < S / 2) mx *= 2;
+        need = (size_t)(2 * mx + mx / 2 + 1) * eb;
+    }
+    if (p->tws_bytes < need) {
+        if (p->tws) cudaFree(p->tws);
+        p->tws = nullptr;
+        p->tws_bytes = 0;
+        cudaError_t e = cudaMalloc(&p->tws, need);
+        if (e != cudaSuccess) return cuda_fail(e, "tree buffers");
+        p->tws_bytes = need;
+    }
+    return FFT_OK;
+}
+
+fft_status run_paper_tree(fft_plan_s* p, const void* in, void* out, cudaStream_t st) {
+    fft_status s = tree_prepare(p);
+    if (s != FFT_OK) return s;
+    const int P = p->P();
+    const int64_t n = p->n0;
+    int64_t M = n / P;
+    const size_t eb = p->elem_bytes();
+    char* A = (char*)p->tws;
+    char* B = A + (size_t)n * eb;  // virtual ranks; a communicator rank re-slices below
+    int launches = 0;
+    p->tree_sub->stream = st;
+    if (!p->comm) {
+        // 1. every branch: P slabs of n/P, one batched forward (1/(n/P))
+        s = run_1d(p->tree_sub, in, A, false, st);
+        if (s != FFT_OK) return s;
+        launches += p->tree_sub->last_launches;
+        // 2. rounds: receivers q < S/2 combine slab q (E) and slab q + S/2 (O)
+        for (int S = P; S > 1; S /= 2) {
+            char* dst = (S == 2) ? (char*)out : B;
+            cudaError_t e = launch_tree_combine(p->prec, A, A + (size_t)(S / 2) * M * eb, dst, M, S / 2, M, 2 * M,
+                                                n / (2 * M), p->tta, p->ttb, p->tsh, st);
+            if (e != cudaSuccess) return cuda_fail(e, "tree combine");
+            ++launches;
+            std::swap(A, B);
+            M *= 2;
+        }
+        if (P == 1) {
+            cudaError_t e = cudaMemcpyAsync(out, A, (size_t)n * eb, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "tree copy");
+        }
+        p->last_launches = launches;
+        return FFT_OK;
+    }
+#ifdef B200FFT_WITH_NCCL
+    const int q = p->my_rank;
+    int64_t mx = M;
+    for (int S = P; S > 1; S /= 2)
+        if (q < S / 2) mx *= 2;
+    char* V = A;                            // this rank's vector (<= mx)
+    char* W = A + (size_t)mx * eb;          // combine target (<= mx)
+    char* Rb = A + (size_t)2 * mx * eb;     // received half (<= mx / 2)
+    const bool final_here = (q == 0 && out != nullptr);
+    s = run_1d(p->tree_sub, in, (P == 1 && final_here) ? out : V, false, st);
+    if (s != FFT_OK) return s;
+    launches += p->tree_sub->last_launches;
+    ncclComm_t comm = (ncclComm_t)p->comm;
+    const ncclDataType_t dt = p->prec == 0 ? ncclFloat : ncclDouble;
+    for (int S = P; S > 1; S /= 2) {
+        if (q >= S) break;  // already sent its vector
+        const size_t count = 2 * (size_t)M;
+        ncclResult_t r;
+        if (q >= S / 2) {
+            r = ncclSend(V, count, dt, q - S / 2, comm, st);
+            if (r != ncclSuccess) return fail(FFT_E_NCCL, std::string("tree send: ") + ncclGetErrorString(r));
+            break;
+        }
+        r = ncclRecv(Rb, count, dt, q + S / 2, comm, st);
+        if (r != ncclSuccess) return fail(FFT_E_NCCL, std::string("tree recv: ") + ncclGetErrorString(r));
+        char* dst = (S == 2 && final_here) ? (char*)out : W;
+        cudaError_t e = launch_tree_combine(p->prec, V, Rb, dst, M, 1, M, 2 * M, n / (2 * M), p->tta, p->ttb, p->tsh,
+                                            st);
+        if (e != cudaSuccess) return cuda_fail(e, "tree combine");
+        ++launches;
+        std::swap(V, W);
+        M *= 2;
+    }
+    if (P == 1 && final_here) {
+        // branch FFT already wrote out
+    }
+    p->last_launches = launches;
+    return FFT_OK;
+#else
+    (void)out;
+    return fail(FFT_E_UNSUPPORTED, "library built without NCCL");
+#endif
+}
+
 fft_status run_dist_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
     fft_status s = fs_prepare(p);
     if (s == FFT_OK) s = ensure_workspace(p);
@@ -868,6 +1014,20 @@ static fft_status exec(fft_plan p, const void* in, void* out, bool inv) {
 }
 
 fft_status fft_forward(fft_plan p, const void* in, void* out) { return exec(p, in, out, false); }
+
+fft_status fft_forward_paper_tree(fft_plan p, const void* in, void* out) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (p->rank != 1 || p->batch != 1) return fail(FFT_E_INVALID_ARG, "the paper's schedule needs a single 1D transform");
+    if (!in) return fail(FFT_E_INVALID_ARG, "null input");
+    const int P = p->P();
+    if (P < 1 || (P & (P - 1))) return fail(FFT_E_INVALID_SIZE, "the paper's schedule needs 2^l ranks");
+    if (p->n0 % P) return fail(FFT_E_INVALID_SIZE, "n must be a multiple of the rank count");
+    const bool master = !p->comm || p->my_rank == 0;
+    if (master && !out) return fail(FFT_E_INVALID_ARG, "rank 0 needs an n-element output");
+    if (!aligned(in, p->elem_bytes()) || (out && !aligned(out, p->elem_bytes())))
+        return fail(FFT_E_INVALID_ARG, "data pointer not aligned to the element size");
+    return run_paper_tree(p, in, master ? out : nullptr, p->stream);
+}
 fft_status fft_inverse(fft_plan p, const void* in, void* out) { return exec(p, in, out, true); }
 
 fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filter filter, double param) {
@@ -1077,8 +1237,6 @@ fft_status fft_plan_set_virtual_ranks(fft_plan p, int nranks) {
     if (p->comm) return fail(FFT_E_STATE, "plan has a communicator");
     if (nranks < 1 || p->n0 % nranks || (p->rank == 2 && p->n1 % nranks))
         return fail(FFT_E_INVALID_SIZE, "sizes must be divisible by the rank count");
-    if (p->rank == 1 && (int64_t)nranks * nranks > p->n0)
-        return fail(FFT_E_INVALID_SIZE, "1D four-step needs n >= nranks^2");
     p->virt = nranks;
     if (p->ws_owned && p->ws) {
         cudaFree(p->ws);
@@ -1096,6 +1254,10 @@ fft_status fft_plan_destroy(fft_plan p) {
     if (p->tw4) cudaFree(p->tw4);
     if (p->fta) cudaFree(p->fta);
     if (p->ftb) cudaFree(p->ftb);
+    if (p->tree_sub) fft_plan_destroy(p->tree_sub);
+    if (p->tta) cudaFree(p->tta);
+    if (p->ttb) cudaFree(p->ttb);
+    if (p->tws) cudaFree(p->tws);
     if (p->sub_a) fft_plan_destroy(p->sub_a);
     if (p->sub_b) fft_plan_destroy(p->sub_b);
     for (void* q : p->pa)

@@ -324,3 +324,94 @@ def test_block_layout_roundtrip():
     for row in range(SN):
         for v in range(16):
             assert flat[(((v >> sh) * SN + row) << sh) | (v & (SM - 1))] == a[row, v]
+
+
+# ---------------------------------------------- NEXT-2: the paper's tree
+def _branches(x, P):
+    """Rank q's branch = the cyclic subsequence x[q + P j]."""
+    return np.concatenate([x[q::P] for q in range(P)])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("m", [3, 10, 16, 20])
+def test_virtual_ranks_paper_tree(P, m):
+    """fft_forward_paper_tree on P virtual ranks: branch FFTs of the cyclic
+    subsequences, log2 P combine rounds, the MASTER's vector = (1/n) DFT."""
+    b = _lib()
+    n = 1 << m
+    x = fixtures.complex_input(n, fixtures.NORMAL, seed=800 + m)
+    p = b.Plan((n,), batch=1)
+    if P > 1:
+        p.set_virtual_ranks(P)
+    xd = torch.from_numpy(_branches(x, P)).cuda()
+    out = torch.empty(n, dtype=torch.complex64, device="cuda")
+    p.forward_paper_tree(xd, out)
+    torch.cuda.synchronize()
+    p.destroy()
+    assert oracle.rel_l2(out.cpu().numpy(), oracle.fft(x)) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_paper_tree_nccl_single_rank():
+    """The NCCL branch of the schedule with a 1-rank communicator (no rounds)."""
+    b = _lib()
+    n = 1 << 14
+    x = fixtures.complex_input(n, fixtures.NORMAL, seed=810)
+    p = b.Plan((n,), batch=1)
+    p.set_comm(b.nccl_unique_id(), 1, 0)
+    out = torch.empty(n, dtype=torch.complex64, device="cuda")
+    p.forward_paper_tree(torch.from_numpy(x).cuda(), out)
+    torch.cuda.synchronize()
+    p.destroy()
+    assert oracle.rel_l2(out.cpu().numpy(), oracle.fft(x)) <= 1e-5
+
+
+def _worker_tree(rank, world, port, m, q):
+    """The library's tree protocol (plan.cu run_paper_tree) with numpy local
+    steps and gloo point-to-point messages: round S sends q + S/2 -> q."""
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        P, n = world, 1 << m
+        x = fixtures.complex_input(n, fixtures.NORMAL, seed=33, dtype=np.complex128)
+        v = oracle.fft(x[rank::P])  # branch, with its 1/len
+        S = P
+        while S > 1:
+            if rank >= S:
+                break
+            if rank >= S // 2:
+                dist.send(torch.from_numpy(np.ascontiguousarray(v)), rank - S // 2)
+                break
+            o = torch.empty(v.size, dtype=torch.complex128)
+            dist.recv(o, rank + S // 2)
+            M = v.size
+            w = np.exp(-2j * np.pi * np.arange(M) / (2 * M))
+            v = np.concatenate([(v + w * o.numpy()) / 2, (v - w * o.numpy()) / 2])
+            S //= 2
+        q.put((rank, oracle.rel_l2(v, oracle.fft(x)) if rank == 0 else 0.0))
+    except Exception as exc:
+        q.put((rank, f"error: {exc!r}"))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_paper_tree_protocol(world):
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_tree, args=(r, world, port, 10, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=90) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[0] <= 1e-13, res
