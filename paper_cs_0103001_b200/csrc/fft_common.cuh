@@ -174,28 +174,39 @@ __device__ __forceinline__ void dft(C* v) {
 
 // --------------------------------------------------------------------------
 // Radix schedule of an R-point DFT done inside one CTA (R = 2^m <= 8192):
-// sub-passes of radix 16, then one remainder radix (2, 4 or 8) last.
+// sub-passes of the largest radix 2^ML (ML = 4: radix 16, the default; ML
+// = 3: radix 8, for kernels that keep E = 8 values per thread), then one
+// remainder radix last.
 // --------------------------------------------------------------------------
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
-__host__ __device__ constexpr int n_steps(int R) {
-    return R <= 16 ? 1 : (ilog2c(R) / 4 + ((ilog2c(R) % 4) ? 1 : 0));
+__host__ __device__ constexpr int n_steps(int R, int ML = 4) {
+    return R <= (1 << ML) ? 1 : (ilog2c(R) / ML + ((ilog2c(R) % ML) ? 1 : 0));
 }
-__host__ __device__ constexpr int radix_at(int R, int s) {
-    return R <= 16 ? R : ((s < ilog2c(R) / 4) ? 16 : (1 << (ilog2c(R) % 4)));
+__host__ __device__ constexpr int radix_at(int R, int s, int ML = 4) {
+    return R <= (1 << ML) ? R : ((s < ilog2c(R) / ML) ? (1 << ML) : (1 << (ilog2c(R) % ML)));
 }
-__host__ __device__ constexpr int span_at(int R, int s) {  // product of radices before step s
-    return s == 0 ? 1 : span_at(R, s - 1) * radix_at(R, s - 1);
+__host__ __device__ constexpr int span_at(int R, int s, int ML = 4) {  // product of radices before step s
+    return s == 0 ? 1 : span_at(R, s - 1, ML) * radix_at(R, s - 1, ML);
 }
 
 // offset of step s's twiddles in the step-major table of an R-point DFT:
 // step s (s >= 1) owns (rho_s - 1) * Ns_s entries laid out [r - 1][k],
 // value W_{Ns rho}^{k r}; consecutive k (consecutive threads) are adjacent.
-__host__ __device__ constexpr int tw_off(int R, int s) {
-    return s <= 1 ? 0 : tw_off(R, s - 1) + (radix_at(R, s - 1) - 1) * span_at(R, s - 1);
+__host__ __device__ constexpr int tw_off(int R, int s, int ML = 4) {
+    return s <= 1 ? 0 : tw_off(R, s - 1, ML) + (radix_at(R, s - 1, ML) - 1) * span_at(R, s - 1, ML);
 }
-__host__ __device__ constexpr int tw_size(int R) { return tw_off(R, n_steps(R)); }
-// all R = 2, 4, ..., 8192 tables concatenated: base offset of R's table
-__host__ __device__ constexpr int tw_base(int R) { return R <= 2 ? 0 : tw_base(R / 2) + tw_size(R / 2); }
+__host__ __device__ constexpr int tw_size(int R, int ML = 4) { return tw_off(R, n_steps(R, ML), ML); }
+// all R = 2, 4, ..., 8192 tables concatenated (the ML = 4 set first, then
+// the ML = 3 set): base offset of R's table
+__host__ __device__ constexpr int tw_base_ml(int R, int ML) {
+    return R <= 2 ? 0 : tw_base_ml(R / 2, ML) + tw_size(R / 2, ML);
+}
+__host__ __device__ constexpr int tw_base(int R, int ML = 4) {
+    return ML == 4 ? tw_base_ml(R, 4) : tw_base_ml(16384, 4) + tw_base_ml(R, ML);
+}
+__host__ __device__ constexpr int tw_total() { return tw_base_ml(16384, 4) + tw_base_ml(16384, 3); }
+// largest radix of a kernel holding E values per thread
+__host__ __device__ constexpr int ml_of(int E) { return E >= 16 ? 4 : (E >= 8 ? 3 : 4); }
 
 // padded shared-memory index: one spare slot every 16 elements (breaks the
 // stride-16 bank pattern of the first Stockham write)

@@ -36,11 +36,12 @@ __device__ __forceinline__ int swz16(int i) { return i ^ ((i >> 4) & 15); }
 template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false>
 struct LineFFT {
     using C = cpx<T>;
+    static constexpr int ML = ml_of(E);  // largest radix 2^ML (16, or 8 when E = 8)
     static constexpr int TPL = R / E;
-    static constexpr int S = n_steps(R);
+    static constexpr int S = n_steps(R, ML);
     static constexpr int LS = pad16c(R) + 1;  // odd line stride in smem (slots)
-    static constexpr int RHO0 = radix_at(R, 0);
-    static constexpr int RHOL = radix_at(R, S - 1);
+    static constexpr int RHO0 = radix_at(R, 0, ML);
+    static constexpr int RHOL = radix_at(R, S - 1, ML);
     static_assert(E % RHO0 == 0 && E % RHOL == 0, "E must be a multiple of every radix");
 
     // register slot of boundary element m (element index lt + TPL m)
@@ -53,13 +54,13 @@ struct LineFFT {
 
     template <int s>
     __device__ __forceinline__ static void compute(C* v, int lt, const C* __restrict__ tw) {
-        constexpr int rho = radix_at(R, s), Ns = span_at(R, s), nb = E / rho;
+        constexpr int rho = radix_at(R, s, ML), Ns = span_at(R, s, ML), nb = E / rho;
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
             if constexpr (Ns > 1) {
                 const int j = lt + b * TPL;
                 const int k = j & (Ns - 1);
-                const C* __restrict__ ts = tw + tw_off(R, s) + k;
+                const C* __restrict__ ts = tw + tw_off(R, s, ML) + k;
 #pragma unroll
                 for (int r = 1; r < rho; ++r) {
                     const C w = __ldg(ts + (r - 1) * Ns);
@@ -75,7 +76,7 @@ struct LineFFT {
     // they are few enough: (rho - 1) * nb <= 16 complex values.
     template <int s>
     static constexpr int ntw() {
-        return (span_at(R, s) > 1) ? (radix_at(R, s) - 1) * (E / radix_at(R, s)) : 0;
+        return (span_at(R, s, ML) > 1) ? (radix_at(R, s, ML) - 1) * (E / radix_at(R, s, ML)) : 0;
     }
     template <int s>
     static constexpr bool prefetch_tw() {
@@ -83,18 +84,18 @@ struct LineFFT {
     }
     template <int s>
     __device__ __forceinline__ static void load_tw(C* w, int lt, const C* __restrict__ tw) {
-        constexpr int rho = radix_at(R, s), Ns = span_at(R, s), nb = E / rho;
+        constexpr int rho = radix_at(R, s, ML), Ns = span_at(R, s, ML), nb = E / rho;
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
             const int k = (lt + b * TPL) & (Ns - 1);
-            const C* __restrict__ ts = tw + tw_off(R, s) + k;
+            const C* __restrict__ ts = tw + tw_off(R, s, ML) + k;
 #pragma unroll
             for (int r = 1; r < rho; ++r) w[b * (rho - 1) + r - 1] = __ldg(ts + (r - 1) * Ns);
         }
     }
     template <int s>
     __device__ __forceinline__ static void compute_tw(C* v, const C* w) {
-        constexpr int rho = radix_at(R, s), nb = E / rho;
+        constexpr int rho = radix_at(R, s, ML), nb = E / rho;
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
 #pragma unroll
@@ -108,7 +109,7 @@ struct LineFFT {
     // (folded into the LDS/STS immediates) cover every element.
     template <int s>
     __device__ __forceinline__ static void write_out(C* line, const C* v, int lt) {
-        constexpr int rho = radix_at(R, s), Ns = span_at(R, s), nb = E / rho;
+        constexpr int rho = radix_at(R, s, ML), Ns = span_at(R, s, ML), nb = E / rho;
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
             const int j = lt + b * TPL;
@@ -134,7 +135,7 @@ struct LineFFT {
 
     template <int s>
     __device__ __forceinline__ static void read_in(const C* line, C* v, int lt) {
-        constexpr int rho = radix_at(R, s), nb = E / rho;
+        constexpr int rho = radix_at(R, s, ML), nb = E / rho;
         constexpr int st = R / rho;
 #pragma unroll
         for (int b = 0; b < nb; ++b) {

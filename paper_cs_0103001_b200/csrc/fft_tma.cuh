@@ -64,8 +64,8 @@ struct RowsTmaCfg {
 // is the transposed real grid.  Half the lines, half the bytes of promoting
 // each real row to complex.
 template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false, bool TRANS = false,
-          bool PAIR = false>
-__global__ void __launch_bounds__(W*(R / E), 1)
+          bool PAIR = false, int MINB = 1>
+__global__ void __launch_bounds__(W*(R / E), MINB)
     k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
                const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt) {
     using C = cpx<T>;

@@ -50,14 +50,14 @@ cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double s
 }
 
 // persistent TMA-fed variant (fft_tma.cuh): 3 stages of ~64 KiB, 512 threads
-template <typename T, int R, bool INV, bool REAL_IN, bool FILT, bool TRANS = false, bool PAIR = false>
+template <typename T, int R, bool INV, bool REAL_IN, bool FILT, bool TRANS = false, bool PAIR = false, int E = 16,
+          int OCC = 1>
 cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw, const void* rowfilt,
                        cudaStream_t st) {
-    constexpr int E = 16;
     constexpr int W = (int)((64 * 1024) / (R * sizeof(cpx<T>))) < 1 ? 1 : (int)((64 * 1024) / (R * sizeof(cpx<T>)));
-    constexpr int STAGES = 3;
+    constexpr int STAGES = OCC > 1 ? 1 : 3;  // OCC CTAs per SM (registers capped) with one stage each
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
-    auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS, PAIR>;
+    auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS, PAIR, OCC>;
     static int grid_max = 0;
     if (!grid_max) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
@@ -72,9 +72,19 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     const int64_t tiles = (batch + W - 1) / W;
     const int grid = (int)(tiles < grid_max ? tiles : grid_max);
     kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(in, reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
-                                                   reinterpret_cast<const cpx<T>*>(tw) + tw_base(R),
+                                                   reinterpret_cast<const cpx<T>*>(tw) + tw_base(R, ml_of(E)),
                                                    reinterpret_cast<const T*>(rowfilt));
     return cudaGetLastError();
+}
+
+// B200FFT_ROWS_E=8: the 2048- and 8192-point row kernels with 8 values per
+// thread (radix-8 steps, twice the threads per row) -- a tuning knob
+int rows_e() {
+    static const int v = [] {
+        const char* e = getenv("B200FFT_ROWS_E");
+        return e ? atoi(e) : 16;
+    }();
+    return v;
 }
 
 template <bool INV, bool REAL_IN, bool FILT>
@@ -84,9 +94,20 @@ cudaError_t rows_tma_r(int64_t R, const void* in, void* out, int64_t batch, doub
         case 256: return rows_tma_t<float, 256, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         case 512: return rows_tma_t<float, 512, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         case 1024: return rows_tma_t<float, 1024, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
-        case 2048: return rows_tma_t<float, 2048, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 2048:
+            if (rows_e() == 8)
+                return rows_tma_t<float, 2048, INV, REAL_IN, FILT, false, false, 8>(in, out, batch, scale, tw, rowfilt,
+                                                                                 st);
+            return rows_tma_t<float, 2048, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         case 4096: return rows_tma_t<float, 4096, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
-        case 8192: return rows_tma_t<float, 8192, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 8192:
+            if (rows_e() == 8)
+                return rows_tma_t<float, 8192, INV, REAL_IN, FILT, false, false, 8>(in, out, batch, scale, tw, rowfilt,
+                                                                                 st);
+            if (rows_e() == 2)
+                return rows_tma_t<float, 8192, INV, REAL_IN, FILT, false, false, 16, 2>(in, out, batch, scale, tw,
+                                                                                     rowfilt, st);
+            return rows_tma_t<float, 8192, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -110,6 +131,12 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
         case 1024:
             return rows_tma_t<float, 1024, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
         case 2048:
+            if (rows_e() == 8)
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 8>(in, out, batch, scale, tw, rowfilt,
+                                                                                 st);
+            if (rows_e() == 2)
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 2>(in, out, batch, scale, tw,
+                                                                                     rowfilt, st);
             return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
         default: return cudaErrorInvalidValue;
     }

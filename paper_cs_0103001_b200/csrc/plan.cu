@@ -81,15 +81,17 @@ struct DeviceTables {
 // (fft_common.cuh tw_base / tw_off): entry [r - 1][k] of step s is
 // W_{Ns rho}^{k r} = exp(-2 pi i k r / (Ns rho)).
 void fill_step_tables(std::vector<double>& v) {
-    const int total = tw_base(2 * RMAX);
+    static_assert(2 * RMAX == 16384, "tw_base's concatenation bound");
+    const int total = tw_total();
     v.assign(2 * (size_t)total, 0.0);
+    for (int ml = 4; ml >= 3; --ml)
     for (int R = 2; R <= RMAX; R *= 2) {
-        for (int s = 1; s < n_steps(R); ++s) {
-            const int rho = radix_at(R, s), Ns = span_at(R, s);
+        for (int s = 1; s < n_steps(R, ml); ++s) {
+            const int rho = radix_at(R, s, ml), Ns = span_at(R, s, ml);
             const int64_t n = (int64_t)Ns * rho;
             for (int r = 1; r < rho; ++r)
                 for (int k = 0; k < Ns; ++k) {
-                    const int64_t idx = (int64_t)tw_base(R) + tw_off(R, s) + (int64_t)(r - 1) * Ns + k;
+                    const int64_t idx = (int64_t)tw_base(R, ml) + tw_off(R, s, ml) + (int64_t)(r - 1) * Ns + k;
                     const int64_t x = ((int64_t)k * r) % n;
                     const double ang = -2.0 * M_PI * (double)x / (double)n;
                     v[2 * idx] = std::cos(ang);
