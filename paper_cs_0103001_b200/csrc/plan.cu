@@ -1114,7 +1114,14 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
     // transforms); 2D plans over the batch of grids.
     const int64_t unit = p->rank == 1 ? p->n0 : p->n0 * p->n1;  // elements per transform
     const int64_t units = p->batch;
-    const size_t target = (size_t)256 << 20;
+    // chunk size (B200FFT_HOST_CHUNK_MB, default 64 MiB): small enough that the
+    // pipeline fill (first H2D) and drain (last D2H) stay short, large
+    // enough to keep the copy engines at full rate
+    static const size_t target = [] {
+        const char* v = getenv("B200FFT_HOST_CHUNK_MB");
+        const long mb = v ? atol(v) : 64;
+        return (size_t)(mb > 0 ? mb : 64) << 20;
+    }();
     int64_t per = (int64_t)(target / (unit * eb));
     if (per < 1) per = 1;
     if (per > units) per = units;
