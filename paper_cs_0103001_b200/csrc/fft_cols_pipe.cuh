@@ -23,28 +23,42 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <typename T, int R, int W>
+template <typename T, int R, int W, int NS = 2>
 struct ColsPipeCfg {
     static constexpr int LSC = cols_ls<T, R, W>();
     static constexpr size_t STAGE_ELEMS = (size_t)W * LSC;
-    static constexpr size_t SMEM_BYTES = 2 * STAGE_ELEMS * sizeof(cpx<T>);
+    static constexpr size_t SMEM_BYTES = NS * STAGE_ELEMS * sizeof(cpx<T>);
 };
 
-template <typename T, int R, int E, int W, int MODE>
+// MODE 3 / 4 (the column direction of the 2D pipeline as a four-step over
+// the column length N = N1 N2): MODE 3 is the
+// forward column DFT (length R = N1, rows N2 M apart) followed by the
+// twiddle W_N^{n2 u} (n2 = col / tdiv); MODE 4 multiplies the loaded
+// element u by conj(W_N^{n2 u}) and runs the inverse DFT.  With kind 6,
+// MODE 2's filter is g[img + n1 * u] (the frequency k1 + N1 k2 of the
+// four-step's digit order).
+// NS: ring of NS stages, NS - 1 tiles prefetched ahead (HBM bytes in
+// flight per SM is what these streaming passes are bound by).
+template <typename T, int R, int E, int W, int MODE, int NS = 2>
 __global__ void __launch_bounds__(W*(R / E), 1)
     k_cols_pipe(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, int64_t S, int64_t nimg, T scale,
                 const cpx<T>* __restrict__ tw, FilterArgs filt) {
     using C = cpx<T>;
-    constexpr bool INV0 = (MODE == 1);
+    constexpr bool INV0 = (MODE == 1 || MODE == 4);
     using F = LineFFT<T, R, E, INV0, 0, true>;
     using FI = LineFFT<T, R, E, true, 0, true>;
-    using G = ColsPipeCfg<T, R, W>;
+    using G = ColsPipeCfg<T, R, W, NS>;
     constexpr int NT = W * F::TPL;
     constexpr int LSC = G::LSC;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* stage0 = reinterpret_cast<C*>(smem_raw);
     const int tid = threadIdx.x;
-    const int t = tid / F::TPL, lt = tid % F::TPL;
+    // short lines (TPL < 32): lines are the thread-fastest index, so a warp
+    // touches 32 different lines at one offset and the odd line stride keeps
+    // every exchange conflict-free (lane-fastest within a 4-/8-/16-thread line
+    // put several lines in one bank group: 4-way conflicts, profiles/README.md)
+    constexpr bool LF = F::TPL < 32;
+    const int t = LF ? tid % W : tid / F::TPL, lt = LF ? tid / W : tid % F::TPL;
     const int64_t tiles_per_img = (S + W - 1) / W;
     const int64_t ntiles = tiles_per_img * nimg;
 
@@ -66,14 +80,15 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         cp_async_commit();  // one group per call (possibly empty): uniform wait counts
     };
 
-    prefetch(blockIdx.x, 0);
+#pragma unroll
+    for (int j = 0; j < NS - 1; ++j) prefetch(blockIdx.x + (int64_t)j * gridDim.x, j);
     for (int64_t k = 0;; ++k) {
         const int64_t tile = blockIdx.x + k * gridDim.x;
         if (tile >= ntiles) break;
-        const int buf = (int)(k & 1);
-        prefetch(tile + gridDim.x, buf ^ 1);
-        cp_async_wait<1>();  // this thread's copies of tile k have landed
-        __syncthreads();     // ... and everyone else's
+        const int buf = (int)(k % NS);
+        prefetch(tile + (int64_t)(NS - 1) * gridDim.x, (int)((k + NS - 1) % NS));
+        cp_async_wait<NS - 1>();  // this thread's copies of tile k have landed
+        __syncthreads();          // ... and everyone else's
         const int64_t img = tile / tiles_per_img;
         const int64_t s0 = (tile - img * tiles_per_img) * W;
         const int wv = (int)((S - s0) < W ? (S - s0) : W);
@@ -82,8 +97,22 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         C v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
-        const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
+        if constexpr (MODE == 4) {
+            const int64_t n2 = (s0 + t) / filt.tdiv;
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                v[F::pos_in(m)] = cmulc(v[F::pos_in(m)],
+                                        __ldg(reinterpret_cast<const C*>(filt.tw_l) + n2 * (lt + F::TPL * m)));
+        }
+        const int bar = (!LF && F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
         F::run(v, line, lt, tw, bar);
+        if constexpr (MODE == 3) {
+            const int64_t n2 = (s0 + t) / filt.tdiv;
+#pragma unroll
+            for (int m = 0; m < E; ++m)
+                v[F::pos_out(m)] = cmul(v[F::pos_out(m)],
+                                        __ldg(reinterpret_cast<const C*>(filt.tw_l) + n2 * (lt + F::TPL * m)));
+        }
         if constexpr (MODE == 2) {
             C w[E];
             const int64_t col = s0 + t;
@@ -96,7 +125,9 @@ __global__ void __launch_bounds__(W*(R / E), 1)
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const int64_t u = lt + F::TPL * m;
-                const T h = (col < S) ? filter_value<T>(filt, u, col + filt.col_off) * scale : (T)0;
+                const T hv = (filt.kind == 6) ? __ldg(reinterpret_cast<const T*>(filt.gu) + img + filt.n1 * u)
+                                              : filter_value<T>(filt, u, col + filt.col_off);
+                const T h = (col < S) ? hv * scale : (T)0;
                 w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], h);
             }
             FI::run(w, line, lt, tw, bar);
@@ -116,7 +147,7 @@ __global__ void __launch_bounds__(W*(R / E), 1)
             const int tt = idx % W, r = idx / W;
             if (tt < wv) dst[(int64_t)r * S + tt] = sm[tt * LSC + pad16(r)];
         }
-        __syncthreads();  // buffer `buf` is free for the prefetch two tiles ahead
+        __syncthreads();  // buffer `buf` is free for the prefetch NS tiles ahead
     }
     cp_async_wait<0>();
 }

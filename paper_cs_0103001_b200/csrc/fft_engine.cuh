@@ -301,6 +301,12 @@ struct FilterArgs {
     int64_t col_off;    // global index of local column 0 (column slab of a distributed plan)
     float* spec;        // optional (MODE 2, complex64): |F(u,v)| * spec_scale -> spec[img][u][v]
     float spec_scale;   // eq5's 1/N (the column pass holds the unnormalised 2D sums)
+    // four-step column passes (k_cols_pipe MODE 3 / 4, kind 6): twiddle
+    // W_L^{(col / tdiv) * u} from tw_l (L entries, fp64-generated), and the
+    // pass-B filter index img + n1 * u into gu
+    const void* tw_l;
+    int64_t tdiv;
+    int64_t n1;
 };
 
 // spectrum sqrt(Re^2 + Im^2) of one forward-transformed column (Sec. 6,
@@ -356,7 +362,12 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* smem = reinterpret_cast<C*>(smem_raw);
     const int tid = threadIdx.x;
-    const int t = tid / F::TPL, lt = tid % F::TPL;
+    // short lines (TPL < 32): lines are the thread-fastest index, so a warp
+    // touches 32 different lines at one offset and the odd line stride keeps
+    // every exchange conflict-free (lane-fastest within a 4-/8-/16-thread line
+    // put several lines in one bank group: 4-way conflicts, profiles/README.md)
+    constexpr bool LF = F::TPL < 32;
+    const int t = LF ? tid % W : tid / F::TPL, lt = LF ? tid / W : tid % F::TPL;
     const int64_t s0 = (int64_t)blockIdx.x * W;
     const int64_t img = blockIdx.y;
     const C* src = in + img * (int64_t)R * S + s0;
@@ -376,7 +387,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
 #pragma unroll
     for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
     // lines synchronise on their own named barrier (1 + t) between steps
-    const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
+    const int bar = (!LF && F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
     F::run(v, line, lt, tw, bar);
     if constexpr (MODE == 2) {
         C w[E];
@@ -432,7 +443,12 @@ __global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ i
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* smem = reinterpret_cast<C*>(smem_raw);
     const int tid = threadIdx.x;
-    const int t = tid / F::TPL, lt = tid % F::TPL;
+    // short lines (TPL < 32): lines are the thread-fastest index, so a warp
+    // touches 32 different lines at one offset and the odd line stride keeps
+    // every exchange conflict-free (lane-fastest within a 4-/8-/16-thread line
+    // put several lines in one bank group: 4-way conflicts, profiles/README.md)
+    constexpr bool LF = F::TPL < 32;
+    const int t = LF ? tid % W : tid / F::TPL, lt = LF ? tid / W : tid % F::TPL;
     const int64_t LR = L / R;                     // butterflies per transform
     const int64_t gl0 = (int64_t)blockIdx.x * W;  // first line of the tile (W | LR)
     const int64_t bidx = gl0 / LR;

@@ -39,7 +39,12 @@ __global__ void __launch_bounds__(W*(R / E), 1)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* stage0 = reinterpret_cast<C*>(smem_raw);
     const int tid = threadIdx.x;
-    const int t = tid / F::TPL, lt = tid % F::TPL;
+    // short lines (TPL < 32): lines are the thread-fastest index, so a warp
+    // touches 32 different lines at one offset and the odd line stride keeps
+    // every exchange conflict-free (lane-fastest within a 4-/8-/16-thread line
+    // put several lines in one bank group: 4-way conflicts, profiles/README.md)
+    constexpr bool LF = F::TPL < 32;
+    const int t = LF ? tid % W : tid / F::TPL, lt = LF ? tid / W : tid % F::TPL;
     const int tt = tid % W, r0 = tid / W;  // load / store mapping
     const int pr0 = pad16(r0);
     // padded slot of element r0 + it RS: compile-time offsets when RS is a
@@ -91,7 +96,7 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         C v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
-        const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
+        const int bar = (!LF && F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
         F::run(v, line, lt, tw, bar);
         F::lsync(bar);
 #pragma unroll
@@ -181,7 +186,12 @@ __global__ void __launch_bounds__(W*(R / E), 1)
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(smem_raw + G::BAR_OFF);
     const uint32_t st0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const int tid = threadIdx.x;
-    const int t = tid / F::TPL, lt = tid % F::TPL;
+    // short lines (TPL < 32): lines are the thread-fastest index, so a warp
+    // touches 32 different lines at one offset and the odd line stride keeps
+    // every exchange conflict-free (lane-fastest within a 4-/8-/16-thread line
+    // put several lines in one bank group: 4-way conflicts, profiles/README.md)
+    constexpr bool LF = F::TPL < 32;
+    const int t = LF ? tid % W : tid / F::TPL, lt = LF ? tid / W : tid % F::TPL;
     const int64_t LR = L / R;
     const int64_t ntiles = nlines / W;
     const int64_t KLO = (int64_t)1 << klo_sh;
@@ -249,7 +259,7 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         C v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
-        const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
+        const int bar = (!LF && F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
         F::run(v, line, lt, tw, bar);
         F::lsync(bar);
 #pragma unroll

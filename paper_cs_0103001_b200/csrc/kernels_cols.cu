@@ -12,14 +12,16 @@ namespace {
 
 // persistent double-buffered variant (fft_cols_pipe.cuh), complex64,
 // 256 <= R <= 4096: W columns per tile so that two tiles fit in smem
-template <int R> constexpr int pipe_w() { return R >= 4096 ? 2 : (R >= 2048 ? 4 : (R >= 1024 ? 8 : 16)); }
+template <int R> constexpr int pipe_w() {
+    return R >= 4096 ? 2 : (R >= 2048 ? 4 : (R >= 1024 ? 8 : (R >= 256 ? 16 : (R >= 128 ? 32 : 64))));
+}
 
-template <int R, int MODE>
+template <int R, int MODE, int WF = 0, int NS = 2>
 cudaError_t cols_pipe_t(const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
                         const FilterArgs& f, cudaStream_t st) {
-    constexpr int E = 16, W = pipe_w<R>();
-    using G = ColsPipeCfg<float, R, W>;
-    auto kern = k_cols_pipe<float, R, E, W, MODE>;
+    constexpr int E = 16, W = WF ? WF : pipe_w<R>();
+    using G = ColsPipeCfg<float, R, W, NS>;
+    auto kern = k_cols_pipe<float, R, E, W, MODE, NS>;
     static int grid_max = 0;
     if (!grid_max) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
@@ -43,6 +45,8 @@ template <int MODE>
 cudaError_t cols_pipe_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
                         const FilterArgs& f, cudaStream_t st) {
     switch (R) {
+        case 64: return cols_pipe_t<64, MODE>(in, out, S, nimg, scale, tw, f, st);
+        case 128: return cols_pipe_t<128, MODE>(in, out, S, nimg, scale, tw, f, st);
         case 256: return cols_pipe_t<256, MODE>(in, out, S, nimg, scale, tw, f, st);
         case 512: return cols_pipe_t<512, MODE>(in, out, S, nimg, scale, tw, f, st);
         case 1024: return cols_pipe_t<1024, MODE>(in, out, S, nimg, scale, tw, f, st);
@@ -129,6 +133,50 @@ cudaError_t cols_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg
 }
 
 }  // namespace
+
+// four-step column passes: short columns, so narrower tiles and a deeper
+// ring keep more HBM bytes in flight per SM (B200FFT_COLS4_CFG picks one)
+template <int MODE>
+cudaError_t cols4_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
+                    const FilterArgs& f, cudaStream_t st) {
+    static const int cfg = [] {
+        const char* v = getenv("B200FFT_COLS4_CFG");
+        return v ? atoi(v) : 1;
+    }();
+    if (cfg == 1) {
+        if (R == 64) return cols_pipe_t<64, MODE, 32, 4>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128) return cols_pipe_t<128, MODE, 16, 4>(in, out, S, nimg, scale, tw, f, st);
+    } else if (cfg == 2) {
+        if (R == 64) return cols_pipe_t<64, MODE, 16, 4>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128) return cols_pipe_t<128, MODE, 16, 3>(in, out, S, nimg, scale, tw, f, st);
+    } else if (cfg == 3) {
+        if (R == 64) return cols_pipe_t<64, MODE, 32, 6>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128) return cols_pipe_t<128, MODE, 32, 4>(in, out, S, nimg, scale, tw, f, st);
+    }
+    return cols_pipe_r<MODE>(R, in, out, S, nimg, scale, tw, f, st);
+}
+
+cudaError_t launch_cols_fourstep(int mode, int64_t R, const void* in, void* out, int64_t S, int64_t nimg,
+                                 double scale, const void* tw, const FilterArgs& f, cudaStream_t st) {
+    if (R < 64 || R > 4096) return cudaErrorInvalidValue;
+    switch (mode) {
+        case 2: return cols4_r<2>(R, in, out, S, nimg, scale, tw, f, st);
+        case 3: return cols4_r<3>(R, in, out, S, nimg, scale, tw, f, st);
+        case 4: return cols4_r<4>(R, in, out, S, nimg, scale, tw, f, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_cols_fourstep_default(int mode, int64_t R, const void* in, void* out, int64_t S, int64_t nimg,
+                                         double scale, const void* tw, const FilterArgs& f, cudaStream_t st) {
+    if (R < 64 || R > 4096) return cudaErrorInvalidValue;
+    switch (mode) {
+        case 2: return cols_pipe_r<2>(R, in, out, S, nimg, scale, tw, f, st);
+        case 3: return cols_pipe_r<3>(R, in, out, S, nimg, scale, tw, f, st);
+        case 4: return cols_pipe_r<4>(R, in, out, S, nimg, scale, tw, f, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
 
 cudaError_t launch_cols(int prec, int mode, int64_t R, const void* in, void* out, int64_t S,
                         int64_t nimg, double scale, const void* tw, const FilterArgs& f,

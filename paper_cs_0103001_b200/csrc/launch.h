@@ -38,6 +38,13 @@ cudaError_t launch_cols(int prec, int mode, int64_t R, const void* in, void* out
                         int64_t nimg, double scale, const void* tw, const FilterArgs& f,
                         cudaStream_t st);
 
+// The column direction of the 2D pipeline as a four-step (complex64,
+// 64 <= R <= 4096, k_cols_pipe): mode 3 = forward DFT over R rows + twiddle
+// W_L^{(col / f.tdiv) u}, mode 4 = conj twiddle + inverse DFT, mode 2 with
+// f.kind 6 = fwd * g[img + f.n1 u] * scale * inv.
+cudaError_t launch_cols_fourstep(int mode, int64_t R, const void* in, void* out, int64_t S, int64_t nimg,
+                                 double scale, const void* tw, const FilterArgs& f, cudaStream_t st);
+
 // Kernel family C: one global Stockham pass of radix R (128..1024) over
 // `batch` rows of length L with span Ns; pa/pb: the pass twiddle tables
 // (pa[r][k mod 2^klo_sh], pb[r][k >> klo_sh]).

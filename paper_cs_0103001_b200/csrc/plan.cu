@@ -165,6 +165,9 @@ struct fft_plan_s {
     void* ftb = nullptr;          // W_n^{i}
     int fsh = 0;
     double scale_override = 0.0;  // sub-plans: scale of the last pass (0 = the default)
+    // four-step column passes of the Gaussian pipeline: W_N^x, x < N
+    void* twl = nullptr;
+    int64_t twl_n = 0;
     // the paper's own tree schedule (NEXT-2, fft_forward_paper_tree)
     fft_plan_s* tree_sub = nullptr;  // branch FFTs: length n / P, batch = local ranks
     void* tta = nullptr;             // W_n^{i << tsh}
@@ -397,6 +400,50 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
             if (e != cudaSuccess) return cuda_fail(e, "k_rows_tma (transposed) launch");
         }
         p->last_launches = (int)(2 * p->batch);
+        return FFT_OK;
+    }
+    // rows pass (fwd * g_M * inv) -> the column direction as a four-step
+    // over N = 64 N2: A = column DFT over the
+    // 64 rows N2 apart + twiddle W_N^{n2 k1}; B = fwd * g_N[k1 + 64 k2] / N *
+    // inv over each block of N2 consecutive rows; A' = conj twiddle + inverse
+    // over the 64 rows.  No transposes, no 8192-long column lines.
+    const char* c4_env = getenv("B200FFT_PIPE_COLS4");
+    const bool c4_default = false;
+    if (filter == FFT_FILTER_GAUSS && !literal && p->prec == 0 && N >= 4096 && N <= 8192 && M >= 256 &&
+        M <= 8192 && (c4_env ? c4_env[0] == '1' : c4_default)) {
+        if (p->twl_n != N) {
+            if (p->twl) cudaFree(p->twl);
+            p->twl = nullptr;
+            std::vector<double> t(2 * (size_t)N);
+            for (int64_t x = 0; x < N; ++x) {
+                const double ang = -2.0 * M_PI * (double)x / (double)N;
+                t[2 * x] = std::cos(ang);
+                t[2 * x + 1] = std::sin(ang);
+            }
+            e = upload(t, p->prec, &p->twl);
+            if (e != cudaSuccess) return cuda_fail(e, "column twiddle upload");
+            p->twl_n = N;
+        }
+        const int64_t N1 = 64, N2 = N / 64;
+        const size_t in_grid = (size_t)N * M * (real_in ? 4 : p->elem_bytes());
+        const size_t grid = (size_t)N * M * p->elem_bytes();
+        FilterArgs fa{};
+        fa.tw_l = p->twl;
+        fa.tdiv = M;
+        FilterArgs fb{};
+        fb.kind = 6;
+        fb.gu = p->gu;
+        fb.n1 = N1;
+        for (int64_t g = 0; g < p->batch; ++g) {
+            char* o = (char*)out + g * grid;
+            e = launch_rows(p->prec, false, real_in, M, (const char*)in + g * in_grid, o, N, 1.0 / (double)M, p->tw,
+                            st, -1, -1, p->gv);
+            if (e == cudaSuccess) e = launch_cols_fourstep(3, N1, o, o, N2 * M, 1, 1.0, p->tw, fa, st);
+            if (e == cudaSuccess) e = launch_cols_fourstep(2, N2, o, o, M, N1, 1.0 / (double)N, p->tw, fb, st);
+            if (e == cudaSuccess) e = launch_cols_fourstep(4, N1, o, o, N2 * M, 1, 1.0, p->tw, fa, st);
+            if (e != cudaSuccess) return cuda_fail(e, "four-step column pipeline launch");
+        }
+        p->last_launches = (int)(4 * p->batch);
         return FFT_OK;
     }
     // rows pass -> tiled transpose -> rows pass (of the transposed grid) ->
@@ -633,7 +680,8 @@ fft_status tree_prepare(fft_plan_s* p) {
     const int64_t n = p->n0, L = n / P;
     const int nloc = p->comm ? 1 : P;
     if (!p->tree_sub || p->tree_sub->n0 != L || p->tree_sub->batch != nloc) {
-        if (p->tree_sub) fft_plan_destroy(p->tree_sub);
+        if (p->twl) cudaFree(p->twl);
+    if (p->tree_sub) fft_plan_destroy(p->tree_sub);
         p->tree_sub = nullptr;
         int64_t d = L;
         fft_status s = fft_plan_create_ex(&p->tree_sub, &d, 1, nloc, p->prec == 0 ? FFT_C64 : FFT_C128, 0);
