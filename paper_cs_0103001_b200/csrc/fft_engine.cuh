@@ -30,6 +30,9 @@ constexpr int RMAX = 8192;  // largest in-CTA DFT
 // a permutation inside every 16-element group that makes both the
 // consecutive and the stride-16 access patterns of the steps conflict-free
 __device__ __forceinline__ int swz16(int i) { return i ^ ((i >> 4) & 15); }
+// LAYOUT 2: 16 lines interleaved element by element (element x of line t at
+// x * 16 + t: a dense [R][16] TMA box of 16 columns); with the 16 lines as
+// the thread-fastest index every exchange is conflict-free
 
 // PF: prefetch each step's twiddles into registers before its exchange
 // barriers (for kernels with a 128-register budget)
@@ -118,6 +121,9 @@ struct LineFFT {
             if constexpr (LAYOUT == 1) {
 #pragma unroll
                 for (int q = 0; q < rho; ++q) line[swz16(base + q * Ns)] = v[b * rho + q];
+            } else if constexpr (LAYOUT == 2) {
+#pragma unroll
+                for (int q = 0; q < rho; ++q) line[(base + q * Ns) * 16] = v[b * rho + q];
             } else if constexpr (Ns % 16 == 0) {
                 const int pb = pad16(base);
 #pragma unroll
@@ -143,6 +149,9 @@ struct LineFFT {
             if constexpr (LAYOUT == 1) {
 #pragma unroll
                 for (int r = 0; r < rho; ++r) v[b * rho + r] = line[swz16(j + r * st)];
+            } else if constexpr (LAYOUT == 2) {
+#pragma unroll
+                for (int r = 0; r < rho; ++r) v[b * rho + r] = line[(j + r * st) * 16];
             } else if constexpr (st % 16 == 0) {
                 const int pj = pad16(j);
 #pragma unroll
@@ -157,6 +166,7 @@ struct LineFFT {
     // padded index of boundary element m (element lt + TPL m of the line)
     __device__ __forceinline__ static int bpos(int lt, int m) {
         if constexpr (LAYOUT == 1) return swz16(lt + TPL * m);
+        else if constexpr (LAYOUT == 2) return (lt + TPL * m) * 16;
         else if constexpr (TPL % 16 == 0) return pad16(lt) + m * (TPL + TPL / 16);
         else return pad16(lt + TPL * m);
     }
@@ -165,6 +175,10 @@ struct LineFFT {
     // threads of this line through named barrier `bar` -- lines of one CTA
     // then never wait for each other.  Needs TPL % 32 == 0 (whole warps).
     __device__ __forceinline__ static void lsync(int bar) {
+        if (bar < 0) {  // the -bar threads of a warp-specialised CTA's compute group (named barrier 1)
+            asm volatile("bar.sync 1, %0;\n" ::"r"(-bar) : "memory");
+            return;
+        }
         if constexpr (TPL % 32 == 0) {
             if (bar > 0) {
                 asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "n"(TPL) : "memory");

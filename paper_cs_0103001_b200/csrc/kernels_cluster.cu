@@ -1,7 +1,10 @@
 // kernels_cluster.cu -- instantiations and launcher of the one-pass cluster
 // FFT (fft_cluster.cuh) for 1D lengths that do not fit one CTA.
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 
+#include "fft_abbulk.cuh"
 #include "fft_cluster.cuh"
 #include "launch.h"
 
@@ -352,6 +355,154 @@ cudaError_t ab_pipe_t(const void* in, void* out, int64_t batch, double scale, co
     return cudaLaunchKernelExC(&cfg, (const void*)k, args);
 }
 
+template <bool INV>
+cudaError_t ab_bulk_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                      cudaStream_t st) {
+    using G = AbBulkCfg;
+    auto k = k_ab_bulk<INV>;
+    static int grid = 0, D = 0, ring_slots = 0;
+    static void* ring = nullptr;
+    static int* ctl = nullptr;
+    static int64_t ctl_n = 0;
+    if (!grid) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, G::SMEM);
+        if (e != cudaSuccess) return e;
+        grid = sms * (occ > 0 ? occ : 1);
+        D = (2 * grid + 15) / 16 + 8;
+        const char* rv = getenv("B200FFT_AB_RING");
+        ring_slots = D + (rv ? atoi(rv) : 16);
+        e = cudaMalloc(&ring, (size_t)ring_slots * 65536 * sizeof(float2));
+        if (e != cudaSuccess) return e;
+        if (getenv("B200FFT_VERBOSE")) fprintf(stderr, "ab_bulk: grid %d (occ %d), D %d, ring %d\n", grid, occ, D, ring_slots);
+    }
+    if (batch <= 0) return cudaSuccess;
+    if (ctl_n < 2 * batch) {
+        if (ctl) cudaFree(ctl);
+        cudaError_t e = cudaMalloc(&ctl, sizeof(int) * 2 * batch);
+        if (e != cudaSuccess) return e;
+        ctl_n = 2 * batch;
+    }
+    cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
+    if (e != cudaSuccess) return e;
+    AbBulkCtl c{ctl, ctl + batch, D, ring_slots};
+    const float2* a_in = reinterpret_cast<const float2*>(in);
+    float2* a_out = reinterpret_cast<float2*>(out);
+    float2* a_ring = reinterpret_cast<float2*>(ring);
+    float a_scale = (float)scale;
+    const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
+    const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
+    int64_t a_batch = batch;
+    void* args[] = {&a_in, &a_out, &a_ring, &a_batch, &a_scale, &a_tw4, &a_tw, &c};
+    const int64_t tasks = 32 * batch;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3((unsigned)(tasks < grid ? tasks : grid), 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, (const void*)k, args);
+}
+
+// tensor maps of variant 41 (cuTensorMapEncodeTiled through the runtime's
+// driver entry point: no libcuda link)
+bool encode3(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+             bool swz128) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !enc)
+            return false;
+    }
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {d0 * 8, d0 * d1 * 8};
+    const cuuint32_t box[3] = {b0, b1, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool INV, bool WS = false>
+cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                     cudaStream_t st) {
+    constexpr size_t SMEM = WS ? AbWsCfg::SMEM : AbTmaCfg::SMEM;
+    constexpr int NT = WS ? 288 : 256;
+    auto k = WS ? k_ab_ws<INV> : k_ab_tma<INV>;
+    static int grid = 0, D = 0, ring_slots = 0;
+    static void* ring = nullptr;
+    static int* ctl = nullptr;
+    static int64_t ctl_n = 0;
+    static CUtensorMap m_yst, m_yld;
+    if (!grid) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, SMEM);
+        if (e != cudaSuccess) return e;
+        grid = sms * (occ > 0 ? occ : 1);
+        // every wait must point at least (tasks in flight per CTA) x grid
+        // positions back in the task order: 2 for 41, NS = 3 for 42
+        const int depth = WS ? AbWsCfg::NS : 2;
+        const char* dv = getenv("B200FFT_AB_D");
+        D = (depth * grid + 15) / 16 + (dv ? atoi(dv) : 8);
+        const char* rv = getenv("B200FFT_AB_RING");
+        ring_slots = D + (rv ? atoi(rv) : (depth * grid + 31) / 32 + 8);
+        e = cudaMalloc(&ring, (size_t)ring_slots * 65536 * sizeof(float2));
+        if (e != cudaSuccess) return e;
+        if (!encode3(&m_yst, ring, 256, 256, ring_slots, 16, 256, false) ||
+            !encode3(&m_yld, ring, 256, 256, ring_slots, 256, 16, false))
+            return cudaErrorInvalidValue;
+        if (getenv("B200FFT_VERBOSE")) fprintf(stderr, "ab_tma(ws=%d): grid %d (occ %d), D %d, ring %d\n", (int)WS, grid, occ, D, ring_slots);
+    }
+    if (batch <= 0) return cudaSuccess;
+    CUtensorMap m_x, m_out;
+    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, false) ||
+        !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, true))
+        return cudaErrorInvalidValue;
+    if (ctl_n < 2 * batch) {
+        if (ctl) cudaFree(ctl);
+        cudaError_t e = cudaMalloc(&ctl, sizeof(int) * 2 * batch);
+        if (e != cudaSuccess) return e;
+        ctl_n = 2 * batch;
+    }
+    cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
+    if (e != cudaSuccess) return e;
+    AbBulkCtl c{ctl, ctl + batch, D, ring_slots};
+    float a_scale = (float)scale;
+    const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
+    const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
+    int64_t a_batch = batch;
+    const float2* a_ring = reinterpret_cast<const float2*>(ring);
+    static const int opts = [] {
+        const char* v = getenv("B200FFT_AB_OPTS");
+        return v ? atoi(v) : 1;  // 1: discard consumed Y rows from L2 (measured best)
+    }();
+    int a_opts = opts;
+    void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
+    const int64_t tasks = 32 * batch;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3((unsigned)(tasks < grid ? tasks : grid), 1, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, (const void*)k, args);
+}
+
 }  // namespace
 
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2) {
@@ -395,6 +546,9 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 27: return cluster6_t<float, 5, INV, false>(in, out, batch, scale, tw4, tw, st);
         case 28: return ab_pipe_t<float, 3, INV>(in, out, batch, scale, tw4, tw, st);
         case 31: return cluster2_t<float, 256, 256, 16, 16, 6, INV, true, true>(in, out, batch, scale, tw4, tw, st);
+        case 40: return ab_bulk_t<INV>(in, out, batch, scale, tw4, tw, st);
+        case 41: return ab_tma_t<INV>(in, out, batch, scale, tw4, tw, st);
+        case 42: return ab_tma_t<INV, true>(in, out, batch, scale, tw4, tw, st);
         case 29: return ab_pipe_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
         case 30: return ab_pipe_t<float, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 22: return step_ab2_t<float, INV>(in, out, batch, scale, tw4, tw, st);
