@@ -431,53 +431,68 @@ bool encode3(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool INV, bool WS = false>
-cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
-                     cudaStream_t st) {
-    constexpr size_t SMEM = WS ? AbWsCfg::SMEM : AbTmaCfg::SMEM;
-    constexpr int NT = WS ? 288 : 256;
-    auto k = WS ? k_ab_ws<INV> : k_ab_tma<INV>;
-    static int grid = 0, D = 0, ring_slots = 0;
-    static void* ring = nullptr;
-    static int* ctl = nullptr;
-    static int64_t ctl_n = 0;
-    static CUtensorMap m_yst, m_yld;
-    if (!grid) {
+// launch geometry of variants 41 / 42 (cached per kernel): persistent grid,
+// dependency distance D (transforms) and ring slots
+struct AbGeom {
+    int grid = 0, D = 0, ring = 0;
+};
+template <bool INV, bool WS>
+cudaError_t ab_geom(AbGeom* g) {
+    static AbGeom cached;
+    if (!cached.grid) {
+        constexpr size_t SMEM = WS ? AbWsCfg::SMEM : AbTmaCfg::SMEM;
+        constexpr int NT = WS ? 288 : 256;
+        auto k = WS ? k_ab_ws<INV> : k_ab_tma<INV>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
         int dev = 0, sms = 0, occ = 0;
         if (e == cudaSuccess) e = cudaGetDevice(&dev);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, SMEM);
         if (e != cudaSuccess) return e;
-        grid = sms * (occ > 0 ? occ : 1);
+        AbGeom t;
+        t.grid = sms * (occ > 0 ? occ : 1);
         // every wait must point at least (tasks in flight per CTA) x grid
         // positions back in the task order: 2 for 41, NS = 3 for 42
         const int depth = WS ? AbWsCfg::NS : 2;
         const char* dv = getenv("B200FFT_AB_D");
-        D = (depth * grid + 15) / 16 + (dv ? atoi(dv) : 8);
+        t.D = (depth * t.grid + 15) / 16 + (dv ? atoi(dv) : 8);
         const char* rv = getenv("B200FFT_AB_RING");
-        ring_slots = D + (rv ? atoi(rv) : (depth * grid + 31) / 32 + 8);
-        e = cudaMalloc(&ring, (size_t)ring_slots * 65536 * sizeof(float2));
-        if (e != cudaSuccess) return e;
-        if (!encode3(&m_yst, ring, 256, 256, ring_slots, 16, 256, false) ||
-            !encode3(&m_yld, ring, 256, 256, ring_slots, 256, 16, false))
-            return cudaErrorInvalidValue;
-        if (getenv("B200FFT_VERBOSE")) fprintf(stderr, "ab_tma(ws=%d): grid %d (occ %d), D %d, ring %d\n", (int)WS, grid, occ, D, ring_slots);
+        t.ring = t.D + (rv ? atoi(rv) : (depth * t.grid + 31) / 32 + 8);
+        if (getenv("B200FFT_VERBOSE"))
+            fprintf(stderr, "ab_tma(ws=%d): grid %d (occ %d), D %d, ring %d\n", (int)WS, t.grid, occ, t.D, t.ring);
+        cached = t;
     }
-    if (batch <= 0) return cudaSuccess;
-    CUtensorMap m_x, m_out;
-    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, false) ||
-        !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, true))
-        return cudaErrorInvalidValue;
-    if (ctl_n < 2 * batch) {
-        if (ctl) cudaFree(ctl);
-        cudaError_t e = cudaMalloc(&ctl, sizeof(int) * 2 * batch);
-        if (e != cudaSuccess) return e;
-        ctl_n = 2 * batch;
-    }
-    cudaError_t e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
+    *g = cached;
+    return cudaSuccess;
+}
+
+// caller-provided scratch: the Y ring (ring x 512 KiB) then the counters
+size_t ab_ws_bytes(int64_t ring, int64_t batch) {
+    return (size_t)ring * 65536 * sizeof(float2) + (size_t)2 * batch * sizeof(int);
+}
+
+template <bool INV, bool WS = false>
+cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                     void* ws, size_t ws_bytes, cudaStream_t st) {
+    constexpr size_t SMEM = WS ? AbWsCfg::SMEM : AbTmaCfg::SMEM;
+    constexpr int NT = WS ? 288 : 256;
+    auto k = WS ? k_ab_ws<INV> : k_ab_tma<INV>;
+    AbGeom g;
+    cudaError_t e = ab_geom<INV, WS>(&g);
     if (e != cudaSuccess) return e;
-    AbBulkCtl c{ctl, ctl + batch, D, ring_slots};
+    if (batch <= 0) return cudaSuccess;
+    if (!ws || ws_bytes < ab_ws_bytes(g.ring, batch)) return cudaErrorInvalidValue;
+    void* ring = ws;
+    int* ctl = reinterpret_cast<int*>((char*)ws + (size_t)g.ring * 65536 * sizeof(float2));
+    CUtensorMap m_x, m_out, m_yst, m_yld;
+    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, false) ||
+        !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, true) ||
+        !encode3(&m_yst, ring, 256, 256, g.ring, 16, 256, false) ||
+        !encode3(&m_yld, ring, 256, 256, g.ring, 256, 16, false))
+        return cudaErrorInvalidValue;
+    e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
+    if (e != cudaSuccess) return e;
+    AbBulkCtl c{ctl, ctl + batch, g.D, g.ring};
     float a_scale = (float)scale;
     const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
     const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
@@ -494,7 +509,7 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
-    cfg.gridDim = dim3((unsigned)(tasks < grid ? tasks : grid), 1, 1);
+    cfg.gridDim = dim3((unsigned)(tasks < g.grid ? tasks : g.grid), 1, 1);
     cfg.blockDim = dim3(NT, 1, 1);
     cfg.dynamicSmemBytes = SMEM;
     cfg.stream = st;
@@ -517,7 +532,7 @@ bool cluster_supported(int prec, int64_t n, int* n1, int* n2) {
 
 template <bool INV>
 cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch, double scale, const void* tw4,
-                          const void* tw, cudaStream_t st) {
+                          const void* tw, cudaStream_t st, void* ws, size_t ws_bytes) {
     switch (variant) {
         case 0: return cluster_t<float, 256, 256, 16, 16, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 1: return cluster_t<float, 256, 256, 8, 32, 2, INV>(in, out, batch, scale, tw4, tw, st);
@@ -547,8 +562,8 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 28: return ab_pipe_t<float, 3, INV>(in, out, batch, scale, tw4, tw, st);
         case 31: return cluster2_t<float, 256, 256, 16, 16, 6, INV, true, true>(in, out, batch, scale, tw4, tw, st);
         case 40: return ab_bulk_t<INV>(in, out, batch, scale, tw4, tw, st);
-        case 41: return ab_tma_t<INV>(in, out, batch, scale, tw4, tw, st);
-        case 42: return ab_tma_t<INV, true>(in, out, batch, scale, tw4, tw, st);
+        case 41: return ab_tma_t<INV>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
+        case 42: return ab_tma_t<INV, true>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 29: return ab_pipe_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
         case 30: return ab_pipe_t<float, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 22: return step_ab2_t<float, INV>(in, out, batch, scale, tw4, tw, st);
@@ -560,11 +575,20 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
     }
 }
 
+size_t cluster_workspace_bytes(int prec, int64_t n, int variant, int64_t batch) {
+    if (prec != 0 || n != 65536 || (variant != 41 && variant != 42)) return 0;
+    AbGeom g;
+    cudaError_t e = variant == 42 ? ab_geom<false, true>(&g) : ab_geom<false, false>(&g);
+    if (e != cudaSuccess) return 0;
+    return ab_ws_bytes(g.ring, batch);
+}
+
 cudaError_t launch_cluster(int prec, bool inv, int64_t n, const void* in, void* out, int64_t batch,
-                           double scale, const void* tw4, const void* tw, int variant, cudaStream_t st) {
+                           double scale, const void* tw4, const void* tw, int variant, cudaStream_t st, void* ws,
+                           size_t ws_bytes) {
     if (prec == 0 && n == 65536)
-        return inv ? cluster_65536<true>(variant, in, out, batch, scale, tw4, tw, st)
-                   : cluster_65536<false>(variant, in, out, batch, scale, tw4, tw, st);
+        return inv ? cluster_65536<true>(variant, in, out, batch, scale, tw4, tw, st, ws, ws_bytes)
+                   : cluster_65536<false>(variant, in, out, batch, scale, tw4, tw, st, ws, ws_bytes);
     return cudaErrorInvalidValue;
 }
 

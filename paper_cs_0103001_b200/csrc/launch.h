@@ -76,7 +76,11 @@ cudaError_t launch_tree_combine(int prec, const void* e, const void* o, void* y,
 // One-pass cluster FFT (fft_cluster.cuh): n = n1 * n2 in one thread-block
 // cluster per transform.  tw4: W_n^{n1 k2} laid out [k2][n1].
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2);
+// Variants 41 / 42 (fft_abbulk.cuh) need caller-provided scratch of
+// cluster_workspace_bytes (the L2-resident Y ring and the task counters).
+size_t cluster_workspace_bytes(int prec, int64_t n, int variant, int64_t batch);
 cudaError_t launch_cluster(int prec, bool inv, int64_t n, const void* in, void* out, int64_t batch,
-                           double scale, const void* tw4, const void* tw, int variant, cudaStream_t st);
+                           double scale, const void* tw4, const void* tw, int variant, cudaStream_t st,
+                           void* ws = nullptr, size_t ws_bytes = 0);
 
 }  // namespace b200fft

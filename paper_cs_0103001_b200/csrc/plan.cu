@@ -194,6 +194,7 @@ size_t workspace_need(const fft_plan_s* p) {
     if (p->dist()) return 2 * (size_t)p->elems() * p->elem_bytes();  // send + recv slabs
     if (p->rank == 2)  // the transposed grid of the Gaussian pipeline (allocated on first use)
         return (size_t)p->n0 * p->n1 * p->elem_bytes();
+    if (p->rank == 1 && p->tw4) return cluster_workspace_bytes(p->prec, p->n0, p->cvariant, p->batch);
     if (p->rank == 1 && !p->radices.empty()) {
         size_t one = (size_t)p->elems() * p->elem_bytes();
         return p->radices.size() % 2 == 1 ? 2 * one : one;  // odd pass counts may need ws1 (run_1d)
@@ -248,7 +249,10 @@ fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream
     if (p->tw4) {
         // one HBM pass: the cluster kernel reads each transform fully before
         // it writes it, so out == in is safe
-        e = launch_cluster(p->prec, inv, L, in, out, p->batch, scale, p->tw4, p->tw, p->cvariant, st);
+        fft_status s = ensure_workspace(p);  // variants 41 / 42: the Y ring and counters
+        if (s != FFT_OK) return s;
+        e = launch_cluster(p->prec, inv, L, in, out, p->batch, scale, p->tw4, p->tw, p->cvariant, st, p->ws,
+                           p->ws_bytes);
         p->last_launches = 1;
         if (e != cudaSuccess) return cuda_fail(e, "k_cluster launch");
         return FFT_OK;
@@ -973,11 +977,12 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
                 t[2 * (k2 * cn1 + n1) + 1] = std::sin(ang);
             }
         const char* var = getenv("B200FFT_CLUSTER_VARIANT");
-        // default 23: st.async transpose with rank-rotated send order (no
-        // incast), 16-CTA clusters, 48 registers -> 5 CTAs/SM (the fastest
-        // measured, profiles/README.md); 8/9 are timing-only
-        p->cvariant = var ? atoi(var) : 23;
-        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 23;
+        // default 42: the warp-specialised TMA task pipeline (fft_abbulk.cuh:
+        // column / row tasks through an L2-resident ring, 1.32 ms vs 1.43 ms
+        // for the best cluster variant 23, profiles/README.md); 8/9 are
+        // timing-only
+        p->cvariant = var ? atoi(var) : 42;
+        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 42;
         if (var && atoi(var) == 8 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 8;
         if (var && atoi(var) == 9 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 9;
         e = upload(t, ip, &p->tw4);
