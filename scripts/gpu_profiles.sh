@@ -9,6 +9,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${R}_ncu_launches.log 2>&1
 echo launches=$?
 C2_BATCH=4096 python scripts/prof_small.py c2 > gpurun_out/${R}_prof_plain.log 2>&1 && \
-C2_BATCH=4096 ncu --set full --clock-control none --import-source on -k regex:k_cluster -s 1 -c 1 \
+C2_BATCH=4096 ncu --set full --clock-control none --import-source on -k regex:"k_cluster|k_ab" -s 1 -c 1 \
     -o gpurun_out/${R}_c2_full python scripts/prof_small.py c2 > gpurun_out/${R}_ncu_full.log 2>&1
 echo full=$?
