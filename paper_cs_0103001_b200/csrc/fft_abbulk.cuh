@@ -420,20 +420,22 @@ __global__ void __launch_bounds__(256, 2)
 // completion and signals done_a / done_b, so the compute warps only ever wait
 // on the stage's full barrier and on their own named barrier.
 // ---------------------------------------------------------------------------
-struct AbWsCfg {
-    static constexpr int NS = 3;
+template <int NS_ = 3>
+struct AbWsCfgN {
+    static constexpr int NS = NS_;
     static constexpr size_t STAGE = 16 * 256 * 8;
     static constexpr size_t BAR_OFF = NS * STAGE;  // full[NS], comp[NS]
     static constexpr size_t SMEM = BAR_OFF + 16 * NS;
 };
+using AbWsCfg = AbWsCfgN<3>;
 
-template <bool INV>
-__global__ void __launch_bounds__(288, 2)
+template <bool INV, int NSV = 3>
+__global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
     k_ab_ws(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yst,
             const __grid_constant__ CUtensorMap map_yld, const __grid_constant__ CUtensorMap map_out, int64_t batch,
             float scale, const float2* __restrict__ tw4, const float2* __restrict__ tw256, AbBulkCtl ctl,
             const float2* ring, int opts) {
-    using G = AbWsCfg;
+    using G = AbWsCfgN<NSV>;
     constexpr int NS = G::NS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
@@ -575,10 +577,15 @@ __global__ void __launch_bounds__(288, 2)
         float2 v[16];
         if (!isb) {
             const int t = tid % 16, l = tid / 16;  // line = column n1 = 16 part + t
-            float2 w[16];
             const float2* tp = tw4 + (int64_t)l * 256 + part * 16 + t;
+            // the four-step twiddles: prefetched before the stage wait when
+            // registers allow (3 stages, 2 CTAs/SM), else loaded at use
+            constexpr int NPF = NSV >= 3 ? 16 : 1;
+            float2 w[NPF];
+            if constexpr (NPF == 16) {
 #pragma unroll
-            for (int m = 0; m < 16; ++m) w[m] = __ldg(tp + (int64_t)m * 16 * 256);
+                for (int m = 0; m < 16; ++m) w[m] = __ldg(tp + (int64_t)m * 16 * 256);
+            }
             bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));
             float2* line = st + t;
 #pragma unroll
@@ -586,7 +593,10 @@ __global__ void __launch_bounds__(288, 2)
             FA::run(v, line, l, tw256, -256);
             FA::lsync(-256);
 #pragma unroll
-            for (int m = 0; m < 16; ++m) line[(l + 16 * m) * 16] = cmul_dir<INV>(v[FA::pos_out(m)], w[m]);
+            for (int m = 0; m < 16; ++m) {
+                const float2 wm = (NPF == 16) ? w[m % NPF] : __ldg(tp + (int64_t)m * 16 * 256);
+                line[(l + 16 * m) * 16] = cmul_dir<INV>(v[FA::pos_out(m)], wm);
+            }
         } else {
             const int t = tid / 16, l = tid % 16;  // line = row k2 = 16 part + t of Y
             bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));

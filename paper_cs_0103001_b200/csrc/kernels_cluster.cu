@@ -436,13 +436,13 @@ bool encode3(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2
 struct AbGeom {
     int grid = 0, D = 0, ring = 0;
 };
-template <bool INV, bool WS>
+template <bool INV, bool WS, int NSV = 3>
 cudaError_t ab_geom(AbGeom* g) {
     static AbGeom cached;
     if (!cached.grid) {
-        constexpr size_t SMEM = WS ? AbWsCfg::SMEM : AbTmaCfg::SMEM;
+        constexpr size_t SMEM = WS ? AbWsCfgN<NSV>::SMEM : AbTmaCfg::SMEM;
         constexpr int NT = WS ? 288 : 256;
-        auto k = WS ? k_ab_ws<INV> : k_ab_tma<INV>;
+        auto k = WS ? k_ab_ws<INV, NSV> : k_ab_tma<INV>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
         int dev = 0, sms = 0, occ = 0;
         if (e == cudaSuccess) e = cudaGetDevice(&dev);
@@ -453,11 +453,14 @@ cudaError_t ab_geom(AbGeom* g) {
         t.grid = sms * (occ > 0 ? occ : 1);
         // every wait must point at least (tasks in flight per CTA) x grid
         // positions back in the task order: 2 for 41, NS = 3 for 42
-        const int depth = WS ? AbWsCfg::NS : 2;
+        const int depth = WS ? NSV : 2;
         const char* dv = getenv("B200FFT_AB_D");
         t.D = (depth * t.grid + 15) / 16 + (dv ? atoi(dv) : 8);
         const char* rv = getenv("B200FFT_AB_RING");
-        t.ring = t.D + (rv ? atoi(rv) : (depth * t.grid + 31) / 32 + 8);
+        // ring = D + 24 slots: an A store waits on the B parts 24 transforms
+        // (768 task positions) back, always an earlier task; 24 measured best
+        // for variant 44 (B200FFT_AB_RING sweeps it)
+        t.ring = t.D + (rv ? atoi(rv) : 24);
         if (getenv("B200FFT_VERBOSE"))
             fprintf(stderr, "ab_tma(ws=%d): grid %d (occ %d), D %d, ring %d\n", (int)WS, t.grid, occ, t.D, t.ring);
         cached = t;
@@ -471,14 +474,14 @@ size_t ab_ws_bytes(int64_t ring, int64_t batch) {
     return (size_t)ring * 65536 * sizeof(float2) + (size_t)2 * batch * sizeof(int);
 }
 
-template <bool INV, bool WS = false>
+template <bool INV, bool WS = false, int NSV = 3>
 cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
                      void* ws, size_t ws_bytes, cudaStream_t st) {
-    constexpr size_t SMEM = WS ? AbWsCfg::SMEM : AbTmaCfg::SMEM;
+    constexpr size_t SMEM = WS ? AbWsCfgN<NSV>::SMEM : AbTmaCfg::SMEM;
     constexpr int NT = WS ? 288 : 256;
-    auto k = WS ? k_ab_ws<INV> : k_ab_tma<INV>;
+    auto k = WS ? k_ab_ws<INV, NSV> : k_ab_tma<INV>;
     AbGeom g;
-    cudaError_t e = ab_geom<INV, WS>(&g);
+    cudaError_t e = ab_geom<INV, WS, NSV>(&g);
     if (e != cudaSuccess) return e;
     if (batch <= 0) return cudaSuccess;
     if (!ws || ws_bytes < ab_ws_bytes(g.ring, batch)) return cudaErrorInvalidValue;
@@ -564,6 +567,8 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 40: return ab_bulk_t<INV>(in, out, batch, scale, tw4, tw, st);
         case 41: return ab_tma_t<INV>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 42: return ab_tma_t<INV, true>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
+        case 43: return ab_tma_t<INV, true, 6>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
+        case 44: return ab_tma_t<INV, true, 2>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 29: return ab_pipe_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
         case 30: return ab_pipe_t<float, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 22: return step_ab2_t<float, INV>(in, out, batch, scale, tw4, tw, st);
@@ -576,9 +581,12 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
 }
 
 size_t cluster_workspace_bytes(int prec, int64_t n, int variant, int64_t batch) {
-    if (prec != 0 || n != 65536 || (variant != 41 && variant != 42)) return 0;
+    if (prec != 0 || n != 65536 || variant < 41 || variant > 44) return 0;
     AbGeom g;
-    cudaError_t e = variant == 42 ? ab_geom<false, true>(&g) : ab_geom<false, false>(&g);
+    cudaError_t e = variant == 42   ? ab_geom<false, true>(&g)
+                    : variant == 43 ? ab_geom<false, true, 6>(&g)
+                    : variant == 44 ? ab_geom<false, true, 2>(&g)
+                                    : ab_geom<false, false>(&g);
     if (e != cudaSuccess) return 0;
     return ab_ws_bytes(g.ring, batch);
 }

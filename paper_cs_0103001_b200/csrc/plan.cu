@@ -977,12 +977,12 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
                 t[2 * (k2 * cn1 + n1) + 1] = std::sin(ang);
             }
         const char* var = getenv("B200FFT_CLUSTER_VARIANT");
-        // default 42: the warp-specialised TMA task pipeline (fft_abbulk.cuh:
-        // column / row tasks through an L2-resident ring, 1.32 ms vs 1.43 ms
-        // for the best cluster variant 23, profiles/README.md); 8/9 are
-        // timing-only
-        p->cvariant = var ? atoi(var) : 42;
-        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 42;
+        // default 44: the warp-specialised TMA task pipeline (fft_abbulk.cuh:
+        // column / row tasks through an L2-resident ring, 3 CTAs/SM x 2
+        // in-place stages, 1.19 ms vs 1.43 ms for the best cluster variant
+        // 23, profiles/README.md); 8/9 are timing-only
+        p->cvariant = var ? atoi(var) : 44;
+        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 44;
         if (var && atoi(var) == 8 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 8;
         if (var && atoi(var) == 9 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 9;
         e = upload(t, ip, &p->tw4);
