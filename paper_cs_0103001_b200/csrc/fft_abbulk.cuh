@@ -248,6 +248,11 @@ __device__ __forceinline__ void store3(const CUtensorMap* map, int c0, int c1, i
         : "memory");
     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
+__device__ __forceinline__ void prefetch3(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(map), "r"(c0), "r"(c1),
+                 "r"(c2)
+                 : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
@@ -537,6 +542,11 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
                     }
                     pend_a = isb ? -1 : b;
                     asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // stage reusable
+                } else if (!isb && (opts & 8)) {
+                    // stage reusable once read; the completion wait and the
+                    // signal follow right after the next load is issued
+                    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                    pend_a = b;
                 } else if (!isb) {
                     bk_store_wait_all();  // Y rows written: signal now (B tasks of other CTAs wait on it)
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -547,9 +557,23 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
             }
             __syncwarp(pmask);
         };
+        const int pf = (opts >> 4) & 7;  // L2 prefetch distance (tasks) for A tiles, 0 = off
         for (int64_t k = 0; k < my_tasks; ++k) {
             if (k >= NS) store(k - NS);
             load(k);
+            if (pf && l0 && k + pf < my_tasks) {  // warm L2 with a later A task's HBM tile
+                bool pb;
+                int64_t pbb;
+                int ppart;
+                decode(blockIdx.x + (k + pf) * gridDim.x, pb, pbb, ppart);
+                if (!pb) tmaops::prefetch3(&map_x, ppart * 16, 0, (int)pbb);
+            }
+            if ((opts & 8) && l0 && pend_a >= 0) {
+                bk_store_wait_all();
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                bk_red_release(ctl.done_a + pend_a, 1);
+                pend_a = -1;
+            }
             __syncwarp(pmask);
         }
         for (int64_t k = (my_tasks > NS ? my_tasks - NS : 0); k < my_tasks; ++k) store(k);
@@ -600,6 +624,10 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
         } else {
             const int t = tid / 16, l = tid % 16;  // line = row k2 = 16 part + t of Y
             bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));
+            if (opts & 4) {  // the Y rows are in smem now: drop their 256 L2 lines (one per thread)
+                const float2* y = ring + (b % ctl.ring) * 65536 + (int64_t)part * 16 * 256 + tid * 16;
+                asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(y) : "memory");
+            }
             float2* line = st + t * 256;
 #pragma unroll
             for (int m = 0; m < 16; ++m) v[FB::pos_in(m)] = line[l + 16 * m];  // as landed (unswizzled)

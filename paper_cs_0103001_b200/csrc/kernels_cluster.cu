@@ -503,7 +503,10 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
     const float2* a_ring = reinterpret_cast<const float2*>(ring);
     static const int opts = [] {
         const char* v = getenv("B200FFT_AB_OPTS");
-        return v ? atoi(v) : 1;  // 1: discard consumed Y rows from L2 (measured best)
+        // bits: 1 / 4 discard consumed Y rows from L2 (producer / compute
+        // warps: fewer DRAM writes, not faster), 2 / 8 signal orders, 16 x d:
+        // L2 tensor prefetch of the A tile d tasks ahead (d = 1 measured best)
+        return v ? atoi(v) : 16;
     }();
     int a_opts = opts;
     void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
