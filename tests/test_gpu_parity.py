@@ -359,3 +359,50 @@ def test_c5_config_single_gpu_sampled(fft):
     torch.cuda.synchronize()
     err = torch.linalg.vector_norm(zd - xd) / torch.linalg.vector_norm(xd)
     assert float(err) <= 1e-5
+
+
+@pytest.mark.parametrize("batch", [1, 2, 5, 37, 300])
+@pytest.mark.parametrize("variant", ["44", "23"])
+def test_c2_kernel_batches_and_inplace(fft, batch, variant, monkeypatch):
+    """The 65536-point one-HBM-pass kernels (default task pipeline 44 and
+    cluster variant 23) at batch sizes that leave the persistent grid partly
+    idle or the task order without its steady A/B phase (batch < D), forward
+    and inverse, out-of-place and in place, against the oracle."""
+    import paper_cs_0103001_b200 as b
+
+    monkeypatch.setenv("B200FFT_CLUSTER_VARIANT", variant)
+    n = 65536
+    x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=900 + batch).reshape(batch, n)
+    p = b.Plan((n,), batch=batch)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    p.forward(xd, yd)
+    zd = yd.clone()
+    p.inverse(zd, zd)  # in place
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy()
+    assert oracle.rel_l2(y, oracle.fft_batch(x)) <= 1e-5
+    assert oracle.rel_l2(zd.cpu().numpy(), oracle.fft_batch(y, inverse=True)) <= 1e-5
+    p.destroy()
+
+
+def test_c2_two_plans_two_streams(fft):
+    """Two plans (each with its own Y-ring workspace) running concurrently on
+    two streams, forward on one and inverse on the other."""
+    import paper_cs_0103001_b200 as b
+
+    n, batch = 65536, 64
+    x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=950).reshape(batch, n)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    p1, p2 = b.Plan((n,), batch=batch, stream=s1), b.Plan((n,), batch=batch, stream=s2)
+    xd = torch.from_numpy(x).cuda()
+    torch.cuda.synchronize()
+    y1, y2 = torch.empty_like(xd), torch.empty_like(xd)
+    for _ in range(3):
+        p1.forward(xd, y1)
+        p2.inverse(xd, y2)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(y1.cpu().numpy(), oracle.fft_batch(x)) <= 1e-5
+    assert oracle.rel_l2(y2.cpu().numpy(), oracle.fft_batch(x, inverse=True)) <= 1e-5
+    p1.destroy()
+    p2.destroy()
