@@ -51,10 +51,12 @@ cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double s
 
 // persistent TMA-fed variant (fft_tma.cuh): 3 stages of ~64 KiB, 512 threads
 template <typename T, int R, bool INV, bool REAL_IN, bool FILT, bool TRANS = false, bool PAIR = false, int E = 16,
-          int OCC = 1>
+          int OCC = 1, int STAGE_KB = 64>
 cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw, const void* rowfilt,
                        cudaStream_t st) {
-    constexpr int W = (int)((64 * 1024) / (R * sizeof(cpx<T>))) < 1 ? 1 : (int)((64 * 1024) / (R * sizeof(cpx<T>)));
+    constexpr int W = (int)((STAGE_KB * 1024) / (R * sizeof(cpx<T>))) < 1
+                          ? 1
+                          : (int)((STAGE_KB * 1024) / (R * sizeof(cpx<T>)));
     constexpr int STAGES = OCC > 1 ? 1 : 3;  // OCC CTAs per SM (registers capped) with one stage each
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
     auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS, PAIR, OCC>;
@@ -137,6 +139,12 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
             if (rows_e() == 2)
                 return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 2>(in, out, batch, scale, tw,
                                                                                      rowfilt, st);
+            if (rows_e() == 32)  // 32 KiB stages (2 rows): two CTAs per SM
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 32>(in, out, batch, scale,
+                                                                                         tw, rowfilt, st);
+            if (rows_e() == 16)  // 16 KiB stages (1 row): four CTAs per SM by shared memory
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 16>(in, out, batch, scale,
+                                                                                         tw, rowfilt, st);
             return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
         default: return cudaErrorInvalidValue;
     }
