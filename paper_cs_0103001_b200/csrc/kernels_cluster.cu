@@ -506,7 +506,9 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
         // bits: 1 / 4 discard consumed Y rows from L2 (producer / compute
         // warps: fewer DRAM writes, not faster), 2 / 8 signal orders, 16 x d:
         // L2 tensor prefetch of the A tile d tasks ahead (d = 1 measured best)
-        return v ? atoi(v) : 16;
+        // 128: the A twiddles W_N^{n1 k2} by a 15-step product from two table
+        // entries instead of 16 loads (-4.5%)
+        return v ? atoi(v) : 144;
     }();
     int a_opts = opts;
     void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
