@@ -588,8 +588,11 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
     }
 
     // ---- compute warps (256 threads) ----
-    using FA = LineFFT<float, 256, 16, INV, 2>;
-    using FB = LineFFT<float, 256, 16, INV, 1>;
+#ifndef B200FFT_AB_TWREC
+#define B200FFT_AB_TWREC 1
+#endif
+    using FA = LineFFT<float, 256, 16, INV, 2, false, (B200FFT_AB_TWREC != 0)>;
+    using FB = LineFFT<float, 256, 16, INV, 1, false, (B200FFT_AB_TWREC != 0)>;
     for (int64_t k = 0; k < my_tasks; ++k) {
         const int64_t i = blockIdx.x + k * gridDim.x;
         bool isb;

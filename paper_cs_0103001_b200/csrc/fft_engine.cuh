@@ -36,7 +36,10 @@ __device__ __forceinline__ int swz16(int i) { return i ^ ((i >> 4) & 15); }
 
 // PF: prefetch each step's twiddles into registers before its exchange
 // barriers (for kernels with a 128-register budget)
-template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false>
+// TWREC: a step's twiddles W^{k r}, r = 1..rho-1, as powers of the one
+// table entry W^{k} (rho - 2 complex products, ~rho ulp in fp32) instead of
+// rho - 1 loads -- for kernels whose warps are short of load bandwidth
+template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false, bool TWREC = false>
 struct LineFFT {
     using C = cpx<T>;
     static constexpr int ML = ml_of(E);  // largest radix 2^ML (16, or 8 when E = 8)
@@ -64,10 +67,20 @@ struct LineFFT {
                 const int j = lt + b * TPL;
                 const int k = j & (Ns - 1);
                 const C* __restrict__ ts = tw + tw_off(R, s, ML) + k;
+                if constexpr (TWREC) {
+                    const C w1 = __ldg(ts);
+                    C w = w1;
 #pragma unroll
-                for (int r = 1; r < rho; ++r) {
-                    const C w = __ldg(ts + (r - 1) * Ns);
-                    v[b * rho + r] = cmul_dir<INV>(v[b * rho + r], w);
+                    for (int r = 1; r < rho; ++r) {
+                        v[b * rho + r] = cmul_dir<INV>(v[b * rho + r], w);
+                        if (r + 1 < rho) w = cmul(w, w1);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 1; r < rho; ++r) {
+                        const C w = __ldg(ts + (r - 1) * Ns);
+                        v[b * rho + r] = cmul_dir<INV>(v[b * rho + r], w);
+                    }
                 }
             }
             dft<rho, INV>(v + b * rho);
