@@ -121,6 +121,13 @@ fft_status fft_plan_set_stream(fft_plan plan, void* cuda_stream);
 size_t fft_plan_workspace_bytes(fft_plan plan);
 fft_status fft_plan_set_workspace(fft_plan plan, void* dev_ptr, size_t bytes);
 
+/* Note (complex64, n = 65536): the one-HBM-pass kernel keeps an
+ * intermediate ring (~44 MiB, in the plan's workspace) in L2 through an
+ * access-policy window and, on first use, sets the device's persisting-L2
+ * set-aside (cudaLimitPersistingL2CacheSize) to the ring's size; other
+ * kernels may still use that L2 portion while it holds no persisting lines.
+ * Set B200FFT_AB_PERSIST=0 to leave the device limit alone. */
+
 /* Forward (1/N, or eq5's 1/N for rank 2) and inverse (unscaled, or the
  * 2D-IDFT's 1/M) transforms.  in/out: device pointers to the local data
  * (batch * prod(dims) elements); out may equal in. */

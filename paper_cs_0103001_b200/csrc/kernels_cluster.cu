@@ -514,7 +514,7 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
     void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
     const int64_t tasks = 32 * batch;
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.gridDim = dim3((unsigned)(tasks < g.grid ? tasks : g.grid), 1, 1);
@@ -523,6 +523,33 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // An L2 access-policy window marks the Y ring persisting for this launch
+    // (with a device persisting-L2 set-aside of the ring's size, set once):
+    // the ring then never spills to HBM (ncu: DRAM bytes = algorithmic,
+    // 1.10 -> 1.07 ms).  B200FFT_AB_PERSIST=0 turns it off.
+    static const bool persist = [] {
+        const char* v = getenv("B200FFT_AB_PERSIST");
+        return !(v && v[0] == '0');
+    }();
+    if (persist) {
+        static bool limit_set = false;
+        const size_t rb = (size_t)g.ring * 65536 * sizeof(float2);
+        if (!limit_set) {
+            int dev = 0, mx = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, rb < (size_t)mx ? rb : (size_t)mx);
+            if (getenv("B200FFT_VERBOSE")) fprintf(stderr, "persisting L2 max %d, ring %zu\n", mx, rb);
+            limit_set = true;
+        }
+        attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[1].val.accessPolicyWindow.base_ptr = ring;
+        attr[1].val.accessPolicyWindow.num_bytes = rb;
+        attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.numAttrs = 2;
+    }
     return cudaLaunchKernelExC(&cfg, (const void*)k, args);
 }
 
