@@ -245,12 +245,12 @@ __device__ __forceinline__ int64_t row_index(int64_t row, int64_t v, int64_t R, 
 
 // FILT: a row filter pass of the separable pipeline: forward
 // transform -> * rowfilt[v] * scale -> inverse transform, stored unscaled.
-template <typename T, int R, int E, bool FILT, int LAYOUT = 0, bool PF = false>
+template <typename T, int R, int E, bool FILT, int LAYOUT = 0, bool PF = false, bool TWREC = false>
 __device__ __forceinline__ void row_filter_pass(cpx<T>* v, cpx<T>* line, int lt, const cpx<T>* __restrict__ tw,
                                                 const T* __restrict__ rowfilt, T& scale, int bar = 0) {
     if constexpr (FILT) {
-        using F = LineFFT<T, R, E, false, LAYOUT, PF>;
-        using FI = LineFFT<T, R, E, true, LAYOUT, PF>;
+        using F = LineFFT<T, R, E, false, LAYOUT, PF, TWREC>;
+        using FI = LineFFT<T, R, E, true, LAYOUT, PF, TWREC>;
         cpx<T> w[E];
 #pragma unroll
         for (int m = 0; m < E; ++m)

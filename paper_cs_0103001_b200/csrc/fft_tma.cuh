@@ -69,7 +69,13 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
     k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
                const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt) {
     using C = cpx<T>;
-    using F = LineFFT<T, R, E, INV, 0, true>;
+#ifndef B200FFT_ROWS_TWREC
+#define B200FFT_ROWS_TWREC 1
+#endif
+    // step twiddles: prefetched table entries (default) or, with
+    // B200FFT_ROWS_TWREC, powers of one entry (LineFFT TWREC)
+    constexpr bool TWR = B200FFT_ROWS_TWREC != 0;
+    using F = LineFFT<T, R, E, INV, 0, !TWR, TWR>;
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
     static_assert(R >= 256 && (R * sizeof(cpx<T>)) % 16 == 0, "bulk copies need >= 16 B rows");
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
         const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
         F::run(v, line, lt, tw, bar);
         T sc = scale;
-        row_filter_pass<T, R, E, FILT, 0, true>(v, line, lt, tw, rowfilt, sc, bar);
+        row_filter_pass<T, R, E, FILT, 0, !TWR, TWR>(v, line, lt, tw, rowfilt, sc, bar);
         const int64_t row = tile * W + t;
         if constexpr (TRANS) {
             F::lsync(bar);

@@ -89,6 +89,16 @@ int rows_e() {
     return v;
 }
 
+// B200FFT_ROWS_STAGE_KB=16|32: smaller stages for the 2048-point transposed
+// filter rows (measured slower; 64 KiB default)
+int rows_stage_kb() {
+    static const int v = [] {
+        const char* e = getenv("B200FFT_ROWS_STAGE_KB");
+        return e ? atoi(e) : 64;
+    }();
+    return v;
+}
+
 template <bool INV, bool REAL_IN, bool FILT>
 cudaError_t rows_tma_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw,
                        const void* rowfilt, cudaStream_t st) {
@@ -139,10 +149,10 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
             if (rows_e() == 2)
                 return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 2>(in, out, batch, scale, tw,
                                                                                      rowfilt, st);
-            if (rows_e() == 32)  // 32 KiB stages (2 rows): two CTAs per SM
+            if (rows_stage_kb() == 32)  // 32 KiB stages (2 rows): two CTAs per SM
                 return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 32>(in, out, batch, scale,
                                                                                          tw, rowfilt, st);
-            if (rows_e() == 16)  // 16 KiB stages (1 row): four CTAs per SM by shared memory
+            if (rows_stage_kb() == 16)  // 16 KiB stages (1 row): four CTAs per SM by shared memory
                 return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 16>(in, out, batch, scale,
                                                                                          tw, rowfilt, st);
             return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
