@@ -465,7 +465,11 @@ __global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ i
                                                     const cpx<T>* __restrict__ pa,
                                                     const cpx<T>* __restrict__ pb, int klo_sh) {
     using C = cpx<T>;
-    using F = LineFFT<T, R, E, INV>;
+    // complex64: step twiddles as powers of one table entry (TWREC) and the
+    // pass twiddles W^{k (r0 + it RS)} = W^{k r0} (W^{k RS})^it from two table
+    // products per thread -- fewer loads per element (fp32, ~R / RS ulp)
+    constexpr bool REC = sizeof(T) == 4;
+    using F = LineFFT<T, R, E, INV, 0, false, REC>;
     constexpr int NT = W * F::TPL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* smem = reinterpret_cast<C*>(smem_raw);
@@ -499,14 +503,27 @@ __global__ void __launch_bounds__(W*(R / E)) k_pass(const cpx<T>* __restrict__ i
         const C* wb = pb + (int64_t)r0 * nhi + (kt >> klo_sh);
         C* d = smem + tt * F::LS;
         const int pr0 = pad16(r0);
+        C w = mk((T)1, (T)0), wstep = w;
+        if (REC && Ns > 1) {  // W^{k r0} and W^{k RS}
+            w = __ldg(wa);
+            if (nhi > 1) w = cmul(w, __ldg(wb));
+            const int64_t drs = (int64_t)RS;
+            wstep = __ldg(pa + drs * KLO + (kt & (KLO - 1)));
+            if (nhi > 1) wstep = cmul(wstep, __ldg(pb + drs * nhi + (kt >> klo_sh)));
+        }
         // fully unrolled so that all of a thread's loads are in flight at once
 #pragma unroll
         for (int it = 0; it < (W * R) / NT; ++it) {
             C a = s[it * sstep];
             if (Ns > 1) {
-                C w = __ldg(wa + (int64_t)it * RS * KLO);
-                if (nhi > 1) w = cmul(w, __ldg(wb + (int64_t)it * RS * nhi));
-                a = cmul_dir<INV>(a, w);
+                if constexpr (REC) {
+                    a = cmul_dir<INV>(a, w);
+                    w = cmul(w, wstep);
+                } else {
+                    C wl = __ldg(wa + (int64_t)it * RS * KLO);
+                    if (nhi > 1) wl = cmul(wl, __ldg(wb + (int64_t)it * RS * nhi));
+                    a = cmul_dir<INV>(a, wl);
+                }
             }
             d[(RS % 16 == 0) ? pr0 + it * (RS + RS / 16) : pad16(r0 + it * RS)] = a;
         }

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(W*(R / E), 1)
                 T scale, const cpx<T>* __restrict__ tw, const cpx<T>* __restrict__ pa,
                 const cpx<T>* __restrict__ pb, int klo_sh) {
     using C = cpx<T>;
-    using F = LineFFT<T, R, E, INV>;
+    using F = LineFFT<T, R, E, INV, 0, false, sizeof(T) == 4>;  // step twiddles by recurrence (c64)
     using G = PassPipeCfg<T, R, W>;
     constexpr int NT = W * F::TPL;
     constexpr int RS = NT / W;  // = TPL
@@ -84,11 +84,15 @@ __global__ void __launch_bounds__(W*(R / E), 1)
             const C* wa = pa + (int64_t)r0 * KLO + (kt & (KLO - 1));
             const C* wb = pb + (int64_t)r0 * nhi + (kt >> klo_sh);
             C* d = sm + tt * G::LS;
+            // W^{k (r0 + it RS)} = W^{k r0} (W^{k RS})^it: two table products
+            C w = __ldg(wa);
+            if (nhi > 1) w = cmul(w, __ldg(wb));
+            C ws = __ldg(pa + (int64_t)RS * KLO + (kt & (KLO - 1)));
+            if (nhi > 1) ws = cmul(ws, __ldg(pb + (int64_t)RS * nhi + (kt >> klo_sh)));
 #pragma unroll
             for (int it = 0; it < R / RS; ++it) {
-                C w = __ldg(wa + (int64_t)it * RS * KLO);
-                if (nhi > 1) w = cmul(w, __ldg(wb + (int64_t)it * RS * nhi));
                 d[slot(it)] = cmul_dir<INV>(d[slot(it)], w);
+                w = cmul(w, ws);
             }
         }
         __syncthreads();
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(W*(R / E), 1)
                T scale, const cpx<T>* __restrict__ tw, const cpx<T>* __restrict__ pa, const cpx<T>* __restrict__ pb,
                int klo_sh) {
     using C = cpx<T>;
-    using F = LineFFT<T, R, E, INV>;
+    using F = LineFFT<T, R, E, INV, 0, false, sizeof(T) == 4>;  // step twiddles by recurrence (c64)
     using G = PassTmaCfg<T, R, W>;
     constexpr int NT = W * F::TPL;
     static_assert((W * sizeof(C)) % 16 == 0, "bulk copies move multiples of 16 B");

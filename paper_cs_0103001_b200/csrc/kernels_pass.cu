@@ -102,7 +102,7 @@ cudaError_t pass_r(int64_t R, const void* in, void* out, int64_t L, int64_t Ns, 
                    cudaStream_t st) {
     static const int pipe = [] {
         const char* v = getenv("B200FFT_PASS_PIPE");
-        return v ? atoi(v) : 0;  // 0: k_pass (measured faster, profiles/README.md)
+        return v ? atoi(v) : 4;  // 4: k_pass everywhere (with twiddle recurrences it streams at 5-6 TB/s)
     }();
     if constexpr (sizeof(T) == 4) {
         if (pipe == 5) {  // TMA-bulk-fed tiles

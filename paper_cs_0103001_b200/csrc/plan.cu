@@ -229,10 +229,13 @@ bool aligned(const void* ptr, size_t a) { return ((uintptr_t)ptr % a) == 0; }
 // profiles/README.md) -- one pass more, each ~2x faster.
 std::vector<int64_t> split_radices(int64_t L, int prec) {
     int m = ilog2(L);
-    int rmax = 10;
+    // complex64 from 2^21 on: radix <= 512, so every pass tile is 16 lines
+    // wide (128-B runs: radix-1024 passes have 8-line tiles, 64-B runs, which
+    // DRAM serves at half rate at multi-MiB strides) -- 2^30 in 4 passes at
+    // ~5.9 TB/s each (11.6 ms) instead of 3 at 3.45 TB/s (14.9 ms)
+    int rmax = (prec == 0 && m >= 21) ? 9 : 10;
     const char* rv = getenv("B200FFT_PASS_RMAX");
     if (rv) rmax = atoi(rv);
-    (void)prec;  // rmax = 8 for m >= 29 measured slower (4 passes at 2.8 TB/s, profiles/README.md)
     int P = (m + rmax - 1) / rmax;
     std::vector<int64_t> r;
     for (int i = 0; i < P; ++i) {
