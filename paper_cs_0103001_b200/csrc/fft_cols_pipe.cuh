@@ -45,8 +45,11 @@ __global__ void __launch_bounds__(W*(R / E), 1)
                 const cpx<T>* __restrict__ tw, FilterArgs filt) {
     using C = cpx<T>;
     constexpr bool INV0 = (MODE == 1 || MODE == 4);
-    using F = LineFFT<T, R, E, INV0, 0, true>;
-    using FI = LineFFT<T, R, E, true, 0, true>;
+    // step twiddles: powers of one table entry for complex64 (TWREC), else
+    // prefetched table entries
+    constexpr bool TWR = sizeof(T) == 4;
+    using F = LineFFT<T, R, E, INV0, 0, !TWR, TWR>;
+    using FI = LineFFT<T, R, E, true, 0, !TWR, TWR>;
     using G = ColsPipeCfg<T, R, W, NS>;
     constexpr int NT = W * F::TPL;
     constexpr int LSC = G::LSC;
@@ -97,21 +100,29 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         C v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
-        if constexpr (MODE == 4) {
+        if constexpr (MODE == 4) {  // conj(W^{n2 (lt + TPL m)}) = conj(W^{n2 lt} (W^{n2 TPL})^m)
             const int64_t n2 = (s0 + t) / filt.tdiv;
+            const C* tl = reinterpret_cast<const C*>(filt.tw_l);
+            C wm = __ldg(tl + n2 * lt);
+            const C ws = __ldg(tl + n2 * F::TPL);
 #pragma unroll
-            for (int m = 0; m < E; ++m)
-                v[F::pos_in(m)] = cmulc(v[F::pos_in(m)],
-                                        __ldg(reinterpret_cast<const C*>(filt.tw_l) + n2 * (lt + F::TPL * m)));
+            for (int m = 0; m < E; ++m) {
+                v[F::pos_in(m)] = cmulc(v[F::pos_in(m)], wm);
+                wm = cmul(wm, ws);
+            }
         }
         const int bar = (!LF && F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
         F::run(v, line, lt, tw, bar);
-        if constexpr (MODE == 3) {
+        if constexpr (MODE == 3) {  // W^{n2 (lt + TPL m)} = W^{n2 lt} (W^{n2 TPL})^m
             const int64_t n2 = (s0 + t) / filt.tdiv;
+            const C* tl = reinterpret_cast<const C*>(filt.tw_l);
+            C wm = __ldg(tl + n2 * lt);
+            const C ws = __ldg(tl + n2 * F::TPL);
 #pragma unroll
-            for (int m = 0; m < E; ++m)
-                v[F::pos_out(m)] = cmul(v[F::pos_out(m)],
-                                        __ldg(reinterpret_cast<const C*>(filt.tw_l) + n2 * (lt + F::TPL * m)));
+            for (int m = 0; m < E; ++m) {
+                v[F::pos_out(m)] = cmul(v[F::pos_out(m)], wm);
+                wm = cmul(wm, ws);
+            }
         }
         if constexpr (MODE == 2) {
             C w[E];
