@@ -39,7 +39,7 @@ __device__ __forceinline__ int swz16(int i) { return i ^ ((i >> 4) & 15); }
 // TWREC: a step's twiddles W^{k r}, r = 1..rho-1, as powers of the one
 // table entry W^{k} (rho - 2 complex products, ~rho ulp in fp32) instead of
 // rho - 1 loads -- for kernels whose warps are short of load bandwidth
-template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false, bool TWREC = false>
+template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false, bool TWREC = (sizeof(T) == 4)>
 struct LineFFT {
     using C = cpx<T>;
     static constexpr int ML = ml_of(E);  // largest radix 2^ML (16, or 8 when E = 8)
@@ -96,7 +96,7 @@ struct LineFFT {
     }
     template <int s>
     static constexpr bool prefetch_tw() {
-        return PF && ntw<s>() > 0 && ntw<s>() <= 16;
+        return PF && !TWREC && ntw<s>() > 0 && ntw<s>() <= 16;
     }
     template <int s>
     __device__ __forceinline__ static void load_tw(C* w, int lt, const C* __restrict__ tw) {
