@@ -381,7 +381,8 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
                                                     int64_t S, T scale, const cpx<T>* __restrict__ tw,
                                                     FilterArgs filt) {
     using C = cpx<T>;
-    constexpr bool INV0 = (MODE == 1);
+    // MODE 3 / 4 / kind 6: the four-step column passes (see k_cols_pipe)
+    constexpr bool INV0 = (MODE == 1 || MODE == 4);
     using F = LineFFT<T, R, E, INV0>;
     using FI = LineFFT<T, R, E, true>;
     constexpr int NT = W * F::TPL;
@@ -413,9 +414,31 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
     C v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[F::bpos(lt, m)];
+    if constexpr (MODE == 4) {  // conj(W^{n2 (lt + TPL m)}) by recurrence
+        const int64_t n2 = (s0 + t) / filt.tdiv;
+        const C* tl = reinterpret_cast<const C*>(filt.tw_l);
+        C wm = __ldg(tl + n2 * lt);
+        const C ws = __ldg(tl + n2 * F::TPL);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            v[F::pos_in(m)] = cmulc(v[F::pos_in(m)], wm);
+            wm = cmul(wm, ws);
+        }
+    }
     // lines synchronise on their own named barrier (1 + t) between steps
     const int bar = (!LF && F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
     F::run(v, line, lt, tw, bar);
+    if constexpr (MODE == 3) {  // W^{n2 (lt + TPL m)} by recurrence
+        const int64_t n2 = (s0 + t) / filt.tdiv;
+        const C* tl = reinterpret_cast<const C*>(filt.tw_l);
+        C wm = __ldg(tl + n2 * lt);
+        const C ws = __ldg(tl + n2 * F::TPL);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            v[F::pos_out(m)] = cmul(v[F::pos_out(m)], wm);
+            wm = cmul(wm, ws);
+        }
+    }
     if constexpr (MODE == 2) {
         C w[E];
         const int64_t col = s0 + t;
@@ -427,7 +450,9 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int64_t u = lt + F::TPL * m;
-            const T h = (col < S) ? filter_value<T>(filt, u, col + filt.col_off) * scale : (T)0;
+            const T hv = (filt.kind == 6) ? __ldg(reinterpret_cast<const T*>(filt.gu) + img + filt.n1 * u)
+                                          : filter_value<T>(filt, u, col + filt.col_off);
+            const T h = (col < S) ? hv * scale : (T)0;
             w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], h);
         }
         FI::run(w, line, lt, tw, bar);

@@ -141,9 +141,18 @@ cudaError_t cols4_r(int64_t R, const void* in, void* out, int64_t S, int64_t nim
                     const FilterArgs& f, cudaStream_t st) {
     static const int cfg = [] {
         const char* v = getenv("B200FFT_COLS4_CFG");
-        return v ? atoi(v) : 1;
+        return v ? atoi(v) : 5;  // 5: k_cols, E = 16, 16-column tiles (measured best)
     }();
-    if (cfg == 1) {
+    if (cfg == 0) {  // per-CTA tiles (k_cols): many CTAs per SM, twiddles by recurrence
+        if (R == 64) return cols_t<float, 64, MODE>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128) return cols_t<float, 128, MODE>(in, out, S, nimg, scale, tw, f, st);
+    } else if (cfg == 5) {  // E = 16 (8 threads per 128-point line)
+        if (R == 64) return cols_t<float, 64, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128) return cols_t<float, 128, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
+    } else if (cfg == 6) {  // E = 16, 32 columns per tile
+        if (R == 64) return cols_t<float, 64, MODE, 32, 16>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128) return cols_t<float, 128, MODE, 32, 16>(in, out, S, nimg, scale, tw, f, st);
+    } else if (cfg == 1) {
         if (R == 64) return cols_pipe_t<64, MODE, 32, 4>(in, out, S, nimg, scale, tw, f, st);
         if (R == 128) return cols_pipe_t<128, MODE, 16, 4>(in, out, S, nimg, scale, tw, f, st);
     } else if (cfg == 2) {

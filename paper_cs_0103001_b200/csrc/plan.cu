@@ -415,7 +415,7 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
     // inv over each block of N2 consecutive rows; A' = conj twiddle + inverse
     // over the 64 rows.  No transposes, no 8192-long column lines.
     const char* c4_env = getenv("B200FFT_PIPE_COLS4");
-    const bool c4_default = false;
+    const bool c4_default = true;  // 1060 us vs 1130 us for the transposes path (C4, profiles/README.md)
     if (filter == FFT_FILTER_GAUSS && !literal && p->prec == 0 && N >= 4096 && N <= 8192 && M >= 256 &&
         M <= 8192 && (c4_env ? c4_env[0] == '1' : c4_default)) {
         if (p->twl_n != N) {
