@@ -451,6 +451,8 @@ cudaError_t ab_geom(AbGeom* g) {
         if (e != cudaSuccess) return e;
         AbGeom t;
         t.grid = sms * (occ > 0 ? occ : 1);
+        const char* gv = getenv("B200FFT_AB_GRID");
+        if (gv && atoi(gv) > 0 && atoi(gv) < t.grid) t.grid = atoi(gv);
         // every wait must point at least (tasks in flight per CTA) x grid
         // positions back in the task order: 2 for 41, NS = 3 for 42
         const int depth = WS ? NSV : 2;
