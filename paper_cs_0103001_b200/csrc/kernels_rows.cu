@@ -57,7 +57,9 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     constexpr int W = (int)((STAGE_KB * 1024) / (R * sizeof(cpx<T>))) < 1
                           ? 1
                           : (int)((STAGE_KB * 1024) / (R * sizeof(cpx<T>)));
-    constexpr int STAGES = OCC > 1 ? 1 : 3;  // OCC CTAs per SM (registers capped) with one stage each
+    // OCC CTAs per SM (registers capped): one stage each, or (OCC = 3, the
+    // C2 lesson) two smaller stages each
+    constexpr int STAGES = OCC == 3 ? 2 : (OCC > 1 ? 1 : 3);
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
     auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS, PAIR, OCC>;
     static int grid_max = 0;
@@ -149,6 +151,9 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
             if (rows_e() == 2)
                 return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 2>(in, out, batch, scale, tw,
                                                                                      rowfilt, st);
+            if (rows_stage_kb() == 323)  // 3 CTAs/SM x 2 stages of 32 KiB (2 rows)
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 3, 32>(in, out, batch, scale,
+                                                                                         tw, rowfilt, st);
             if (rows_stage_kb() == 32)  // 32 KiB stages (2 rows): two CTAs per SM
                 return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 32>(in, out, batch, scale,
                                                                                          tw, rowfilt, st);
