@@ -661,4 +661,172 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
     }
 }
 
+// ---------------------------------------------------------------------------
+// Variants 45 / 46: k_ab_ws with 8-line tasks (16 KiB stages, 32 A + 32 B
+// parts per transform).  The same 8 compute warps per CTA run ONE task at a
+// time with E = 8 (steps 8, 8, 4): A with the 8 columns as the thread-fastest
+// index (LineFFT LAYOUT 4, conflict-free in the dense [256][8] box), B with
+// one warp per row (LAYOUT 3, warp-synchronous exchanges).  Half the stage
+// size at the same stage memory per SM means NS - 1 of NS stages can be in
+// flight instead of 1 of 2: 45 = 3 CTAs/SM x 4 stages, 46 = 4 CTAs/SM x 3.
+// ---------------------------------------------------------------------------
+template <int NS_>
+struct AbWs8Cfg {
+    static constexpr int NS = NS_;
+    static constexpr size_t STAGE = 8 * 256 * 8;
+    static constexpr size_t BAR_OFF = NS * STAGE;
+    static constexpr size_t SMEM = BAR_OFF + 16 * NS;
+};
+
+template <bool INV, int NS, int MINB>
+__global__ void __launch_bounds__(288, MINB)
+    k_ab_ws8(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yst,
+             const __grid_constant__ CUtensorMap map_yld, const __grid_constant__ CUtensorMap map_out, int64_t batch,
+             float scale, const float2* __restrict__ tw4, const float2* __restrict__ tw256, AbBulkCtl ctl,
+             const float2* ring, int opts) {
+    using G = AbWs8Cfg<NS>;
+    constexpr int PP = 32;  // parts per phase
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t full0 = s_base + (uint32_t)G::BAR_OFF, comp0 = full0 + 8 * NS;
+    const int tid = threadIdx.x;
+    const int64_t Dp = batch < ctl.D ? batch : ctl.D;
+    const int64_t n1t = PP * Dp, n2t = 2 * PP * (batch - Dp), ntasks = 2 * PP * batch;
+    (void)ring;
+
+    auto decode = [&](int64_t i, bool& isb, int64_t& b, int& part) {
+        if (i < n1t) {
+            isb = false;
+            b = i / PP;
+            part = (int)(i % PP);
+        } else if (i < n1t + n2t) {
+            const int64_t j = i - n1t, r = j % (2 * PP);
+            isb = r >= PP;
+            b = Dp + j / (2 * PP) - (isb ? Dp : 0);
+            part = (int)(r % PP);
+        } else {
+            const int64_t j = i - n1t - n2t;
+            isb = true;
+            b = batch - Dp + j / PP;
+            part = (int)(j % PP);
+        }
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            bk_mbar_init(full0 + 8 * s, 1);
+            bk_mbar_init(comp0 + 8 * s, 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t my_tasks = ntasks > blockIdx.x ? (ntasks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (tid >= 256) {  // ---- producer warp: lane 0 drives the TMA ----
+        if (tid != 256) return;
+        const uint64_t pol_stream = tmaops::policy_evict_first();
+        const uint64_t pol_keep = tmaops::policy_evict_last();
+        auto load = [&](int64_t k) {
+            bool isb;
+            int64_t b;
+            int part;
+            decode(blockIdx.x + k * gridDim.x, isb, b, part);
+            const int s = (int)(k % NS);
+            const uint32_t st = s_base + (uint32_t)(s * G::STAGE), bar = full0 + 8 * s;
+            if (!isb) {
+                bk_arrive_expect(bar, (uint32_t)G::STAGE);
+                tmaops::load3(st, &map_x, part * 8, 0, (int)b, bar, pol_stream);
+            } else {
+                while (bk_ld_acquire(ctl.done_a + b) < PP) __nanosleep(32);
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                bk_arrive_expect(bar, (uint32_t)G::STAGE);
+                tmaops::load3(st, &map_yld, 0, part * 8, (int)(b % ctl.ring), bar, pol_keep);
+            }
+        };
+        auto store = [&](int64_t k) {
+            bool isb;
+            int64_t b;
+            int part;
+            decode(blockIdx.x + k * gridDim.x, isb, b, part);
+            const int s = (int)(k % NS);
+            bk_wait(comp0 + 8 * s, (uint32_t)((k / NS) & 1));
+            const uint32_t st = s_base + (uint32_t)(s * G::STAGE);
+            if (!isb) {
+                if (b >= ctl.ring)
+                    while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < PP) __nanosleep(32);
+                tmaops::store3(&map_yst, part * 8, 0, (int)(b % ctl.ring), st, pol_keep);
+                bk_store_wait_all();  // Y rows written: B tasks of other CTAs wait on the signal
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                bk_red_release(ctl.done_a + b, 1);
+            } else {
+                bk_red_release(ctl.done_b + b, 1);  // its ring rows were read at load
+                tmaops::store3(&map_out, part * 8, 0, (int)b, st, pol_stream);
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // stage reusable
+            }
+        };
+        const int pf = (opts >> 4) & 7;
+        for (int64_t k = 0; k < my_tasks; ++k) {
+            if (k >= NS) store(k - NS);
+            load(k);
+            if (pf && k + pf < my_tasks) {
+                bool pb;
+                int64_t pbb;
+                int ppart;
+                decode(blockIdx.x + (k + pf) * gridDim.x, pb, pbb, ppart);
+                if (!pb) tmaops::prefetch3(&map_x, ppart * 8, 0, (int)pbb);
+            }
+        }
+        for (int64_t k = (my_tasks > NS ? my_tasks - NS : 0); k < my_tasks; ++k) store(k);
+        bk_store_wait_all();
+        return;
+    }
+
+    // ---- compute warps (256 threads, one task at a time) ----
+    using FA = LineFFT<float, 256, 8, INV, 4, false, true>;
+    using FB = LineFFT<float, 256, 8, INV, 3, false, true>;
+    for (int64_t k = 0; k < my_tasks; ++k) {
+        bool isb;
+        int64_t b;
+        int part;
+        decode(blockIdx.x + k * gridDim.x, isb, b, part);
+        const int s = (int)(k % NS);
+        float2* st = reinterpret_cast<float2*>(smem_raw + s * G::STAGE);
+        float2 v[8];
+        if (!isb) {
+            const int t = tid & 7, l = tid >> 3;  // line = column n1 = 8 part + t
+            const int n1 = part * 8 + t;
+            float2 wm = __ldg(tw4 + (int64_t)l * 256 + n1);    // W_N^{n1 l}
+            const float2 ws = __ldg(tw4 + (int64_t)32 * 256 + n1);  // W_N^{32 n1}
+            bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));
+            float2* line = st + t;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) v[FA::pos_in(m)] = line[(l + 32 * m) * 8];  // dense, as landed
+            FA::run(v, line, l, tw256, -256);
+            FA::lsync(-256);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {  // Y[k2 = l + 32 m][n1] * W_N^{n1 k2}, dense for the store
+                line[(l + 32 * m) * 8] = cmul_dir<INV>(v[FA::pos_out(m)], wm);
+                wm = cmul(wm, ws);
+            }
+        } else {
+            const int t = tid >> 5, l = tid & 31;  // line = row k2 = 8 part + t of Y (one warp)
+            bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));
+            float2* line = st + t * 256;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) v[FB::pos_in(m)] = line[l + 32 * m];  // as landed
+            FB::run(v, line, l, tw256, -32);
+            FB::lsync(-256);  // the output box spans every warp's row
+            char* sb = reinterpret_cast<char*>(st);  // X box [k1][8 k2], 64-B TMA swizzle
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int k1 = l + 32 * m;
+                *reinterpret_cast<float2*>(sb + k1 * 64 + (((t >> 1) ^ ((k1 >> 1) & 3)) << 4) + ((t & 1) << 3)) =
+                    cscale(v[FB::pos_out(m)], scale);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        bk_arrive(comp0 + 8 * s);
+    }
+}
+
 }  // namespace b200fft

@@ -34,6 +34,19 @@ __device__ __forceinline__ int swz16(int i) { return i ^ ((i >> 4) & 15); }
 // x * 16 + t: a dense [R][16] TMA box of 16 columns); with the 16 lines as
 // the thread-fastest index every exchange is conflict-free
 
+// LAYOUT 3: one warp per 256-point line, E = 8 (steps 8, 8, 4): XOR the low
+// 4 index bits with g(bits 4..7), g(c) = c ^ (bit 2 of c) << 3 -- every
+// exchange of that schedule hits 16 distinct 8-B bank pairs per half-warp
+__device__ __forceinline__ int swz8(int i) {
+    const int c = (i >> 4) & 15;
+    return i ^ (c ^ (((c >> 2) & 1) << 3));
+}
+// LAYOUT 4: 8 lines interleaved element by element (element x of line t at
+// h(x) * 8 + t, h(x) = x ^ bit 3 of x: a dense [R][8] TMA box of 8 columns
+// after the first read) with the 8 lines as the thread-fastest index: the two
+// element positions of a half-warp always differ in h's parity
+__device__ __forceinline__ int il8(int i) { return (i ^ ((i >> 3) & 1)) * 8; }
+
 // PF: prefetch each step's twiddles into registers before its exchange
 // barriers (for kernels with a 128-register budget)
 // TWREC: a step's twiddles W^{k r}, r = 1..rho-1, as powers of the one
@@ -137,6 +150,12 @@ struct LineFFT {
             } else if constexpr (LAYOUT == 2) {
 #pragma unroll
                 for (int q = 0; q < rho; ++q) line[(base + q * Ns) * 16] = v[b * rho + q];
+            } else if constexpr (LAYOUT == 3) {
+#pragma unroll
+                for (int q = 0; q < rho; ++q) line[swz8(base + q * Ns)] = v[b * rho + q];
+            } else if constexpr (LAYOUT == 4) {
+#pragma unroll
+                for (int q = 0; q < rho; ++q) line[il8(base + q * Ns)] = v[b * rho + q];
             } else if constexpr (Ns % 16 == 0) {
                 const int pb = pad16(base);
 #pragma unroll
@@ -165,6 +184,12 @@ struct LineFFT {
             } else if constexpr (LAYOUT == 2) {
 #pragma unroll
                 for (int r = 0; r < rho; ++r) v[b * rho + r] = line[(j + r * st) * 16];
+            } else if constexpr (LAYOUT == 3) {
+#pragma unroll
+                for (int r = 0; r < rho; ++r) v[b * rho + r] = line[swz8(j + r * st)];
+            } else if constexpr (LAYOUT == 4) {
+#pragma unroll
+                for (int r = 0; r < rho; ++r) v[b * rho + r] = line[il8(j + r * st)];
             } else if constexpr (st % 16 == 0) {
                 const int pj = pad16(j);
 #pragma unroll
@@ -180,6 +205,8 @@ struct LineFFT {
     __device__ __forceinline__ static int bpos(int lt, int m) {
         if constexpr (LAYOUT == 1) return swz16(lt + TPL * m);
         else if constexpr (LAYOUT == 2) return (lt + TPL * m) * 16;
+        else if constexpr (LAYOUT == 3) return swz8(lt + TPL * m);
+        else if constexpr (LAYOUT == 4) return il8(lt + TPL * m);
         else if constexpr (TPL % 16 == 0) return pad16(lt) + m * (TPL + TPL / 16);
         else return pad16(lt + TPL * m);
     }
@@ -188,6 +215,10 @@ struct LineFFT {
     // threads of this line through named barrier `bar` -- lines of one CTA
     // then never wait for each other.  Needs TPL % 32 == 0 (whole warps).
     __device__ __forceinline__ static void lsync(int bar) {
+        if (bar == -32) {  // a line owned by one warp
+            __syncwarp();
+            return;
+        }
         if (bar < 0) {  // the -bar threads of a warp-specialised CTA's compute group (named barrier 1)
             asm volatile("bar.sync 1, %0;\n" ::"r"(-bar) : "memory");
             return;

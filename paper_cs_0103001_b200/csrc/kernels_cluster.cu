@@ -414,7 +414,7 @@ cudaError_t ab_bulk_t(const void* in, void* out, int64_t batch, double scale, co
 // tensor maps of variant 41 (cuTensorMapEncodeTiled through the runtime's
 // driver entry point: no libcuda link)
 bool encode3(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
-             bool swz128) {
+             int swz) {  // swz: 0, 64 or 128 (B TMA swizzle span)
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
         cudaDriverEntryPointQueryResult q;
@@ -427,7 +427,8 @@ bool encode3(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2
     const cuuint32_t box[3] = {b0, b1, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : (swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -471,6 +472,36 @@ cudaError_t ab_geom(AbGeom* g) {
     return cudaSuccess;
 }
 
+// variants 45 / 46 (8-line tasks, 32 parts per phase)
+template <bool INV, int NS, int MINB>
+cudaError_t ab8_geom(AbGeom* g) {
+    static AbGeom cached;
+    if (!cached.grid) {
+        constexpr size_t SMEM = AbWs8Cfg<NS>::SMEM;
+        auto k = k_ab_ws8<INV, NS, MINB>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 288, SMEM);
+        if (e != cudaSuccess) return e;
+        AbGeom t;
+        t.grid = sms * (occ > 0 ? occ : 1);
+        const char* gv = getenv("B200FFT_AB_GRID");
+        if (gv && atoi(gv) > 0 && atoi(gv) < t.grid) t.grid = atoi(gv);
+        // waits point at least NS x grid task positions back (32 per transform)
+        const char* dv = getenv("B200FFT_AB_D");
+        t.D = (NS * t.grid + 31) / 32 + (dv ? atoi(dv) : 8);
+        const char* rv = getenv("B200FFT_AB_RING");
+        t.ring = t.D + (rv ? atoi(rv) : 24);
+        if (getenv("B200FFT_VERBOSE"))
+            fprintf(stderr, "ab_ws8<%d,%d>: grid %d (occ %d), D %d, ring %d\n", NS, MINB, t.grid, occ, t.D, t.ring);
+        cached = t;
+    }
+    *g = cached;
+    return cudaSuccess;
+}
+
 // caller-provided scratch: the Y ring (ring x 512 KiB) then the counters
 size_t ab_ws_bytes(int64_t ring, int64_t batch) {
     return (size_t)ring * 65536 * sizeof(float2) + (size_t)2 * batch * sizeof(int);
@@ -490,10 +521,10 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
     void* ring = ws;
     int* ctl = reinterpret_cast<int*>((char*)ws + (size_t)g.ring * 65536 * sizeof(float2));
     CUtensorMap m_x, m_out, m_yst, m_yld;
-    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, false) ||
-        !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, true) ||
-        !encode3(&m_yst, ring, 256, 256, g.ring, 16, 256, false) ||
-        !encode3(&m_yld, ring, 256, 256, g.ring, 256, 16, false))
+    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, 0) ||
+        !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, 128) ||
+        !encode3(&m_yst, ring, 256, 256, g.ring, 16, 256, 0) ||
+        !encode3(&m_yld, ring, 256, 256, g.ring, 256, 16, 0))
         return cudaErrorInvalidValue;
     e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
     if (e != cudaSuccess) return e;
@@ -555,6 +586,73 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
     return cudaLaunchKernelExC(&cfg, (const void*)k, args);
 }
 
+template <bool INV, int NS, int MINB>
+cudaError_t ab8_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
+    constexpr size_t SMEM = AbWs8Cfg<NS>::SMEM;
+    auto k = k_ab_ws8<INV, NS, MINB>;
+    AbGeom g;
+    cudaError_t e = ab8_geom<INV, NS, MINB>(&g);
+    if (e != cudaSuccess) return e;
+    if (batch <= 0) return cudaSuccess;
+    if (!ws || ws_bytes < ab_ws_bytes(g.ring, batch)) return cudaErrorInvalidValue;
+    void* ring = ws;
+    int* ctl = reinterpret_cast<int*>((char*)ws + (size_t)g.ring * 65536 * sizeof(float2));
+    CUtensorMap m_x, m_out, m_yst, m_yld;
+    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 8, 256, 0) ||
+        !encode3(&m_out, out, 256, 256, (uint64_t)batch, 8, 256, 64) ||
+        !encode3(&m_yst, ring, 256, 256, g.ring, 8, 256, 0) || !encode3(&m_yld, ring, 256, 256, g.ring, 256, 8, 0))
+        return cudaErrorInvalidValue;
+    e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
+    if (e != cudaSuccess) return e;
+    AbBulkCtl c{ctl, ctl + batch, g.D, g.ring};
+    float a_scale = (float)scale;
+    const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
+    const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256, 3);
+    int64_t a_batch = batch;
+    const float2* a_ring = reinterpret_cast<const float2*>(ring);
+    static const int opts = [] {
+        const char* v = getenv("B200FFT_AB_OPTS");
+        return v ? atoi(v) : 16;  // 16 x d: L2 prefetch of the A tile d tasks ahead
+    }();
+    int a_opts = opts;
+    void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
+    const int64_t tasks = 64 * batch;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3((unsigned)(tasks < g.grid ? tasks : g.grid), 1, 1);
+    cfg.blockDim = dim3(288, 1, 1);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static const bool persist = [] {
+        const char* v = getenv("B200FFT_AB_PERSIST");
+        return !(v && v[0] == '0');
+    }();
+    if (persist) {
+        static bool limit_set = false;
+        const size_t rb = (size_t)g.ring * 65536 * sizeof(float2);
+        if (!limit_set) {
+            int dev = 0, mx = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, rb < (size_t)mx ? rb : (size_t)mx);
+            limit_set = true;
+        }
+        attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[1].val.accessPolicyWindow.base_ptr = ring;
+        attr[1].val.accessPolicyWindow.num_bytes = rb;
+        attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.numAttrs = 2;
+    }
+    return cudaLaunchKernelExC(&cfg, (const void*)k, args);
+}
+
 }  // namespace
 
 bool cluster_supported(int prec, int64_t n, int* n1, int* n2) {
@@ -603,6 +701,8 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 42: return ab_tma_t<INV, true>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 43: return ab_tma_t<INV, true, 6>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 44: return ab_tma_t<INV, true, 2>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
+        case 45: return ab8_t<INV, 4, 3>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
+        case 46: return ab8_t<INV, 3, 4>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 29: return ab_pipe_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
         case 30: return ab_pipe_t<float, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 22: return step_ab2_t<float, INV>(in, out, batch, scale, tw4, tw, st);
@@ -615,9 +715,11 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
 }
 
 size_t cluster_workspace_bytes(int prec, int64_t n, int variant, int64_t batch) {
-    if (prec != 0 || n != 65536 || variant < 41 || variant > 44) return 0;
+    if (prec != 0 || n != 65536 || variant < 41 || variant > 46) return 0;
     AbGeom g;
-    cudaError_t e = variant == 42   ? ab_geom<false, true>(&g)
+    cudaError_t e = variant == 45   ? ab8_geom<false, 4, 3>(&g)
+                    : variant == 46 ? ab8_geom<false, 3, 4>(&g)
+                    : variant == 42 ? ab_geom<false, true>(&g)
                     : variant == 43 ? ab_geom<false, true, 6>(&g)
                     : variant == 44 ? ab_geom<false, true, 2>(&g)
                                     : ab_geom<false, false>(&g);
