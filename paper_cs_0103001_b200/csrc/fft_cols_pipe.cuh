@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(W*(R / E), 1)
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const int64_t u = lt + F::TPL * m;
-                const T hv = (filt.kind == 6) ? __ldg(reinterpret_cast<const T*>(filt.gu) + img + filt.n1 * u)
+                const T hv = (filt.kind >= 6) ? fourstep_filter<T>(filt, img, u, col < S ? col : 0)
                                               : filter_value<T>(filt, u, col + filt.col_off);
                 const T h = (col < S) ? hv * scale : (T)0;
                 w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], h);

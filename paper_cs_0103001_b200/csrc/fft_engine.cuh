@@ -18,6 +18,7 @@
 // registers (the fused filter pipeline).
 #pragma once
 #include "fft_common.cuh"
+#include "launch.h"
 
 namespace b200fft {
 
@@ -267,11 +268,12 @@ struct LineFFT {
 // W lines (rows) per CTA.  REAL_IN: input rows are float32 real values
 // (promotion to complex fused into the load, BASELINE configs[2]).
 // in_sh / out_sh >= 0: the rows are stored in column blocks of 2^sh (the
-// all-to-all pack layout of the slab-decomposed 2D transform):
-// element (row, v) at ((v >> sh) * batch + row) << sh | (v & (2^sh - 1)).
+// all-to-all layout of the slab-decomposed 2D transform):
+// element (row, v) at ((C*)blocks.p[v >> sh])[(row << sh) | (v & (2^sh - 1))],
+// the blocks local or in peer memory (launch.h BlockPtrs).
 // --------------------------------------------------------------------------
-__device__ __forceinline__ int64_t row_index(int64_t row, int64_t v, int64_t R, int64_t batch, int sh) {
-    return sh < 0 ? row * R + v : ((((v >> sh) * batch + row) << sh) | (v & ((1ll << sh) - 1)));
+__device__ __forceinline__ int64_t block_index(int64_t row, int v, int sh) {
+    return (row << sh) | (int64_t)(v & ((1 << sh) - 1));
 }
 
 // FILT: a row filter pass of the separable pipeline: forward
@@ -296,7 +298,9 @@ __device__ __forceinline__ void row_filter_pass(cpx<T>* v, cpx<T>* line, int lt,
 template <typename T, int R, int E, int W, bool INV, bool REAL_IN, bool FILT = false>
 __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_, cpx<T>* __restrict__ out,
                                                     int64_t batch, T scale, const cpx<T>* __restrict__ tw,
-                                                    int in_sh, int out_sh, const T* __restrict__ rowfilt) {
+                                                    int in_sh, int out_sh, const T* __restrict__ rowfilt,
+                                                    const __grid_constant__ BlockPtrs ib,
+                                                    const __grid_constant__ BlockPtrs ob) {
     using C = cpx<T>;
     using F = LineFFT<T, R, E, INV>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -321,11 +325,12 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_
         } else {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                const int64_t idx = row_index(row, lt + F::TPL * m, R, batch, in_sh);
+                const int x = lt + F::TPL * m;
+                const int64_t idx = block_index(row, x, in_sh);
                 if constexpr (REAL_IN)
-                    v[F::pos_in(m)] = mk((T)__ldg(reinterpret_cast<const float*>(in_) + idx), (T)0);
+                    v[F::pos_in(m)] = mk((T)reinterpret_cast<const float*>(ib.p[x >> in_sh])[idx], (T)0);
                 else
-                    v[F::pos_in(m)] = reinterpret_cast<const C*>(in_)[idx];
+                    v[F::pos_in(m)] = reinterpret_cast<const C*>(ib.p[x >> in_sh])[idx];
             }
         }
     }
@@ -338,8 +343,14 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_
             for (int m = 0; m < E; ++m) o[F::TPL * m] = cscale(v[F::pos_out(m)], scale);
         } else {
 #pragma unroll
-            for (int m = 0; m < E; ++m)
-                out[row_index(row, lt + F::TPL * m, R, batch, out_sh)] = cscale(v[F::pos_out(m)], scale);
+            for (int m = 0; m < E; ++m) {
+                const int x = lt + F::TPL * m;
+                reinterpret_cast<C*>(ob.p[x >> out_sh])[block_index(row, x, out_sh)] =
+                    cscale(v[F::pos_out(m)], scale);
+            }
+            // the blocks may be peer memory read by other GPUs after the
+            // stream-ordered barrier that follows this kernel
+            __threadfence_system();
         }
     }
 }
@@ -366,6 +377,16 @@ struct FilterArgs {
     int64_t tdiv;
     int64_t n1;
 };
+
+// pass-B filter of the four-step column passes: g_N[k1 + n1 k2] (kind 6,
+// the column factor of the separable Gaussian) or, kind 7 (the distributed
+// column slab, whose row passes are unfiltered), times g_M[col + col_off]
+template <typename T>
+__device__ __forceinline__ T fourstep_filter(const FilterArgs& f, int64_t img, int64_t u, int64_t col) {
+    T h = __ldg(reinterpret_cast<const T*>(f.gu) + img + f.n1 * u);
+    if (f.kind == 7) h *= __ldg(reinterpret_cast<const T*>(f.gv) + col + f.col_off);
+    return h;
+}
 
 // spectrum sqrt(Re^2 + Im^2) of one forward-transformed column (Sec. 6,
 // P:369-373), written when the pipeline's caller asked for it
@@ -481,7 +502,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ i
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int64_t u = lt + F::TPL * m;
-            const T hv = (filt.kind == 6) ? __ldg(reinterpret_cast<const T*>(filt.gu) + img + filt.n1 * u)
+            const T hv = (filt.kind >= 6) ? fourstep_filter<T>(filt, img, u, col < S ? col : 0)
                                           : filter_value<T>(filt, u, col + filt.col_off);
             const T h = (col < S) ? hv * scale : (T)0;
             w[FI::pos_in(m)] = cscale(v[F::pos_out(m)], h);

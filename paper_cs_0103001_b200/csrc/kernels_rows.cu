@@ -13,7 +13,7 @@ namespace {
 
 template <typename T, int R, bool INV, bool REAL_IN, bool FILT>
 cudaError_t rows_t(const void* in, void* out, int64_t batch, double scale, const void* tw, int in_sh, int out_sh,
-                   const void* rowfilt, cudaStream_t st) {
+                   const void* rowfilt, cudaStream_t st, const BlockPtrs* ibp, const BlockPtrs* obp) {
     constexpr int E = R < 16 ? R : 16;
     constexpr int TPL = R / E;
     constexpr int W = TPL >= 256 ? 1 : 256 / TPL;
@@ -27,19 +27,36 @@ cudaError_t rows_t(const void* in, void* out, int64_t batch, double scale, const
         attr = true;
     }
     if (batch <= 0) return cudaSuccess;
+    // blocked layouts: the given block pointers, or local blocks of batch
+    // rows x 2^sh elements one after the other
+    BlockPtrs ib{}, ob{};
+    auto blocks = [&](int sh, const void* base, const BlockPtrs* given, size_t eb, BlockPtrs& b) {
+        if (sh < 0) return true;
+        if ((R >> sh) > kMaxBlocks || (R >> sh) < 1) return false;
+        if (given) {
+            b = *given;
+        } else {
+            for (int q = 0; q < (R >> sh); ++q)
+                b.p[q] = const_cast<char*>(reinterpret_cast<const char*>(base)) + (size_t)q * ((size_t)batch << sh) * eb;
+        }
+        return true;
+    };
+    if (!blocks(in_sh, in, ibp, REAL_IN ? sizeof(float) : sizeof(cpx<T>), ib) ||
+        !blocks(out_sh, out, obp, sizeof(cpx<T>), ob))
+        return cudaErrorInvalidValue;
     const int64_t grid = (batch + W - 1) / W;
     kern<<<(unsigned)grid, W * TPL, smem, st>>>(in, reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
                                                  reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), in_sh, out_sh,
-                                                 reinterpret_cast<const T*>(rowfilt));
+                                                 reinterpret_cast<const T*>(rowfilt), ib, ob);
     return cudaGetLastError();
 }
 
 template <typename T, bool INV, bool REAL_IN, bool FILT>
 cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw, int in_sh,
-                   int out_sh, const void* rowfilt, cudaStream_t st) {
+                   int out_sh, const void* rowfilt, cudaStream_t st, const BlockPtrs* ib, const BlockPtrs* ob) {
     switch (R) {
 #define B200_ROWS_CASE(r) \
-    case r: return rows_t<T, r, INV, REAL_IN, FILT>(in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st);
+    case r: return rows_t<T, r, INV, REAL_IN, FILT>(in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st, ib, ob);
         B200_ROWS_CASE(1) B200_ROWS_CASE(2) B200_ROWS_CASE(4) B200_ROWS_CASE(8) B200_ROWS_CASE(16)
         B200_ROWS_CASE(32) B200_ROWS_CASE(64) B200_ROWS_CASE(128) B200_ROWS_CASE(256)
         B200_ROWS_CASE(512) B200_ROWS_CASE(1024) B200_ROWS_CASE(2048) B200_ROWS_CASE(4096)
@@ -181,7 +198,7 @@ cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* i
 
 cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void* in, void* out,
                         int64_t batch, double scale, const void* tw, cudaStream_t st, int in_sh, int out_sh,
-                        const void* rowfilt) {
+                        const void* rowfilt, const BlockPtrs* ib, const BlockPtrs* ob) {
     if (rowfilt && inv) return cudaErrorInvalidValue;  // filter passes start with the forward transform
     // in == out is safe for the TMA kernel: every tile is read (prefetched)
     // by the CTA that later writes it, and no other CTA touches it
@@ -195,17 +212,17 @@ cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void*
     }
     if (prec == 0) {
         if (rowfilt)
-            return real_in ? rows_r<float, false, true, true>(R, in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st)
+            return real_in ? rows_r<float, false, true, true>(R, in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st, ib, ob)
                            : rows_r<float, false, false, true>(R, in, out, batch, scale, tw, in_sh, out_sh, rowfilt,
-                                                               st);
-        if (real_in) return rows_r<float, false, true, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st);
-        return inv ? rows_r<float, true, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st)
-                   : rows_r<float, false, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st);
+                                                               st, ib, ob);
+        if (real_in) return rows_r<float, false, true, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st, ib, ob);
+        return inv ? rows_r<float, true, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st, ib, ob)
+                   : rows_r<float, false, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st, ib, ob);
     }
     if (real_in) return cudaErrorInvalidValue;
-    if (rowfilt) return rows_r<double, false, false, true>(R, in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st);
-    return inv ? rows_r<double, true, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st)
-               : rows_r<double, false, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st);
+    if (rowfilt) return rows_r<double, false, false, true>(R, in, out, batch, scale, tw, in_sh, out_sh, rowfilt, st, ib, ob);
+    return inv ? rows_r<double, true, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st, ib, ob)
+               : rows_r<double, false, false, false>(R, in, out, batch, scale, tw, in_sh, out_sh, nullptr, st, ib, ob);
 }
 
 }  // namespace b200fft

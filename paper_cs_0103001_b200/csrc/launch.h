@@ -7,18 +7,32 @@ namespace b200fft {
 
 struct FilterArgs;
 
+// Base pointers of the column blocks of a blocked row layout (the all-to-all
+// layout of the slab-decomposed 2D transform): element (row, v) of a launch
+// with shift sh lives at ((C*)p[v >> sh])[(row << sh) | (v & (2^sh - 1))].
+// The blocks may be local slabs or PEER memory (CUDA IPC over NVLink): the
+// row pass then stores its blocks straight into the other ranks' receive
+// slabs and the final row pass loads them from there -- the all-to-alls are
+// fused into the row kernels (Multi-GPU).
+constexpr int kMaxBlocks = 16;
+struct BlockPtrs {
+    void* p[kMaxBlocks];
+};
+
 // Largest transform length handled by one CTA, per precision (0 = c64, 1 = c128).
 constexpr int64_t kRowsMax = 8192;
 constexpr int64_t kColsMax[2] = {8192, 4096};
 
 // Kernel family A: batch contiguous rows of length R (power of two <= 8192).
 // in_sh / out_sh >= 0: rows stored in column blocks of 2^sh (all-to-all pack
-// layout, fft_engine.cuh row_index); -1: natural row-major.
+// layout): block q at in_blocks->p[q] / out_blocks->p[q], or, when null, at
+// in / out + q * (batch << sh) elements; -1: natural row-major.
 // rowfilt (T[R], optional): the separable-pipeline row pass, forward ->
 // * rowfilt[v] * scale -> inverse, stored unscaled (inv must be false).
 cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void* in, void* out,
                         int64_t batch, double scale, const void* tw, cudaStream_t st, int in_sh = -1,
-                        int out_sh = -1, const void* rowfilt = nullptr);
+                        int out_sh = -1, const void* rowfilt = nullptr, const BlockPtrs* in_blocks = nullptr,
+                        const BlockPtrs* out_blocks = nullptr);
 
 // Separable-pipeline pass with a transposed store (complex64, 256 <= R <=
 // 2048): rows of length R -> forward -> * rowfilt[v] * scale -> inverse ->

@@ -156,6 +156,13 @@ struct fft_plan_s {
     int nranks = 1, my_rank = 0;
     void* comm = nullptr;  // ncclComm_t owned by the plan
     int virt = 1;          // virtual ranks emulated on this GPU (tests), 1 = off
+    // fused all-to-alls of the 2D slab schedule:
+    // every rank's receive slabs (2 phases) mapped into every rank by CUDA IPC
+    int p2p = 0;                       // 0 not decided, 1 on, -1 off (decided collectively)
+    void* p2p_buf = nullptr;           // this rank's 2 receive slabs (owned)
+    void* peer_buf[kMaxBlocks] = {};   // rank q's p2p_buf as mapped here
+    void* bar_buf = nullptr;           // 1 float: the stream-ordered barrier
+    int64_t dist_phase = 0;            // receive slab of the next grid = phase & 1
     cudaEvent_t dev_ev = nullptr;
     // distributed four-step 1D (one transform of n = fs1 * fs2 over the ranks)
     int64_t fs1 = 0, fs2 = 0;
@@ -345,6 +352,23 @@ fft_status gauss_tables(fft_plan_s* p, double param) {
     return FFT_OK;
 }
 
+// W_N^x, x < N (fp64-generated): the twiddles of the four-step column passes
+cudaError_t ensure_twl(fft_plan_s* p, int64_t N) {
+    if (p->twl_n == N) return cudaSuccess;
+    if (p->twl) cudaFree(p->twl);
+    p->twl = nullptr;
+    p->twl_n = 0;
+    std::vector<double> t(2 * (size_t)N);
+    for (int64_t x = 0; x < N; ++x) {
+        const double ang = -2.0 * M_PI * (double)x / (double)N;
+        t[2 * x] = std::cos(ang);
+        t[2 * x + 1] = std::sin(ang);
+    }
+    cudaError_t e = upload(t, p->prec, &p->twl);
+    if (e == cudaSuccess) p->twl_n = N;
+    return e;
+}
+
 fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter filter, double param,
                         cudaStream_t st) {
     const int64_t N = p->n0, M = p->n1;
@@ -418,19 +442,8 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
     const bool c4_default = true;  // 1060 us vs 1130 us for the transposes path (C4, profiles/README.md)
     if (filter == FFT_FILTER_GAUSS && !literal && p->prec == 0 && N >= 4096 && N <= 8192 && M >= 256 &&
         M <= 8192 && (c4_env ? c4_env[0] == '1' : c4_default)) {
-        if (p->twl_n != N) {
-            if (p->twl) cudaFree(p->twl);
-            p->twl = nullptr;
-            std::vector<double> t(2 * (size_t)N);
-            for (int64_t x = 0; x < N; ++x) {
-                const double ang = -2.0 * M_PI * (double)x / (double)N;
-                t[2 * x] = std::cos(ang);
-                t[2 * x + 1] = std::sin(ang);
-            }
-            e = upload(t, p->prec, &p->twl);
-            if (e != cudaSuccess) return cuda_fail(e, "column twiddle upload");
-            p->twl_n = N;
-        }
+        e = ensure_twl(p, N);
+        if (e != cudaSuccess) return cuda_fail(e, "column twiddle upload");
         const int64_t N1 = 64, N2 = N / 64;
         const size_t in_grid = (size_t)N * M * (real_in ? 4 : p->elem_bytes());
         const size_t grid = (size_t)N * M * p->elem_bytes();
@@ -538,22 +551,228 @@ fft_status dist_exchange(fft_plan_s* p, char* send, char* recv, int64_t blk, cud
     return FFT_OK;
 }
 
+// Column step of the slab schedule on one column slab [N][SM] (global
+// columns col_off ..): the Gaussian pipeline's fwd * H / (N M) * inv as the
+// three four-step column passes (N = 64 N2, as on one GPU; pass B applies
+// g_N[k1 + 64 k2] g_M[col_off + v], filter kind 7), else one k_cols launch
+// over the N-long columns.
+cudaError_t dist_columns(fft_plan_s* p, char* cs, int mode, const FilterArgs& f, int64_t col_off, int64_t SM,
+                         cudaStream_t st, int* launches) {
+    const int64_t N = p->n0, M = p->n1;
+    const char* c4 = getenv("B200FFT_PIPE_COLS4");
+    if (mode == 2 && f.kind == FFT_FILTER_GAUSS && p->prec == 0 && N >= 4096 && N <= 8192 && SM >= 16 &&
+        !(c4 && c4[0] == '0')) {
+        cudaError_t e = ensure_twl(p, N);
+        if (e != cudaSuccess) return e;
+        const int64_t N1 = 64, N2 = N / 64;
+        FilterArgs fa{};
+        fa.tw_l = p->twl;
+        fa.tdiv = SM;
+        FilterArgs fb{};
+        fb.kind = 7;
+        fb.gu = f.gu;
+        fb.gv = f.gv;
+        fb.n1 = N1;
+        fb.col_off = col_off;
+        e = launch_cols_fourstep(3, N1, cs, cs, N2 * SM, 1, 1.0, p->tw, fa, st);
+        if (e == cudaSuccess)
+            e = launch_cols_fourstep(2, N2, cs, cs, SM, N1, 1.0 / ((double)N * (double)M), p->tw, fb, st);
+        if (e == cudaSuccess) e = launch_cols_fourstep(4, N1, cs, cs, N2 * SM, 1, 1.0, p->tw, fa, st);
+        *launches += 3;
+        return e;
+    }
+    FilterArgs fl = f;
+    fl.col_off = col_off;
+    const int cmode = mode == 2 ? 2 : mode;
+    const double sc = mode == 2 ? 1.0 / ((double)N * (double)M) : (mode == 0 ? 1.0 / (double)N : 1.0);
+    *launches += 1;
+    return launch_cols(p->prec, cmode, N, cs, cs, SM, 1, sc, p->tw, fl, st);
+}
+
+// ---- fused all-to-alls: direct block stores / loads over peer memory ----
+// The row pass of rank r stores block q of its rows straight into rank q's
+// receive slab (at block position r), and the final row pass (or unblock
+// copy) loads block q of its rows straight from rank q's column slab: no
+// send buffer, no NCCL all-to-all, two stream-ordered barriers per grid.
+// Receive slabs alternate between two phases, so a rank still reading the
+// previous grid's slabs never races with the next grid's stores (those only
+// start after the next grid's first barrier).  Virtual ranks run the same
+// schedule with local slabs and no barriers.
+#ifdef B200FFT_WITH_NCCL
+void p2p_release(fft_plan_s* p) {
+    for (int q = 0; q < kMaxBlocks; ++q) {
+        if (p->peer_buf[q] && q != p->my_rank) cudaIpcCloseMemHandle(p->peer_buf[q]);
+        p->peer_buf[q] = nullptr;
+    }
+    if (p->p2p_buf) cudaFree(p->p2p_buf);
+    if (p->bar_buf) cudaFree(p->bar_buf);
+    p->p2p_buf = p->bar_buf = nullptr;
+}
+
+// collective: every rank of the communicator calls it at the same point
+fft_status p2p_prepare(fft_plan_s* p, cudaStream_t st) {
+    if (p->p2p != 0) return FFT_OK;
+    const int P = p->nranks, me = p->my_rank;
+    ncclComm_t comm = (ncclComm_t)p->comm;
+    const char* env = getenv("B200FFT_P2P");
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        int ok;
+        int pad;
+    };
+    Rec mine{};
+    int ok = !(env && env[0] == '0') && P <= kMaxBlocks;
+    const size_t bytes = 2 * (size_t)p->elems() * p->elem_bytes();
+    if (ok && cudaMalloc(&p->p2p_buf, bytes) != cudaSuccess) ok = 0;
+    if (ok && cudaMalloc(&p->bar_buf, 16) != cudaSuccess) ok = 0;
+    if (ok && cudaMemsetAsync(p->bar_buf, 0, 16, st) != cudaSuccess) ok = 0;
+    if (ok && cudaIpcGetMemHandle(&mine.h, p->p2p_buf) != cudaSuccess) ok = 0;
+    cudaGetLastError();
+    mine.ok = ok;
+    char* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(Rec) * (P + 1));
+    if (e != cudaSuccess) return cuda_fail(e, "p2p handle exchange buffer");
+    std::vector<Rec> all(P);
+    e = cudaMemcpyAsync(d + P * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, st);
+    ncclResult_t r = ncclAllGather(d + P * sizeof(Rec), d, sizeof(Rec), ncclChar, comm, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(all.data(), d, sizeof(Rec) * P, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    bool all_ok = e == cudaSuccess && r == ncclSuccess;
+    for (int q = 0; q < P && all_ok; ++q) all_ok = all[q].ok != 0;
+    int opened = 1;
+    if (all_ok) {
+        for (int q = 0; q < P; ++q) {
+            if (q == me) {
+                p->peer_buf[q] = p->p2p_buf;
+            } else if (cudaIpcOpenMemHandle(&p->peer_buf[q], all[q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                p->peer_buf[q] = nullptr;
+                opened = 0;
+                cudaGetLastError();
+            }
+        }
+        // every rank must have mapped every peer
+        int* f = reinterpret_cast<int*>(d);
+        e = cudaMemcpyAsync(f, &opened, sizeof(int), cudaMemcpyHostToDevice, st);
+        r = ncclAllReduce(f, f, 1, ncclInt32, ncclMin, comm, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&opened, f, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        all_ok = e == cudaSuccess && r == ncclSuccess && opened == 1;
+    }
+    cudaFree(d);
+    if (!all_ok) p2p_release(p);
+    p->p2p = all_ok ? 1 : -1;
+    if (getenv("B200FFT_VERBOSE")) fprintf(stderr, "rank %d: fused peer all-to-alls %s\n", me, all_ok ? "on" : "off");
+    return FFT_OK;
+}
+
+fft_status dist_barrier(fft_plan_s* p, cudaStream_t st) {
+    ncclResult_t r = ncclAllReduce(p->bar_buf, p->bar_buf, 1, ncclFloat, ncclSum, (ncclComm_t)p->comm, st);
+    if (r != ncclSuccess) return fail(FFT_E_NCCL, std::string("barrier: ") + ncclGetErrorString(r));
+    return FFT_OK;
+}
+#endif
+
+// the fused schedule; returns FFT_E_UNSUPPORTED (nothing launched) when it
+// does not apply, and the caller runs the all-to-all schedule
+fft_status run_dist_2d_fused(fft_plan_s* p, const void* in, void* out, int mode, const FilterArgs& f,
+                             cudaStream_t st) {
+    const int P = p->P();
+    const char* ex = getenv("B200FFT_DIST_EXCHANGE");
+    if (P > kMaxBlocks || (ex && ex[0] == '1')) return FFT_E_UNSUPPORTED;
+    const int64_t N = p->n0, M = p->n1, SN = N / P, SM = M / P;
+    const size_t eb = p->elem_bytes();
+    const int64_t slab = SN * M, blk = SN * SM;
+    const int sh = ilog2(SM);
+    const int nloc = p->comm ? 1 : P;
+    const int r0 = p->comm ? p->my_rank : 0;
+    char* vbase = nullptr;
+    if (p->comm) {
+#ifdef B200FFT_WITH_NCCL
+        fft_status s = p2p_prepare(p, st);
+        if (s != FFT_OK) return s;
+        if (p->p2p != 1) return FFT_E_UNSUPPORTED;
+#else
+        return FFT_E_UNSUPPORTED;
+#endif
+    } else {
+        fft_status s = ensure_workspace(p);
+        if (s != FFT_OK) return s;
+        vbase = (char*)p->ws;
+    }
+    const bool real_in = mode == 2 && (p->flags & FFT_IN_REAL_F32);
+    const size_t in_eb = real_in ? 4 : eb;
+    cudaError_t e;
+    int launches = 0;
+    for (int64_t g = 0; g < p->batch; ++g) {
+        const int ph = (int)(p->dist_phase++ & 1);
+        // rank q's receive (column) slab of this phase
+        auto rslab = [&](int q) -> char* {
+            return p->comm ? (char*)p->peer_buf[q] + (size_t)ph * slab * eb
+                           : vbase + ((size_t)ph * P + q) * slab * eb;
+        };
+        const char* gin = (const char*)in + (size_t)g * nloc * slab * in_eb;
+        char* gout = (char*)out + (size_t)g * nloc * slab * eb;
+        // 1. rows of every local slab, block q stored into rank q's column slab
+        for (int l = 0; l < nloc; ++l) {
+            BlockPtrs ob{};
+            for (int q = 0; q < P; ++q) ob.p[q] = rslab(q) + (size_t)(r0 + l) * blk * eb;
+            const double sc = mode == 1 ? 1.0 / (double)M : 1.0;
+            e = launch_rows(p->prec, mode == 1, real_in, M, gin + (size_t)l * slab * in_eb, nullptr, SN, sc, p->tw, st,
+                            -1, sh, nullptr, nullptr, &ob);
+            if (e != cudaSuccess) return cuda_fail(e, "k_rows (peer-store) launch");
+            ++launches;
+        }
+#ifdef B200FFT_WITH_NCCL
+        if (p->comm) {
+            fft_status s = dist_barrier(p, st);
+            if (s != FFT_OK) return s;
+        }
+#endif
+        // 2. columns (length N) of every local column slab [N][SM], in place
+        for (int l = 0; l < nloc; ++l) {
+            e = dist_columns(p, rslab(r0 + l), mode, f, (int64_t)(r0 + l) * SM, SM, st, &launches);
+            if (e != cudaSuccess) return cuda_fail(e, "column step launch");
+        }
+#ifdef B200FFT_WITH_NCCL
+        if (p->comm) {
+            fft_status s = dist_barrier(p, st);
+            if (s != FFT_OK) return s;
+        }
+#endif
+        // 3. rows of every local slab, block q loaded from rank q's column slab
+        for (int l = 0; l < nloc; ++l) {
+            BlockPtrs ib{};
+            for (int q = 0; q < P; ++q) ib.p[q] = rslab(q) + (size_t)(r0 + l) * blk * eb;
+            char* dst = gout + (size_t)l * slab * eb;
+            if (mode == 2) {
+                e = launch_rows(p->prec, true, false, M, nullptr, dst, SN, 1.0, p->tw, st, sh, -1, nullptr, &ib, nullptr);
+                ++launches;
+            } else {
+                e = cudaSuccess;
+                for (int q = 0; q < P && e == cudaSuccess; ++q)
+                    e = cudaMemcpy2DAsync(dst + (size_t)q * SM * eb, M * eb, ib.p[q], SM * eb, SM * eb, (size_t)SN,
+                                          cudaMemcpyDefault, st);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "final row pass / unblock (peer loads)");
+        }
+    }
+    p->last_launches = launches;
+    return FFT_OK;
+}
+
 // mode 0: forward (eq5), 1: inverse (2D-IDFT), 2: filter pipeline
 fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_filter filter, double param,
                        cudaStream_t st) {
     const int P = p->P();
     const int64_t N = p->n0, M = p->n1, SN = N / P, SM = M / P;
     if (N % P || M % P || SN < 1 || SM < 1) return fail(FFT_E_INVALID_SIZE, "grid not divisible by the rank count");
-    fft_status s = ensure_workspace(p);
-    if (s != FFT_OK) return s;
+    fft_status s = FFT_OK;
     const size_t eb = p->elem_bytes();
     const int64_t slab = SN * M;      // elements per rank per grid
     const int64_t blk = SN * SM;      // elements per (rank, peer) block
     const int sh = ilog2(SM);
     const int nloc = p->comm ? 1 : P;  // slabs handled by this process
     const int r0 = p->comm ? p->my_rank : 0;
-    char* ws0 = (char*)p->ws;
-    char* ws1 = ws0 + (size_t)nloc * slab * eb;
     const bool real_in = mode == 2 && (p->flags & FFT_IN_REAL_F32);
     const size_t in_eb = real_in ? 4 : eb;
     FilterArgs f{};
@@ -568,6 +787,12 @@ fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_f
     } else if (mode == 2) {
         f.b2 = param * param;
     }
+    s = run_dist_2d_fused(p, in, out, mode, f, st);
+    if (s != FFT_E_UNSUPPORTED) return s;
+    s = ensure_workspace(p);
+    if (s != FFT_OK) return s;
+    char* ws0 = (char*)p->ws;
+    char* ws1 = ws0 + (size_t)nloc * slab * eb;
     cudaError_t e;
     int launches = 0;
     for (int64_t g = 0; g < p->batch; ++g) {
@@ -586,14 +811,8 @@ fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_f
         if (s != FFT_OK) return s;
         // 2. columns (length N) of every local column slab [N][SM]
         for (int l = 0; l < nloc; ++l) {
-            FilterArgs fl = f;
-            fl.col_off = (int64_t)(r0 + l) * SM;
-            const int cmode = mode == 2 ? 2 : mode;
-            const double sc = mode == 2 ? 1.0 / ((double)N * (double)M) : (mode == 0 ? 1.0 / (double)N : 1.0);
-            char* cs = ws1 + (size_t)l * slab * eb;
-            e = launch_cols(p->prec, cmode, N, cs, cs, SM, 1, sc, p->tw, fl, st);
-            if (e != cudaSuccess) return cuda_fail(e, "k_cols launch");
-            ++launches;
+            e = dist_columns(p, ws1 + (size_t)l * slab * eb, mode, f, (int64_t)(r0 + l) * SM, SM, st, &launches);
+            if (e != cudaSuccess) return cuda_fail(e, "column step launch");
         }
         s = dist_exchange(p, ws1, ws0, blk, st);
         if (s != FFT_OK) return s;
@@ -1339,6 +1558,7 @@ fft_status fft_plan_destroy(fft_plan p) {
     }
     if (p->hev) cudaEventDestroy(p->hev);
 #ifdef B200FFT_WITH_NCCL
+    p2p_release(p);
     if (p->comm) ncclCommDestroy((ncclComm_t)p->comm);
 #endif
     e = cudaGetLastError();

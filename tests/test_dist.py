@@ -34,9 +34,15 @@ def _lib():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("exchange", [False, True])
 @pytest.mark.parametrize("P", [2, 4, 8])
 @pytest.mark.parametrize("N,M", [(64, 64), (256, 512), (2048, 2048)])
-def test_virtual_ranks_pipeline(P, N, M):
+def test_virtual_ranks_pipeline(P, N, M, exchange, monkeypatch):
+    """Fused schedule (row kernels store / load the blocks of the other
+    ranks' column slabs directly) and, with B200FFT_DIST_EXCHANGE=1, the
+    all-to-all schedule (send slab -> exchange -> receive slab)."""
+    if exchange:
+        monkeypatch.setenv("B200FFT_DIST_EXCHANGE", "1")
     b = _lib()
     f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=500 + P, dtype=np.complex64).reshape(N, M)
     p = b.Plan((N, M))
@@ -53,6 +59,30 @@ def test_virtual_ranks_pipeline(P, N, M):
     torch.cuda.synchronize()
     assert oracle.rel_l2(F.cpu().numpy(), oracle.fft2d(f)) <= 1e-5
     assert oracle.rel_l2(g.cpu().numpy(), oracle.ifft2d(f)) <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exchange", [False, True])
+@pytest.mark.parametrize("P,N,M", [(2, 4096, 1024), (4, 8192, 256), (8, 4096, 2048)])
+def test_virtual_ranks_fourstep_columns(P, N, M, exchange, monkeypatch):
+    """Long columns (N >= 4096): the column step as the three four-step
+    column passes on each [N][M/P] slab, pass B applying g_N[k1 + 64 k2] *
+    g_M[col_off + v] (filter kind 7), batch of two grids."""
+    if exchange:
+        monkeypatch.setenv("B200FFT_DIST_EXCHANGE", "1")
+    b = _lib()
+    f = fixtures.complex_input(2 * N * M, fixtures.UNIFORM, seed=60 + P, dtype=np.complex64).reshape(2, N, M)
+    p = b.Plan((N, M), batch=2)
+    p.set_virtual_ranks(P)
+    fd = torch.from_numpy(f).cuda()
+    od = torch.empty_like(fd)
+    p.filter_pipeline(fd, od, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    assert p.last_launch_count() == 2 * (P + 3 * P + P)
+    p.destroy()
+    out = od.cpu().numpy()
+    for i in range(2):
+        assert oracle.rel_l2(out[i], oracle.gauss_pipeline(f[i], 0.1)) <= 1e-5
 
 
 @pytest.mark.gpu
@@ -150,18 +180,27 @@ def test_virtual_ranks_c5_shape():
 
 
 @pytest.mark.gpu
-def test_nccl_single_rank_communicator():
-    """The NCCL data path (ncclSend/ncclRecv all-to-all) with one rank."""
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_nccl_single_rank_communicator(p2p, monkeypatch):
+    """The communicator data path with one rank: the fused peer-memory
+    schedule (IPC handle exchange over NCCL, stream-ordered NCCL barriers) and,
+    with B200FFT_P2P=0, the ncclSend/ncclRecv all-to-all schedule."""
+    monkeypatch.setenv("B200FFT_P2P", p2p)
     b = _lib()
     N = M = 512
     f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=77).reshape(N, M)
-    p = b.Plan((N, M))
+    p = b.Plan((N, M), batch=1)
     p.set_comm(b.nccl_unique_id(), 1, 0)
     fd = torch.from_numpy(f).cuda()
     od = torch.empty_like(fd)
-    p.filter_pipeline(fd, od, b.FILTER_GAUSS, 0.1)
+    for _ in range(3):  # both receive phases and back
+        p.filter_pipeline(fd, od, b.FILTER_GAUSS, 0.1)
     torch.cuda.synchronize()
     assert oracle.rel_l2(od.cpu().numpy(), oracle.gauss_pipeline(f, 0.1)) <= 1e-5
+    F = torch.empty_like(fd)
+    p.forward(fd, F)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(F.cpu().numpy(), oracle.fft2d(f)) <= 1e-5
     p.destroy()
 
 
@@ -324,6 +363,49 @@ def test_block_layout_roundtrip():
     for row in range(SN):
         for v in range(16):
             assert flat[(((v >> sh) * SN + row) << sh) | (v & (SM - 1))] == a[row, v]
+
+
+def _fused_schedule(grids, P, H):
+    """The fused schedule of run_dist_2d_fused written out on flat per-rank
+    buffers with the library's pointer arithmetic: rank q's receive slab of
+    phase ph, block position r at r * SN * SM, element (row, x) of a block at
+    (row << sh) | (x & (SM - 1)); the row pass of rank r stores block q there,
+    the final pass of rank r loads it back from the same place."""
+    N, M = grids[0].shape
+    SN, SM = N // P, M // P
+    sh = SM.bit_length() - 1
+    blk = SN * SM
+    recv = np.zeros((2, P, N * SM), dtype=complex)  # [phase][rank] column slabs
+    outs = []
+    for g, f in enumerate(grids):
+        ph = g & 1
+        out = np.zeros((N, M), dtype=complex)
+        for r in range(P):  # 1. rows, peer stores
+            rows = np.stack([oracle.fft(x) * M for x in f[r * SN:(r + 1) * SN]])
+            for row in range(SN):
+                for x in range(M):
+                    recv[ph, x >> sh, r * blk + ((row << sh) | (x & (SM - 1)))] = rows[row, x]
+        for q in range(P):  # 2. columns of rank q's slab, filter columns q SM ..
+            cs = recv[ph, q].reshape(N, SM)
+            cf = np.stack([oracle.fft(cs[:, j]) for j in range(SM)], axis=1) * H[:, q * SM:(q + 1) * SM] / M
+            recv[ph, q] = np.stack([oracle.ifft(cf[:, j]) for j in range(SM)], axis=1).ravel()
+        for r in range(P):  # 3. rows, peer loads
+            for row in range(SN):
+                line = np.array([recv[ph, x >> sh, r * blk + ((row << sh) | (x & (SM - 1)))] for x in range(M)])
+                out[r * SN + row] = oracle.ifft(line)
+        outs.append(out)
+    return outs
+
+
+@pytest.mark.parametrize("P,N,M", [(2, 8, 16), (4, 16, 8), (8, 16, 16)])
+def test_fused_peer_schedule_index_maps(P, N, M):
+    """CPU pin of the fused all-to-all addressing (three grids: both receive
+    phases, then phase 0 again, each must be independent)."""
+    grids = [fixtures.complex_input(N * M, fixtures.UNIFORM, seed=40 + i, dtype=np.complex128).reshape(N, M)
+             for i in range(3)]
+    H = oracle.gauss_filter(N, M, 0.1)
+    for f, out in zip(grids, _fused_schedule(grids, P, H)):
+        assert oracle.rel_l2(out, oracle.gauss_pipeline(f, 0.1)) <= 1e-13
 
 
 # ---------------------------------------------- NEXT-2: the paper's tree
