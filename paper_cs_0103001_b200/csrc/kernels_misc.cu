@@ -78,7 +78,54 @@ __global__ void __launch_bounds__(256) k_tree_combine(const cpx<T>* __restrict__
     }
 }
 
+// Distributed transpose (the fused pack -> all-to-all -> unpack of the
+// four-step 1D schedule): the global matrix G[P R][Cn] is held in row slabs
+// of R rows by P ranks (src.p[s]), G^T[Cn][P R] is wanted in row slabs of Cb
+// rows (dst.p[d]).  A launch covers the global rows [row0, row0 + nrows) and
+// columns [col0, col0 + ncols): a rank pushing its own rows into the other
+// ranks' slabs (peer stores), a rank pulling its own output rows from the
+// other ranks' slabs (peer loads), or all P virtual ranks at once.
+// R, Cb: powers of two (shifts rsh, bsh); 32 x 32 tiles through padded smem.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_dist_transpose(const __grid_constant__ BlockPtrs src, const __grid_constant__ BlockPtrs dst, int rsh, int64_t Cn,
+                     int bsh, int64_t Rg, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols) {
+    using C = cpx<T>;
+    __shared__ C tile[32][33];
+    const int64_t gc0 = col0 + (int64_t)blockIdx.x * 32, gr0 = row0 + (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int64_t rmask = (1ll << rsh) - 1, bmask = (1ll << bsh) - 1;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int64_t gr = gr0 + ty + i, gc = gc0 + tx;
+        if (gr < row0 + nrows && gc < col0 + ncols)
+            tile[ty + i][tx] = reinterpret_cast<const C*>(src.p[gr >> rsh])[(gr & rmask) * Cn + gc];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int64_t gc = gc0 + ty + i, gr = gr0 + tx;
+        if (gr < row0 + nrows && gc < col0 + ncols)
+            reinterpret_cast<C*>(dst.p[gc >> bsh])[(gc & bmask) * Rg + gr] = tile[tx][ty + i];
+    }
+    __threadfence_system();  // peer stores, read by other GPUs after the following barrier
+}
+
 }  // namespace
+
+cudaError_t launch_dist_transpose(int prec, const BlockPtrs& src, const BlockPtrs& dst, int64_t R, int64_t Cn,
+                                  int64_t Cb, int64_t P, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols,
+                                  cudaStream_t st) {
+    if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+    if (P > kMaxBlocks || (R & (R - 1)) || (Cb & (Cb - 1))) return cudaErrorInvalidValue;
+    const int rsh = ilog2c((int)R), bsh = ilog2c((int)Cb);
+    dim3 grid((unsigned)((ncols + 31) / 32), (unsigned)((nrows + 31) / 32), 1);
+    if (prec == 0)
+        k_dist_transpose<float><<<grid, 256, 0, st>>>(src, dst, rsh, Cn, bsh, P * R, row0, nrows, col0, ncols);
+    else
+        k_dist_transpose<double><<<grid, 256, 0, st>>>(src, dst, rsh, Cn, bsh, P * R, row0, nrows, col0, ncols);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_transpose(int prec, const void* in, void* out, int64_t R, int64_t Cn, int64_t nmat,
                              cudaStream_t st) {

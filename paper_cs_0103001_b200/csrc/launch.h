@@ -69,6 +69,12 @@ cudaError_t launch_pass(int prec, bool inv, int64_t R, const void* in, void* out
 // Distributed four-step helpers (kernels_misc.cu): batched transpose
 // out[c][r] = in[r][c] of nmat [R][Cn] matrices; four-step twiddle
 // y[row][k2] *= W_N^{(row0 + row) k2} with W_N^x = ta[x >> sh] * tb[x & mask].
+// Distributed transpose G[P R][Cn] (row slabs of R at src.p[s]) -> G^T
+// (row slabs of Cb at dst.p[d]) over global rows [row0, +nrows) x columns
+// [col0, +ncols) (kernels_misc.cu k_dist_transpose).
+cudaError_t launch_dist_transpose(int prec, const BlockPtrs& src, const BlockPtrs& dst, int64_t R, int64_t Cn,
+                                  int64_t Cb, int64_t P, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols,
+                                  cudaStream_t st);
 cudaError_t launch_transpose(int prec, const void* in, void* out, int64_t R, int64_t Cn, int64_t nmat,
                              cudaStream_t st);
 cudaError_t launch_twiddle4(int prec, bool inv, void* y, int64_t rows, int64_t L, int64_t row0, const void* ta,

@@ -1032,8 +1032,111 @@ fft_status run_paper_tree(fft_plan_s* p, const void* in, void* out, cudaStream_t
 #endif
 }
 
-fft_status run_dist_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
+// Fused form of the schedule below: each pack -> all-to-all -> unpack is ONE
+// distributed-transpose launch (k_dist_transpose) whose stores go straight
+// into the other ranks' receive slabs (peer memory) -- the last one pulls
+// this rank's natural-order output from the other ranks' slabs instead, as
+// the caller's output buffer is not mapped by the peers.  Two receive
+// phases: A ([S1][N2] after the first transpose) and B ([S2][N1]).  A rank
+// pushes into phase A only after the previous call's barrier 2 (all ranks
+// done with their phase-A work) and into phase B only after this call's
+// barrier 1 (all ranks done pulling from phase B in the previous call), so
+// two stream-ordered barriers per transform suffice.  Virtual ranks: one
+// launch per transpose for all P ranks, no barriers.
+fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
+    const int P = p->P();
+    const char* ex = getenv("B200FFT_DIST_EXCHANGE");
+    if (P > kMaxBlocks || (ex && ex[0] == '1')) return FFT_E_UNSUPPORTED;
     fft_status s = fs_prepare(p);
+    if (s != FFT_OK) return s;
+    char* vbase = nullptr;
+    if (p->comm) {
+#ifdef B200FFT_WITH_NCCL
+        s = p2p_prepare(p, st);
+        if (s != FFT_OK) return s;
+        if (p->p2p != 1) return FFT_E_UNSUPPORTED;
+#else
+        return FFT_E_UNSUPPORTED;
+#endif
+    } else {
+        s = ensure_workspace(p);
+        if (s != FFT_OK) return s;
+        vbase = (char*)p->ws;
+    }
+    p->sub_a->stream = st;
+    p->sub_b->stream = st;
+    const int64_t N1 = p->fs1, N2 = p->fs2, S1 = N1 / P, S2 = N2 / P;
+    const int64_t loc = p->n0 / P;
+    const size_t eb = p->elem_bytes();
+    const int nloc = p->comm ? 1 : P;
+    const int r0 = p->comm ? p->my_rank : 0;
+    auto buf = [&](int ph, int q) -> char* {
+        return p->comm ? (char*)p->peer_buf[q] + (size_t)ph * loc * eb : vbase + ((size_t)ph * P + q) * loc * eb;
+    };
+    auto local = [&](const void* base, int q) -> void* {  // rank q's slab of a caller buffer
+        return p->comm ? (q == p->my_rank ? const_cast<void*>(base) : nullptr)
+                       : (char*)const_cast<void*>(base) + (size_t)q * loc * eb;
+    };
+    BlockPtrs bin{}, ba{}, bb{}, bout{};
+    for (int q = 0; q < P; ++q) {
+        bin.p[q] = local(in, q);
+        ba.p[q] = buf(0, q);
+        bb.p[q] = buf(1, q);
+        bout.p[q] = local(out, q);
+    }
+    cudaError_t e;
+    int launches = 0;
+    // 1. x viewed as [N2][N1] (rank r: rows n2 in [r S2, ..)) -> phase A
+    //    [N1][N2] slabs of S1 rows (row n1, n2 global); push own rows
+    e = launch_dist_transpose(p->prec, bin, ba, S2, N1, S1, P, (int64_t)r0 * S2, nloc * S2, 0, N1, st);
+    if (e != cudaSuccess) return cuda_fail(e, "distributed transpose 1");
+    ++launches;
+#ifdef B200FFT_WITH_NCCL
+    if (p->comm && (s = dist_barrier(p, st)) != FFT_OK) return s;
+#endif
+    // 2. (A) FFT over n2 (unnormalised) and (T) the four-step twiddle
+    for (int l = 0; l < nloc; ++l) {
+        char* a = buf(0, r0 + l);
+        s = run_1d(p->sub_a, a, a, inv, st);
+        if (s != FFT_OK) return s;
+        launches += p->sub_a->last_launches;
+        e = launch_twiddle4(p->prec, inv, a, S1, N2, (int64_t)(r0 + l) * S1, p->fta, p->ftb, p->fsh, st);
+        if (e != cudaSuccess) return cuda_fail(e, "twiddle");
+        ++launches;
+    }
+    // 3. phase A [N1][N2] (rows n1) -> phase B [N2][N1] slabs of S2 rows; push
+    e = launch_dist_transpose(p->prec, ba, bb, S1, N2, S2, P, (int64_t)r0 * S1, nloc * S1, 0, N2, st);
+    if (e != cudaSuccess) return cuda_fail(e, "distributed transpose 2");
+    ++launches;
+#ifdef B200FFT_WITH_NCCL
+    if (p->comm && (s = dist_barrier(p, st)) != FFT_OK) return s;
+#endif
+    // 4. (B) FFT over n1 with the paper's 1/n (forward): Z[k2][k1] = X[k2 + N2 k1]
+    const bool transposed_out = !inv && (p->flags & FFT_OUT_TRANSPOSED);
+    for (int l = 0; l < nloc; ++l) {
+        char* b = buf(1, r0 + l);
+        const double saved = p->sub_b->scale_override;
+        if (inv) p->sub_b->scale_override = 1.0;
+        s = run_1d(p->sub_b, b, transposed_out ? (char*)bout.p[r0 + l] : b, inv, st);
+        p->sub_b->scale_override = saved;
+        if (s != FFT_OK) return s;
+        launches += p->sub_b->last_launches;
+    }
+    if (!transposed_out) {
+        // 5. natural order: Z [N2][N1] -> X as [N1][N2] slabs of S1 rows
+        //    (rank r: rows k1 in [r S1, ..) = X[r n/P, ..)); pull own rows
+        e = launch_dist_transpose(p->prec, bb, bout, S2, N1, S1, P, 0, N2, (int64_t)r0 * S1, nloc * S1, st);
+        if (e != cudaSuccess) return cuda_fail(e, "distributed transpose 3");
+        ++launches;
+    }
+    p->last_launches = launches;
+    return FFT_OK;
+}
+
+fft_status run_dist_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
+    fft_status s = run_dist_1d_fused(p, in, out, inv, st);
+    if (s != FFT_E_UNSUPPORTED) return s;
+    s = fs_prepare(p);
     if (s == FFT_OK) s = ensure_workspace(p);
     if (s != FFT_OK) return s;
     p->sub_a->stream = st;

@@ -109,13 +109,24 @@ def test_virtual_ranks_c4_shape_real_input():
     assert oracle.rel_l2(o2.cpu().numpy(), oracle.filter_pipeline(img.astype(complex), H)) <= 1e-5
 
 
+def _sched_env(monkeypatch, sched, P):
+    """fused: distributed transposes into peer slabs (default); exchange: the
+    pack -> all-to-all -> unpack schedule (device copies for virtual ranks,
+    ncclSend/ncclRecv with a communicator)."""
+    if sched == "exchange":
+        monkeypatch.setenv("B200FFT_P2P" if P == 1 else "B200FFT_DIST_EXCHANGE", "0" if P == 1 else "1")
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("sched", ["fused", "exchange"])
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
 @pytest.mark.parametrize("m,dtype", [(8, np.complex64), (16, np.complex64), (20, np.complex64),
                                      (22, np.complex64), (18, np.complex128)])
-def test_virtual_ranks_four_step_1d(P, m, dtype):
-    """The distributed four-step 1D schedule (3 all-to-alls, natural order)
-    as P virtual ranks; forward (1/N) and inverse against the oracle."""
+def test_virtual_ranks_four_step_1d(P, m, dtype, sched, monkeypatch):
+    """The distributed four-step 1D schedule (3 transposes across the ranks,
+    natural order) as P virtual ranks (P = 1: a 1-rank NCCL communicator);
+    forward (1/N) and inverse against the oracle."""
+    _sched_env(monkeypatch, sched, P)
     b = _lib()
     n = 1 << m
     x = fixtures.complex_input(n, fixtures.NORMAL, seed=600 + m, dtype=dtype)
@@ -138,10 +149,12 @@ def test_virtual_ranks_four_step_1d(P, m, dtype):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("sched", ["fused", "exchange"])
 @pytest.mark.parametrize("P,m", [(2, 12), (4, 16), (8, 19)])
-def test_virtual_ranks_four_step_transposed_output(P, m):
+def test_virtual_ranks_four_step_transposed_output(P, m, sched, monkeypatch):
     """FFT_OUT_TRANSPOSED: rank r holds X[k2 + N2 k1] for its k2 block at
     local index (k2 - r N2/P) N1 + k1."""
+    _sched_env(monkeypatch, sched, P)
     b = _lib()
     n = 1 << m
     N1, N2 = 1 << (m - m // 2), 1 << (m // 2)
