@@ -421,6 +421,50 @@ def test_fused_peer_schedule_index_maps(P, N, M):
         assert oracle.rel_l2(out, oracle.gauss_pipeline(f, 0.1)) <= 1e-13
 
 
+def _dist_transpose(src, R, Cn, Cb):
+    """k_dist_transpose's addressing over P rank slabs (flat arrays): global
+    element (gr, gc) read from src[gr >> rsh][(gr & (R-1)) * Cn + gc],
+    written to dst[gc >> bsh][(gc & (Cb-1)) * P R + gr]."""
+    P = len(src)
+    rsh, bsh = R.bit_length() - 1, Cb.bit_length() - 1
+    Rg = P * R
+    dst = [np.zeros(Cb * Rg, dtype=complex) for _ in range(P)]
+    gr = np.arange(Rg)[:, None]
+    gc = np.arange(Cn)[None, :]
+    vals = np.stack(src)[gr >> rsh, (gr & (R - 1)) * Cn + gc]
+    d = np.broadcast_to(gc >> bsh, vals.shape)
+    off = (gc & (Cb - 1)) * Rg + gr
+    for q in range(P):
+        sel = d == q
+        dst[q][off[sel]] = vals[sel]
+    return dst
+
+
+@pytest.mark.parametrize("P,m", [(2, 6), (4, 8), (8, 9)])
+def test_fused_four_step_index_maps(P, m):
+    """CPU pin of the fused distributed four-step (run_dist_1d_fused): three
+    cross-rank transposes with the kernel's addressing around the oracle's
+    sub-FFTs and the four-step twiddle equal the oracle's 1D transform."""
+    n = 1 << m
+    N1, N2 = 1 << (m - m // 2), 1 << (m // 2)
+    S1, S2 = N1 // P, N2 // P
+    x = fixtures.complex_input(n, fixtures.NORMAL, seed=31, dtype=np.complex128)
+    slabs = [x[r * n // P:(r + 1) * n // P] for r in range(P)]
+    a = _dist_transpose(slabs, S2, N1, S1)  # rank q: [S1][N2], rows n1
+    for r in range(P):
+        A = a[r].reshape(S1, N2)
+        A = np.stack([oracle.fft(row) * N2 for row in A])
+        n1 = r * S1 + np.arange(S1)[:, None]
+        A = A * np.exp(-2j * np.pi * ((n1 * np.arange(N2)[None, :]) % n) / n)
+        a[r] = A.ravel()
+    bb = _dist_transpose(a, S1, N2, S2)  # rank q: [S2][N1], rows k2
+    for r in range(P):
+        B = bb[r].reshape(S2, N1)
+        bb[r] = (np.stack([oracle.fft(row) * N1 for row in B]) / n).ravel()
+    out = _dist_transpose(bb, S2, N1, S1)  # rank q: X[q n/P, ..)
+    assert oracle.rel_l2(np.concatenate(out), oracle.fft(x)) <= 1e-13
+
+
 # ---------------------------------------------- NEXT-2: the paper's tree
 def _branches(x, P):
     """Rank q's branch = the cyclic subsequence x[q + P j]."""
