@@ -66,6 +66,18 @@ __device__ __forceinline__ int bk_ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// wait until *p >= target: relaxed polling (no L1 invalidation per poll --
+// an acquire load invalidates the SM's L1, twiddle tables included, every
+// iteration), then one acquire fence
+__device__ __forceinline__ void bk_wait_count(const int* p, int target) {
+    int v;
+    for (;;) {
+        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+        if (v >= target) break;
+        __nanosleep(32);
+    }
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+}
 __device__ __forceinline__ void bk_red_release(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -498,7 +510,10 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
                 bk_arrive_expect(bar, (uint32_t)G::STAGE);
                 tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
             } else {
-                while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
+                if (opts & 256)
+                    bk_wait_count(ctl.done_a + b, 16);
+                else
+                    while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
                 asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 bk_arrive_expect(bar, (uint32_t)G::STAGE);
                 tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
@@ -526,8 +541,12 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
             }
             if (l0) {
                 if (!isb) {
-                    if (b >= ctl.ring)
-                        while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
+                    if (b >= ctl.ring) {
+                        if (opts & 256)
+                            bk_wait_count(ctl.done_b + (b - ctl.ring), 16);
+                        else
+                            while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
+                    }
                     tmaops::store3(&map_yst, part * 16, 0, (int)(b % ctl.ring), st, pol_keep);
                 } else {
                     bk_red_release(ctl.done_b + b, 1);  // the ring slot rows are free

@@ -507,6 +507,22 @@ size_t ab_ws_bytes(int64_t ring, int64_t batch) {
     return (size_t)ring * 65536 * sizeof(float2) + (size_t)2 * batch * sizeof(int);
 }
 
+// Grid of one task-pipeline launch.  A CTA's A task at local index k is
+// signalled (done_a) only once its producer has issued its loads up to local
+// index k + NS - 1 (or its last one), i.e. task position j + (NS - 1) grid.
+// A B load at position i waits for A parts at positions j <= i - d, so the
+// schedule is deadlock-free when every such distance d exceeds (NS - 1) grid:
+// in the steady state d >= 16 D + 1 (D is sized for it, ab_geom); with fewer
+// transforms than D every A precedes every B and d >= PP (batch - 1) + 1,
+// so the grid is capped there -- unless every CTA holds at most one task.
+int64_t ab_launch_grid(int64_t grid, int64_t batch, int64_t D, int PP, int NS) {
+    const int64_t tasks = 2 * (int64_t)PP * batch;
+    if (tasks <= grid) return tasks;
+    if (batch >= D || NS <= 1 || getenv("B200FFT_AB_NOCAP")) return grid;
+    const int64_t cap = ((int64_t)PP * (batch - 1)) / (NS - 1);  // (NS - 1) g <= PP (batch - 1) < d
+    return cap < 1 ? 1 : (cap < grid ? cap : grid);
+}
+
 template <bool INV, bool WS = false, int NSV = 3>
 cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
                      void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -545,12 +561,11 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
     }();
     int a_opts = opts;
     void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
-    const int64_t tasks = 32 * batch;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
-    cfg.gridDim = dim3((unsigned)(tasks < g.grid ? tasks : g.grid), 1, 1);
+    cfg.gridDim = dim3((unsigned)ab_launch_grid(g.grid, batch, g.D, 16, WS ? NSV : 2), 1, 1);
     cfg.blockDim = dim3(NT, 1, 1);
     cfg.dynamicSmemBytes = SMEM;
     cfg.stream = st;
@@ -617,12 +632,11 @@ cudaError_t ab8_t(const void* in, void* out, int64_t batch, double scale, const 
     }();
     int a_opts = opts;
     void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
-    const int64_t tasks = 64 * batch;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
-    cfg.gridDim = dim3((unsigned)(tasks < g.grid ? tasks : g.grid), 1, 1);
+    cfg.gridDim = dim3((unsigned)ab_launch_grid(g.grid, batch, g.D, 32, NS), 1, 1);
     cfg.blockDim = dim3(288, 1, 1);
     cfg.dynamicSmemBytes = SMEM;
     cfg.stream = st;

@@ -361,13 +361,16 @@ def test_c5_config_single_gpu_sampled(fft):
     assert float(err) <= 1e-5
 
 
-@pytest.mark.parametrize("batch", [1, 2, 5, 37, 300])
+@pytest.mark.parametrize("batch", [1, 2, 5, 20, 27, 28, 37, 300])
 @pytest.mark.parametrize("variant", ["44", "45", "46", "23"])
 def test_c2_kernel_batches_and_inplace(fft, batch, variant, monkeypatch):
-    """The 65536-point one-HBM-pass kernels (default task pipeline 44 and
-    cluster variant 23) at batch sizes that leave the persistent grid partly
-    idle or the task order without its steady A/B phase (batch < D), forward
-    and inverse, out-of-place and in place, against the oracle."""
+    """The 65536-point one-HBM-pass kernels (default task pipeline 44, the
+    8-line pipelines 45 / 46 and cluster variant 23) at batch sizes that
+    leave the persistent grid partly idle or the task order without its
+    steady A/B phase (batch < D), forward and inverse, out-of-place and in
+    place, against the oracle.  27 / 28 put a B task exactly one grid after
+    an A task it depends on (the self-wait that the small-batch grid cap of
+    kernels_cluster.cu ab_launch_grid removes: without it 44 hangs there)."""
     import paper_cs_0103001_b200 as b
 
     monkeypatch.setenv("B200FFT_CLUSTER_VARIANT", variant)
