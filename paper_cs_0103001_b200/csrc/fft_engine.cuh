@@ -216,9 +216,11 @@ struct LineFFT {
     // threads of this line through named barrier `bar` -- lines of one CTA
     // then never wait for each other.  Needs TPL % 32 == 0 (whole warps).
     __device__ __forceinline__ static void lsync(int bar) {
-        if (bar == -32) {  // a line owned by one warp
-            __syncwarp();
-            return;
+        if constexpr (TPL == 32) {
+            if (bar == -32) {  // a line owned by one warp
+                __syncwarp();
+                return;
+            }
         }
         if (bar < 0) {  // the -bar threads of a warp-specialised CTA's compute group (named barrier 1)
             asm volatile("bar.sync 1, %0;\n" ::"r"(-bar) : "memory");
