@@ -62,9 +62,11 @@ struct RowsTmaCfg {
 // so the result is L(a) + i L(b) exactly: real part = filtered a, imaginary
 // part = filtered b, stored as the float pair (a', b') -- which, with TRANS,
 // is the transposed real grid.  Half the lines, half the bytes of promoting
-// each real row to complex.
+// each real row to complex.  PAIR = 2: the same, stored as the transposed
+// COMPLEX grid (a', 0), (b', 0) -- the last pass of a real-input pipeline
+// with complex output, whose exact result is real.
 template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false, bool TRANS = false,
-          bool PAIR = false, int MINB = 1>
+          int PAIR = 0, int MINB = 1>
 __global__ void __launch_bounds__(W*(R / E), MINB)
     k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
                const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt) {
@@ -141,7 +143,15 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
             for (int it = 0; it < (W * R) / NT; ++it) {
                 const int idx = tid + it * NT;
                 const int tt = idx % W, vv = idx / W;
-                if (r0 + tt < batch) out[(int64_t)vv * batch + r0 + tt] = sg[tt * G::LS + pad16(vv)];
+                if (r0 + tt < batch) {
+                    if constexpr (PAIR == 2) {
+                        const C x = sg[tt * G::LS + pad16(vv)];
+                        reinterpret_cast<float4*>(out)[(int64_t)vv * batch + r0 + tt] =
+                            make_float4((float)x.x, 0.f, (float)x.y, 0.f);
+                    } else {
+                        out[(int64_t)vv * batch + r0 + tt] = sg[tt * G::LS + pad16(vv)];
+                    }
+                }
             }
         } else if (row < batch) {
             C* o = out + row * R + lt;

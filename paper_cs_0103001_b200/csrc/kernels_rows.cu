@@ -67,7 +67,7 @@ cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double s
 }
 
 // persistent TMA-fed variant (fft_tma.cuh): 3 stages of ~64 KiB, 512 threads
-template <typename T, int R, bool INV, bool REAL_IN, bool FILT, bool TRANS = false, bool PAIR = false, int E = 16,
+template <typename T, int R, bool INV, bool REAL_IN, bool FILT, bool TRANS = false, int PAIR = 0, int E = 16,
           int OCC = 1, int STAGE_KB = 64>
 cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw, const void* rowfilt,
                        cudaStream_t st) {
@@ -151,7 +151,7 @@ bool use_tma_rows(int prec, int64_t R, int in_sh, int out_sh) {
     return !off && prec == 0 && R >= 256 && R <= 8192 && in_sh < 0 && out_sh < 0;
 }
 
-template <bool REAL_IN, bool PAIR = false>
+template <bool REAL_IN, int PAIR = 0>
 cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw,
                                 const void* rowfilt, cudaStream_t st) {
     switch (R) {
@@ -190,8 +190,9 @@ bool rows_filter_transposed_supported(int prec, int64_t R) {
 
 cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* in, void* out, int64_t batch,
                                           double scale, const void* tw, const void* rowfilt, cudaStream_t st,
-                                          bool pair) {
-    if (pair) return rows_filter_trans_r<false, true>(R, in, out, batch, scale, tw, rowfilt, st);
+                                          int pair) {
+    if (pair == 2) return rows_filter_trans_r<false, 2>(R, in, out, batch, scale, tw, rowfilt, st);
+    if (pair) return rows_filter_trans_r<false, 1>(R, in, out, batch, scale, tw, rowfilt, st);
     return real_in ? rows_filter_trans_r<true>(R, in, out, batch, scale, tw, rowfilt, st)
                    : rows_filter_trans_r<false>(R, in, out, batch, scale, tw, rowfilt, st);
 }

@@ -39,12 +39,13 @@ cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void*
 // out[v][row] (leading dimension batch).  Two of these (rows, then the rows
 // of the transposed grid) are the whole Gaussian pipeline.
 bool rows_filter_transposed_supported(int prec, int64_t R);
-// pair = true (NEXT-3): `in` holds 2 batch real float32 rows, transformed
+// pair = 1 (NEXT-3): `in` holds 2 batch real float32 rows, transformed
 // two at a time as one complex row (a + i b); out is the transposed real
-// grid [R][2 batch] (the row filter must be real and even).
+// grid [R][2 batch] (the row filter must be real and even).  pair = 2: the
+// same, out is the transposed complex grid with zero imaginary parts.
 cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* in, void* out, int64_t batch,
                                           double scale, const void* tw, const void* rowfilt, cudaStream_t st,
-                                          bool pair = false);
+                                          int pair = 0);
 
 // Kernel family B: column transforms of nimg grids [R][S]; mode 0 fwd, 1 inv,
 // 2 fwd -> filter*scale -> inv.

@@ -320,6 +320,33 @@ def test_c3_config(fft):
     assert oracle.rel_l2(out, ref) <= 1e-5
 
 
+@pytest.mark.parametrize("realpair", ["1", "0"])
+@pytest.mark.parametrize("N,M,batch", [(2048, 2048, 1), (512, 1024, 3), (256, 2048, 2)])
+def test_real_input_complex_output_gauss(fft, N, M, batch, realpair, monkeypatch):
+    """Real input, complex output, Gaussian: by default two real rows per
+    complex line in both passes and an exactly zero imaginary part (DESIGN.md
+    R20; the oracle's imaginary part is rounding noise); with
+    B200FFT_PIPE_REALPAIR=0 the promoted complex passes.  Both against the
+    oracle's complex fp64 pipeline."""
+    import paper_cs_0103001_b200 as b
+
+    monkeypatch.setenv("B200FFT_PIPE_REALPAIR", realpair)
+    imgs = np.stack([fixtures.sky_image(N, M, seed=810 + i, nsrc=80) for i in range(batch)])
+    p = b.Plan((N, M), batch=batch, flags=b.IN_REAL_F32)
+    x = torch.from_numpy(imgs).cuda()
+    o = torch.empty((batch, N, M), dtype=torch.complex64, device="cuda")
+    p.filter_pipeline(x, o, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    assert p.last_launch_count() == 2 * batch
+    p.destroy()
+    out = o.cpu().numpy()
+    ref = np.stack([oracle.gauss_pipeline(imgs[i].astype(np.complex128), 0.1) for i in range(batch)])
+    assert oracle.rel_l2(out, ref) <= 1e-5
+    assert np.abs(ref.imag).max() <= 1e-9 * np.abs(ref.real).max()
+    if realpair == "1":
+        assert np.all(out.imag == 0)
+
+
 def test_c4_config_single_gpu(fft):
     """BASELINE configs[3] at P=1: 8192^2 complex64 U[-1,1], seed 4, same
     Gaussian; compared with the oracle over the whole grid."""
