@@ -430,8 +430,9 @@ __host__ __device__ constexpr int cols_ls() {
     return ((pad16c(R) + SL - 1) / SL) * SL + (W >= SL ? 1 : SL / W);
 }
 
-template <typename T, int R, int E, int W, int MODE>
-__global__ void __launch_bounds__(W*(R / E)) k_cols(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out,
+// MINB > 0: a register cap for MINB CTAs/SM (0: the compiler's choice)
+template <typename T, int R, int E, int W, int MODE, int MINB = 0>
+__global__ void __launch_bounds__(W*(R / E), MINB) k_cols(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out,
                                                     int64_t S, T scale, const cpx<T>* __restrict__ tw,
                                                     FilterArgs filt) {
     using C = cpx<T>;

@@ -81,14 +81,14 @@ int cols_variant() {
     return v;
 }
 
-template <typename T, int R, int MODE, int W = cols_w<T, R>(), int E = cols_e<T, R>()>
+template <typename T, int R, int MODE, int W = cols_w<T, R>(), int E = cols_e<T, R>(), int MINB = 0>
 cudaError_t cols_t(const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
                    const FilterArgs& f, cudaStream_t st) {
     constexpr int TPL = R / E;
     using F = LineFFT<T, R, E, MODE == 1>;
     constexpr size_t smem = sizeof(cpx<T>) * W * cols_ls<T, R, W>();
     static_assert(smem <= 227 * 1024, "column tile exceeds shared memory");
-    auto kern = k_cols<T, R, E, W, MODE>;
+    auto kern = k_cols<T, R, E, W, MODE, MINB>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -141,7 +141,7 @@ cudaError_t cols4_r(int64_t R, const void* in, void* out, int64_t S, int64_t nim
                     const FilterArgs& f, cudaStream_t st) {
     static const int cfg = [] {
         const char* v = getenv("B200FFT_COLS4_CFG");
-        return v ? atoi(v) : 5;  // 5: k_cols, E = 16, 16-column tiles (measured best)
+        return v ? atoi(v) : 8;  // 8: k_cols, E = 16, 16-column tiles, the 128-point pass at 9 CTAs/SM (measured best)
     }();
     if (cfg == 0) {  // per-CTA tiles (k_cols): many CTAs per SM, twiddles by recurrence
         if (R == 64) return cols_t<float, 64, MODE>(in, out, S, nimg, scale, tw, f, st);
@@ -149,6 +149,11 @@ cudaError_t cols4_r(int64_t R, const void* in, void* out, int64_t S, int64_t nim
     } else if (cfg == 5) {  // E = 16 (8 threads per 128-point line)
         if (R == 64) return cols_t<float, 64, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
         if (R == 128) return cols_t<float, 128, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
+    } else if (cfg >= 7 && cfg <= 9) {  // as 5, the 128-point pass capped at 64 / 56 / 48 registers (8 / 9 / 10 CTAs/SM)
+        if (R == 64) return cols_t<float, 64, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128 && cfg == 7) return cols_t<float, 128, MODE, 16, 16, 8>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128 && cfg == 8) return cols_t<float, 128, MODE, 16, 16, 9>(in, out, S, nimg, scale, tw, f, st);
+        if (R == 128) return cols_t<float, 128, MODE, 16, 16, 10>(in, out, S, nimg, scale, tw, f, st);
     } else if (cfg == 6) {  // E = 16, 32 columns per tile
         if (R == 64) return cols_t<float, 64, MODE, 32, 16>(in, out, S, nimg, scale, tw, f, st);
         if (R == 128) return cols_t<float, 128, MODE, 32, 16>(in, out, S, nimg, scale, tw, f, st);
