@@ -86,6 +86,12 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
     const int t = tid / F::TPL, lt = tid % F::TPL;
     const int64_t ntiles = (batch + W - 1) / W;
     const char* in = reinterpret_cast<const char*>(in_);
+    // programmatic dependent launch: when this launch overlaps the tail of
+    // the previous kernel (the second pass of a pipeline), wait for that
+    // kernel's results before the first load; let the next one launch early
+    // (both no-ops for an ordinary launch)
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     auto issue = [&](int64_t tile, int s) {
         const int64_t r0 = tile * W;

@@ -70,7 +70,7 @@ cudaError_t rows_r(int64_t R, const void* in, void* out, int64_t batch, double s
 template <typename T, int R, bool INV, bool REAL_IN, bool FILT, bool TRANS = false, int PAIR = 0, int E = 16,
           int OCC = 1, int STAGE_KB = 64>
 cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, const void* tw, const void* rowfilt,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool pdl = false) {
     constexpr int W = (int)((STAGE_KB * 1024) / (R * sizeof(cpx<T>))) < 1
                           ? 1
                           : (int)((STAGE_KB * 1024) / (R * sizeof(cpx<T>)));
@@ -92,9 +92,23 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     if (batch <= 0) return cudaSuccess;
     const int64_t tiles = (batch + W - 1) / W;
     const int grid = (int)(tiles < grid_max ? tiles : grid_max);
-    kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(in, reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
-                                                   reinterpret_cast<const cpx<T>*>(tw) + tw_base(R, ml_of(E)),
-                                                   reinterpret_cast<const T*>(rowfilt));
+    cpx<T>* a_out = reinterpret_cast<cpx<T>*>(out);
+    const cpx<T>* a_tw = reinterpret_cast<const cpx<T>*>(tw) + tw_base(R, ml_of(E));
+    const T* a_filt = reinterpret_cast<const T*>(rowfilt);
+    if (pdl) {  // may start on the SMs the previous kernel's CTAs leave (it waits for its results)
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(W * (R / E));
+        cfg.dynamicSmemBytes = G::SMEM_BYTES;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, in, a_out, batch, (T)scale, a_tw, a_filt);
+    }
+    kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(in, a_out, batch, (T)scale, a_tw, a_filt);
     return cudaGetLastError();
 }
 
@@ -153,31 +167,26 @@ bool use_tma_rows(int prec, int64_t R, int in_sh, int out_sh) {
 
 template <bool REAL_IN, int PAIR = 0>
 cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw,
-                                const void* rowfilt, cudaStream_t st) {
+                                const void* rowfilt, cudaStream_t st, bool pdl) {
     switch (R) {
         case 256:
-            return rows_tma_t<float, 256, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
+            return rows_tma_t<float, 256, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st, pdl);
         case 512:
-            return rows_tma_t<float, 512, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
+            return rows_tma_t<float, 512, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st, pdl);
         case 1024:
-            return rows_tma_t<float, 1024, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
+            return rows_tma_t<float, 1024, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st, pdl);
         case 2048:
             if (rows_e() == 8)
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 8>(in, out, batch, scale, tw, rowfilt,
-                                                                                 st);
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 8>(in, out, batch, scale, tw, rowfilt, st, pdl);
             if (rows_e() == 2)
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 2>(in, out, batch, scale, tw,
-                                                                                     rowfilt, st);
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 2>(in, out, batch, scale, tw, rowfilt, st, pdl);
             if (rows_stage_kb() == 323)  // 3 CTAs/SM x 2 stages of 32 KiB (2 rows)
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 3, 32>(in, out, batch, scale,
-                                                                                         tw, rowfilt, st);
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 3, 32>(in, out, batch, scale, tw, rowfilt, st, pdl);
             if (rows_stage_kb() == 32)  // 32 KiB stages (2 rows): two CTAs per SM
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 32>(in, out, batch, scale,
-                                                                                         tw, rowfilt, st);
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 32>(in, out, batch, scale, tw, rowfilt, st, pdl);
             if (rows_stage_kb() == 16)  // 16 KiB stages (1 row): four CTAs per SM by shared memory
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 16>(in, out, batch, scale,
-                                                                                         tw, rowfilt, st);
-            return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st);
+                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 16>(in, out, batch, scale, tw, rowfilt, st, pdl);
+            return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st, pdl);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -190,11 +199,11 @@ bool rows_filter_transposed_supported(int prec, int64_t R) {
 
 cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* in, void* out, int64_t batch,
                                           double scale, const void* tw, const void* rowfilt, cudaStream_t st,
-                                          int pair) {
-    if (pair == 2) return rows_filter_trans_r<false, 2>(R, in, out, batch, scale, tw, rowfilt, st);
-    if (pair) return rows_filter_trans_r<false, 1>(R, in, out, batch, scale, tw, rowfilt, st);
-    return real_in ? rows_filter_trans_r<true>(R, in, out, batch, scale, tw, rowfilt, st)
-                   : rows_filter_trans_r<false>(R, in, out, batch, scale, tw, rowfilt, st);
+                                          int pair, bool pdl) {
+    if (pair == 2) return rows_filter_trans_r<false, 2>(R, in, out, batch, scale, tw, rowfilt, st, pdl);
+    if (pair) return rows_filter_trans_r<false, 1>(R, in, out, batch, scale, tw, rowfilt, st, pdl);
+    return real_in ? rows_filter_trans_r<true>(R, in, out, batch, scale, tw, rowfilt, st, pdl)
+                   : rows_filter_trans_r<false>(R, in, out, batch, scale, tw, rowfilt, st, pdl);
 }
 
 cudaError_t launch_rows(int prec, bool inv, bool real_in, int64_t R, const void* in, void* out,

@@ -43,9 +43,11 @@ bool rows_filter_transposed_supported(int prec, int64_t R);
 // two at a time as one complex row (a + i b); out is the transposed real
 // grid [R][2 batch] (the row filter must be real and even).  pair = 2: the
 // same, out is the transposed complex grid with zero imaginary parts.
+// pdl: programmatic dependent launch (the second pass of a pipeline starts
+// on the SMs the first one leaves and waits for its results on the device).
 cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* in, void* out, int64_t batch,
                                           double scale, const void* tw, const void* rowfilt, cudaStream_t st,
-                                          int pair = 0);
+                                          int pair = 0, bool pdl = false);
 
 // Kernel family B: column transforms of nimg grids [R][S]; mode 0 fwd, 1 inv,
 // 2 fwd -> filter*scale -> inv.

@@ -352,6 +352,16 @@ fft_status gauss_tables(fft_plan_s* p, double param) {
     return FFT_OK;
 }
 
+// programmatic dependent launch of a pipeline's second row pass
+// (B200FFT_PDL=0 turns it off)
+bool pdl_on() {
+    static const bool on = [] {
+        const char* v = getenv("B200FFT_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 // W_N^x, x < N (fp64-generated): the twiddles of the four-step column passes
 cudaError_t ensure_twl(fft_plan_s* p, int64_t N) {
     if (p->twl_n == N) return cudaSuccess;
@@ -405,7 +415,7 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
                                               p->gv, st, true);
             if (e == cudaSuccess)
                 e = launch_rows_filter_transposed(false, N, p->ws, (char*)out + g * grid, M / 2, 1.0 / (double)N,
-                                                  p->tw, p->gu, st, true);
+                                                  p->tw, p->gu, st, 1, pdl_on());
             if (e != cudaSuccess) return cuda_fail(e, "k_rows_tma (real pairs) launch");
         }
         p->last_launches = (int)(2 * p->batch);
@@ -430,7 +440,7 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
                                               p->tw, p->gv, st, 1);
             if (e == cudaSuccess)
                 e = launch_rows_filter_transposed(false, N, p->ws, (char*)out + g * grid, M / 2, 1.0 / (double)N,
-                                                  p->tw, p->gu, st, 2);
+                                                  p->tw, p->gu, st, 2, pdl_on());
             if (e != cudaSuccess) return cuda_fail(e, "k_rows_tma (real pairs, complex out) launch");
         }
         p->last_launches = (int)(2 * p->batch);
@@ -450,7 +460,7 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
                                               p->tw, p->gv, st);
             if (e == cudaSuccess)
                 e = launch_rows_filter_transposed(false, N, p->ws, (char*)out + g * grid, M, 1.0 / (double)N, p->tw,
-                                                  p->gu, st);
+                                                  p->gu, st, 0, pdl_on());
             if (e != cudaSuccess) return cuda_fail(e, "k_rows_tma (transposed) launch");
         }
         p->last_launches = (int)(2 * p->batch);
