@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(W*(R / E), 1)
     k_cols_pipe(const cpx<T>* __restrict__ in, cpx<T>* __restrict__ out, int64_t S, int64_t nimg, T scale,
                 const cpx<T>* __restrict__ tw, FilterArgs filt) {
     using C = cpx<T>;
+    B200FFT_PDL_PROLOGUE();
     constexpr bool INV0 = (MODE == 1 || MODE == 4);
     // step twiddles: powers of one table entry for complex64 (TWREC), else
     // prefetched table entries

@@ -13,6 +13,17 @@
 
 namespace b200fft {
 
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while the
+// previous kernel on its stream is finishing; it waits here, before its first
+// global-memory access, for that kernel's results, and lets the next kernel
+// launch early.  Both instructions are no-ops for an ordinary launch.
+#define B200FFT_PDL_PROLOGUE()                                     \
+    do {                                                           \
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");       \
+        asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); \
+    } while (0)
+
 template <typename T> struct cpx_t;
 template <> struct cpx_t<float> { using type = float2; };
 template <> struct cpx_t<double> { using type = double2; };

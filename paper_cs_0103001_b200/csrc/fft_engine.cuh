@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows(const void* __restrict__ in_
                                                     const __grid_constant__ BlockPtrs ob) {
     using C = cpx<T>;
     using F = LineFFT<T, R, E, INV>;
+    B200FFT_PDL_PROLOGUE();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* smem = reinterpret_cast<C*>(smem_raw);
     const int tid = threadIdx.x;
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(W*(R / E), MINB) k_cols(const cpx<T>* __restri
                                                     int64_t S, T scale, const cpx<T>* __restrict__ tw,
                                                     FilterArgs filt) {
     using C = cpx<T>;
+    B200FFT_PDL_PROLOGUE();
     // MODE 3 / 4 / kind 6: the four-step column passes (see k_cols_pipe)
     constexpr bool INV0 = (MODE == 1 || MODE == 4);
     using F = LineFFT<T, R, E, INV0>;

@@ -90,8 +90,7 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
     // the previous kernel (the second pass of a pipeline), wait for that
     // kernel's results before the first load; let the next one launch early
     // (both no-ops for an ordinary launch)
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    B200FFT_PDL_PROLOGUE();
 
     auto issue = [&](int64_t tile, int s) {
         const int64_t r0 = tile * W;

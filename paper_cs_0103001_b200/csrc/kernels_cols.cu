@@ -35,10 +35,9 @@ cudaError_t cols_pipe_t(const void* in, void* out, int64_t S, int64_t nimg, doub
     if (S <= 0 || nimg <= 0) return cudaSuccess;
     const int64_t tiles = (S + W - 1) / W * nimg;
     const int grid = (int)(tiles < grid_max ? tiles : grid_max);
-    kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out),
-                                                   S, nimg, (float)scale,
-                                                   reinterpret_cast<const float2*>(tw) + tw_base(R), f);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(grid), dim3(W * (R / E)), G::SMEM_BYTES, st, reinterpret_cast<const float2*>(in),
+                      reinterpret_cast<float2*>(out), S, nimg, (float)scale,
+                      reinterpret_cast<const float2*>(tw) + tw_base(R), f);
 }
 
 template <int MODE>
@@ -97,9 +96,8 @@ cudaError_t cols_t(const void* in, void* out, int64_t S, int64_t nimg, double sc
     }
     if (S <= 0 || nimg <= 0) return cudaSuccess;
     dim3 grid((unsigned)((S + W - 1) / W), (unsigned)nimg);
-    kern<<<grid, W * TPL, smem, st>>>(reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<cpx<T>*>(out), S,
-                                      (T)scale, reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), f);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, dim3(W * TPL), smem, st, reinterpret_cast<const cpx<T>*>(in),
+                      reinterpret_cast<cpx<T>*>(out), S, (T)scale, reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), f);
 }
 
 template <typename T, int MODE>

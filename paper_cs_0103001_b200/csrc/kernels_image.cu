@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_image_rows_fwd(const uint8_t* __r
                                                               int64_t nrows, int64_t N, int64_t h, int64_t w,
                                                               const float2* __restrict__ tw) {
     using F = LineFFT<float, R, E, false>;
+    B200FFT_PDL_PROLOGUE();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* smem = reinterpret_cast<float2*>(smem_raw);
     const int tid = threadIdx.x;
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_image_rows_inv(const float2* __re
                                                               int64_t nrows, int64_t N, int64_t h, int64_t w,
                                                               float max_val, const float2* __restrict__ tw) {
     using F = LineFFT<float, R, E, true>;
+    B200FFT_PDL_PROLOGUE();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2* smem = reinterpret_cast<float2*>(smem_raw);
     const int tid = threadIdx.x;
@@ -118,13 +120,11 @@ cudaError_t image_rows_t(bool inv, const void* in, void* out, int64_t nrows, int
     const unsigned grid = (unsigned)((nrows + W - 1) / W);
     const float2* t = reinterpret_cast<const float2*>(tw) + tw_base(R);
     if (!inv)
-        k_image_rows_fwd<R, E, W><<<grid, W * TPL, smem, st>>>(reinterpret_cast<const uint8_t*>(in),
-                                                              reinterpret_cast<float2*>(out), nrows, N, h, w, t);
-    else
-        k_image_rows_inv<R, E, W><<<grid, W * TPL, smem, st>>>(reinterpret_cast<const float2*>(in),
-                                                              reinterpret_cast<uint8_t*>(out), nrows, N, h, w,
-                                                              (float)max_val, t);
-    return cudaGetLastError();
+        return launch_pdl(k_image_rows_fwd<R, E, W>, dim3(grid), dim3(W * TPL), smem, st,
+                          reinterpret_cast<const uint8_t*>(in), reinterpret_cast<float2*>(out), nrows, N, h, w, t);
+    return launch_pdl(k_image_rows_inv<R, E, W>, dim3(grid), dim3(W * TPL), smem, st,
+                      reinterpret_cast<const float2*>(in), reinterpret_cast<uint8_t*>(out), nrows, N, h, w,
+                      (float)max_val, t);
 }
 
 }  // namespace

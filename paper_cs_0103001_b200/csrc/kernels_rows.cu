@@ -9,6 +9,19 @@
 
 namespace b200fft {
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = getenv("B200FFT_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+bool& pdl_hint() {
+    static thread_local bool hint = false;
+    return hint;
+}
+
 namespace {
 
 template <typename T, int R, bool INV, bool REAL_IN, bool FILT>
@@ -45,10 +58,9 @@ cudaError_t rows_t(const void* in, void* out, int64_t batch, double scale, const
         !blocks(out_sh, out, obp, sizeof(cpx<T>), ob))
         return cudaErrorInvalidValue;
     const int64_t grid = (batch + W - 1) / W;
-    kern<<<(unsigned)grid, W * TPL, smem, st>>>(in, reinterpret_cast<cpx<T>*>(out), batch, (T)scale,
-                                                 reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), in_sh, out_sh,
-                                                 reinterpret_cast<const T*>(rowfilt), ib, ob);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3((unsigned)grid), dim3(W * TPL), smem, st, in, reinterpret_cast<cpx<T>*>(out), batch,
+                      (T)scale, reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), in_sh, out_sh,
+                      reinterpret_cast<const T*>(rowfilt), ib, ob);
 }
 
 template <typename T, bool INV, bool REAL_IN, bool FILT>
@@ -95,7 +107,7 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     cpx<T>* a_out = reinterpret_cast<cpx<T>*>(out);
     const cpx<T>* a_tw = reinterpret_cast<const cpx<T>*>(tw) + tw_base(R, ml_of(E));
     const T* a_filt = reinterpret_cast<const T*>(rowfilt);
-    if (pdl) {  // may start on the SMs the previous kernel's CTAs leave (it waits for its results)
+    if (pdl && pdl_enabled()) {  // may start on the SMs the previous kernel's CTAs leave (it waits for its results)
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

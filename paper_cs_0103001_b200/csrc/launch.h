@@ -19,6 +19,37 @@ struct BlockPtrs {
     void* p[kMaxBlocks];
 };
 
+// Programmatic dependent launch of the per-CTA kernels (B200FFT_PDL=0: off);
+// every such kernel starts with B200FFT_PDL_PROLOGUE (fft_common.cuh).  It
+// is applied only where it measured faster (PdlScope around those launches:
+// the image application's chain of short kernels; the C4 chain of column
+// passes measured 12% slower with it).
+bool pdl_enabled();
+bool& pdl_hint();  // thread-local: launches inside a PdlScope use PDL
+struct PdlScope {
+    bool saved;
+    PdlScope() : saved(pdl_hint()) { pdl_hint() = true; }
+    ~PdlScope() { pdl_hint() = saved; }
+};
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    if (!pdl_enabled() || !pdl_hint()) {
+        kern<<<grid, block, smem, st>>>(args...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Largest transform length handled by one CTA, per precision (0 = c64, 1 = c128).
 constexpr int64_t kRowsMax = 8192;
 constexpr int64_t kColsMax[2] = {8192, 4096};
