@@ -114,11 +114,20 @@ cudaError_t pass_r(int64_t R, const void* in, void* out, int64_t L, int64_t Ns, 
             }
         }
         // radix <= 256 passes: pipelined, 32 / 64 lines per tile (256-B / 512-B runs)
-        if (pipe != 4) {
+        if (pipe != 4 && pipe != 6 && pipe != 7) {
             switch (R) {
                 case 128: return pass_pipe_t<T, 128, 64, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
                 case 256: return pass_pipe_t<T, 256, 32, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
                 case 512: return pass_pipe_t<T, 512, 16, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                default: break;
+            }
+        }
+        if (pipe == 6 || pipe == 7) {  // per-CTA k_pass with 32 lines per tile (256-B runs); 7: 64 for radix 128
+            switch (R) {
+                case 128:
+                    if (pipe == 7) return pass_t<T, 128, INV, 64>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                    return pass_t<T, 128, INV, 32>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
+                case 256: return pass_t<T, 256, INV, 32>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
                 default: break;
             }
         }
