@@ -510,10 +510,13 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
                 bk_arrive_expect(bar, (uint32_t)G::STAGE);
                 tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
             } else {
-                if (opts & 256)
+                if (opts & 512) {
+                    // timing experiment only (WRONG results): no A -> B dependency wait
+                } else if (opts & 256) {
                     bk_wait_count(ctl.done_a + b, 16);
-                else
+                } else {
                     while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
+                }
                 asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 bk_arrive_expect(bar, (uint32_t)G::STAGE);
                 tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
@@ -541,7 +544,7 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
             }
             if (l0) {
                 if (!isb) {
-                    if (b >= ctl.ring) {
+                    if (b >= ctl.ring && !(opts & 512)) {
                         if (opts & 256)
                             bk_wait_count(ctl.done_b + (b - ctl.ring), 16);
                         else

@@ -557,7 +557,9 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
         // L2 tensor prefetch of the A tile d tasks ahead (d = 1 measured best)
         // 128: the A twiddles W_N^{n1 k2} by a 15-step product from two table
         // entries instead of 16 loads (-4.5%)
-        return v ? atoi(v) : 144;
+        const int o = v ? atoi(v) : 144;
+        // 512: drop the A -> B and ring waits (timing experiment, wrong results)
+        return (o & 512) && !getenv("B200FFT_ALLOW_WRONG") ? (o & ~512) : o;
     }();
     int a_opts = opts;
     void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
