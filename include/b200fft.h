@@ -201,17 +201,27 @@ fft_status fft_execute_host(fft_plan plan, int direction, const void* host_in, v
  *          contiguous elements per rank, all-to-all transposes);
  *  rank 2: row slabs of N/nranks rows per rank (all-to-all transposes).
  * Every rank calls every distributed entry point with identical plan
- * parameters (collective semantics, NCCL-style). */
+ * parameters (collective semantics, NCCL-style).
+ * The all-to-alls are fused into the kernels by default: on the first
+ * distributed call each rank allocates two receive slabs of its own (plan-
+ * owned, 2 x the local slab; freed at destroy), maps every other rank's by
+ * CUDA IPC (handles exchanged over the communicator; a collective decision,
+ * so either all ranks use peer memory or none), and the row / transpose
+ * kernels store into (and the final pass loads from) the other ranks' slabs
+ * directly over NVLink, with two stream-ordered NCCL barriers per transform.
+ * If any rank cannot map a peer, or B200FFT_P2P=0, the ncclSend/ncclRecv
+ * all-to-all schedule runs instead (in the caller-visible workspace). */
 fft_status fft_nccl_unique_id(unsigned char id[128]); /* on one rank; broadcast it */
 /* Collective over the nranks processes: creates the plan's own NCCL
  * communicator (ncclCommInitRank).  After it, rank-2 plans take LOCAL slabs
  * (batch x N/nranks x M elements per call); rank-1 plans keep their own
  * (local) batch and run without any collective. */
 fft_status fft_plan_set_comm(fft_plan plan, const unsigned char id[128], int nranks, int my_rank);
-/* Tests / diagnostics: run the slab-decomposed schedule of a rank-2 plan as
- * `nranks` virtual ranks on this one GPU (the all-to-alls become device
- * copies); in/out stay the whole grid.  Same kernels and layouts as the NCCL
- * path. */
+/* Tests / diagnostics: run the slab-decomposed schedule of a rank-2 plan (or
+ * the four-step of a rank-1, batch-1 plan) as `nranks` virtual ranks on this
+ * one GPU: the fused schedule with local slabs in place of peer memory
+ * (B200FFT_DIST_EXCHANGE=1: the all-to-all schedule with device copies);
+ * in/out stay the whole grid.  Same kernels and layouts as the NCCL path. */
 fft_status fft_plan_set_virtual_ranks(fft_plan plan, int nranks);
 
 fft_status fft_plan_destroy(fft_plan plan);
