@@ -851,4 +851,193 @@ __global__ void __launch_bounds__(288, MINB)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Variant 47: k_ab_ws (44) with the A tasks' Y rows stored by the compute
+// warps straight from registers (coalesced 128-B rows: the 16 columns of a
+// task are the thread-fastest index), so an A task's stage is free as soon
+// as its last exchange has been read -- the producer reloads it while the
+// compute warps are still storing.  Publication: every compute thread
+// fences its stores (fence.acq_rel.gpu) and arrives on the stage's pub
+// barrier; the producer waits for it after issuing the next load, then
+// releases done_a.  The ring-slot check moves from the A store to the A
+// load.  B tasks are unchanged (TMA box store).
+// ---------------------------------------------------------------------------
+struct AbDsCfg {
+    static constexpr int NS = 2;
+    static constexpr size_t STAGE = 16 * 256 * 8;
+    static constexpr size_t BAR_OFF = NS * STAGE;  // full[NS], comp[NS], pub[NS]
+    static constexpr size_t SMEM = BAR_OFF + 24 * NS;
+};
+
+template <bool INV>
+__global__ void __launch_bounds__(288, 3)
+    k_ab_ds(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yst,
+            const __grid_constant__ CUtensorMap map_yld, const __grid_constant__ CUtensorMap map_out, int64_t batch,
+            float scale, const float2* __restrict__ tw4, const float2* __restrict__ tw256, AbBulkCtl ctl,
+            const float2* ring, int opts) {
+    using G = AbDsCfg;
+    constexpr int NS = G::NS;
+    (void)map_yst;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t full0 = s_base + (uint32_t)G::BAR_OFF, comp0 = full0 + 8 * NS, pub0 = comp0 + 8 * NS;
+    const int tid = threadIdx.x;
+    const int64_t Dp = batch < ctl.D ? batch : ctl.D;
+    const int64_t n1t = 16 * Dp, n2t = 32 * (batch - Dp), ntasks = 32 * batch;
+
+    auto decode = [&](int64_t i, bool& isb, int64_t& b, int& part) {
+        if (i < n1t) {
+            isb = false;
+            b = i / 16;
+            part = (int)(i % 16);
+        } else if (i < n1t + n2t) {
+            const int64_t j = i - n1t, r = j % 32;
+            isb = r >= 16;
+            b = Dp + j / 32 - (isb ? Dp : 0);
+            part = (int)(r % 16);
+        } else {
+            const int64_t j = i - n1t - n2t;
+            isb = true;
+            b = batch - Dp + j / 16;
+            part = (int)(j % 16);
+        }
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            bk_mbar_init(full0 + 8 * s, 1);
+            bk_mbar_init(comp0 + 8 * s, 256);
+            bk_mbar_init(pub0 + 8 * s, 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t my_tasks = ntasks > blockIdx.x ? (ntasks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (tid >= 256) {  // ---- producer: lane 0 ----
+        if (tid != 256) return;
+        const uint64_t pol_stream = tmaops::policy_evict_first();
+        const uint64_t pol_keep = tmaops::policy_evict_last();
+        int npub[NS] = {};  // A tasks published per stage so far (pub barrier phases)
+        auto load = [&](int64_t k) {
+            bool isb;
+            int64_t b;
+            int part;
+            decode(blockIdx.x + k * gridDim.x, isb, b, part);
+            const int s = (int)(k % NS);
+            const uint32_t st = s_base + (uint32_t)(s * G::STAGE), bar = full0 + 8 * s;
+            if (!isb) {
+                // the compute warps will store this task's Y rows into the ring slot
+                if (b >= ctl.ring)
+                    while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
+                bk_arrive_expect(bar, (uint32_t)G::STAGE);
+                tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
+            } else {
+                while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                bk_arrive_expect(bar, (uint32_t)G::STAGE);
+                tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
+            }
+        };
+        // stage of task k free (A: its exchanges read; B: its X box stored)
+        auto finish = [&](int64_t k) {
+            bool isb;
+            int64_t b;
+            int part;
+            decode(blockIdx.x + k * gridDim.x, isb, b, part);
+            const int s = (int)(k % NS);
+            bk_wait(comp0 + 8 * s, (uint32_t)((k / NS) & 1));
+            if (isb) {
+                const uint32_t st = s_base + (uint32_t)(s * G::STAGE);
+                bk_red_release(ctl.done_b + b, 1);  // its ring rows were read at load
+                tmaops::store3(&map_out, part * 16, 0, (int)b, st, pol_stream);
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            }
+        };
+        // task k's Y rows globally visible: release done_a
+        auto publish = [&](int64_t k) {
+            bool isb;
+            int64_t b;
+            int part;
+            decode(blockIdx.x + k * gridDim.x, isb, b, part);
+            if (isb) return;
+            const int s = (int)(k % NS);
+            bk_wait(pub0 + 8 * s, (uint32_t)(npub[s] & 1));
+            ++npub[s];
+            bk_red_release(ctl.done_a + b, 1);
+        };
+        const int pf = (opts >> 4) & 7;
+        for (int64_t k = 0; k < my_tasks; ++k) {
+            if (k >= NS) finish(k - NS);
+            load(k);
+            if (k >= NS) publish(k - NS);
+            if (pf && k + pf < my_tasks) {
+                bool pb;
+                int64_t pbb;
+                int ppart;
+                decode(blockIdx.x + (k + pf) * gridDim.x, pb, pbb, ppart);
+                if (!pb) tmaops::prefetch3(&map_x, ppart * 16, 0, (int)pbb);
+            }
+        }
+        for (int64_t k = (my_tasks > NS ? my_tasks - NS : 0); k < my_tasks; ++k) {
+            finish(k);
+            publish(k);
+        }
+        bk_store_wait_all();
+        return;
+    }
+
+    // ---- compute warps (256 threads) ----
+    using FA = LineFFT<float, 256, 16, INV, 2, false, true>;
+    using FB = LineFFT<float, 256, 16, INV, 1, false, true>;
+    float2* yring = const_cast<float2*>(ring);
+    for (int64_t k = 0; k < my_tasks; ++k) {
+        bool isb;
+        int64_t b;
+        int part;
+        decode(blockIdx.x + k * gridDim.x, isb, b, part);
+        const int s = (int)(k % NS);
+        float2* st = reinterpret_cast<float2*>(smem_raw + s * G::STAGE);
+        float2 v[16];
+        if (!isb) {
+            const int t = tid % 16, l = tid / 16;  // line = column n1 = 16 part + t
+            const float2* tp = tw4 + (int64_t)l * 256 + part * 16 + t;
+            bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));
+            float2* line = st + t;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) v[FA::pos_in(m)] = line[FA::bpos(l, m)];
+            FA::run(v, line, l, tw256, -256);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            bk_arrive(comp0 + 8 * s);  // this thread is done with the stage
+            float2 wm = __ldg(tp);
+            const float2 ws = __ldg(tw4 + (int64_t)16 * 256 + part * 16 + t);
+            float2* y = yring + (b % ctl.ring) * 65536 + part * 16 + t;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {  // Y[k2 = l + 16 m][n1]: 16 threads = one 128-B row segment
+                y[(l + 16 * m) * 256] = cmul_dir<INV>(v[FA::pos_out(m)], wm);
+                wm = cmul(wm, ws);
+            }
+            asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+            bk_arrive(pub0 + 8 * s);
+        } else {
+            const int t = tid / 16, l = tid % 16;  // line = row k2 = 16 part + t of Y
+            bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));
+            float2* line = st + t * 256;
+#pragma unroll
+            for (int m = 0; m < 16; ++m) v[FB::pos_in(m)] = line[l + 16 * m];
+            FB::run(v, line, l, tw256, -256);
+            FB::lsync(-256);
+            char* sb = reinterpret_cast<char*>(st);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int k1 = l + 16 * m;
+                *reinterpret_cast<float2*>(sb + k1 * 128 + (((t >> 1) ^ (k1 & 7)) << 4) + ((t & 1) << 3)) =
+                    cscale(v[FB::pos_out(m)], scale);
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            bk_arrive(comp0 + 8 * s);
+        }
+    }
+}
+
 }  // namespace b200fft

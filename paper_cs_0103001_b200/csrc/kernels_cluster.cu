@@ -603,6 +603,94 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
     return cudaLaunchKernelExC(&cfg, (const void*)k, args);
 }
 
+// variant 47 (direct Y stores, fft_abbulk.cuh k_ab_ds)
+template <bool INV>
+cudaError_t ds_geom(AbGeom* g) {
+    static AbGeom cached;
+    if (!cached.grid) {
+        constexpr size_t SMEM = AbDsCfg::SMEM;
+        auto k = k_ab_ds<INV>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        int dev = 0, sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 288, SMEM);
+        if (e != cudaSuccess) return e;
+        AbGeom t;
+        t.grid = sms * (occ > 0 ? occ : 1);
+        // done_a is released one load later than in 44: waits must point
+        // (NS = 2) x grid positions back, plus margin
+        const char* dv = getenv("B200FFT_AB_D");
+        t.D = (3 * t.grid + 15) / 16 + (dv ? atoi(dv) : 8);
+        const char* rv = getenv("B200FFT_AB_RING");
+        t.ring = t.D + (rv ? atoi(rv) : 24);
+        if (getenv("B200FFT_VERBOSE"))
+            fprintf(stderr, "ab_ds: grid %d (occ %d), D %d, ring %d\n", t.grid, occ, t.D, t.ring);
+        cached = t;
+    }
+    *g = cached;
+    return cudaSuccess;
+}
+
+template <bool INV>
+cudaError_t ab_ds_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+    auto k = k_ab_ds<INV>;
+    AbGeom g;
+    cudaError_t e = ds_geom<INV>(&g);
+    if (e != cudaSuccess) return e;
+    if (batch <= 0) return cudaSuccess;
+    if (!ws || ws_bytes < ab_ws_bytes(g.ring, batch)) return cudaErrorInvalidValue;
+    void* ring = ws;
+    int* ctl = reinterpret_cast<int*>((char*)ws + (size_t)g.ring * 65536 * sizeof(float2));
+    CUtensorMap m_x, m_out, m_yst, m_yld;
+    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, 0) ||
+        !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, 128) ||
+        !encode3(&m_yst, ring, 256, 256, g.ring, 16, 256, 0) || !encode3(&m_yld, ring, 256, 256, g.ring, 256, 16, 0))
+        return cudaErrorInvalidValue;
+    e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
+    if (e != cudaSuccess) return e;
+    AbBulkCtl c{ctl, ctl + batch, g.D, g.ring};
+    float a_scale = (float)scale;
+    const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
+    const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
+    int64_t a_batch = batch;
+    const float2* a_ring = reinterpret_cast<const float2*>(ring);
+    static const int opts = [] {
+        const char* v = getenv("B200FFT_AB_OPTS");
+        return v ? atoi(v) : 16;
+    }();
+    int a_opts = opts;
+    void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_ring, &a_opts};
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3((unsigned)ab_launch_grid(g.grid, batch, g.D, 16, 3), 1, 1);
+    cfg.blockDim = dim3(288, 1, 1);
+    cfg.dynamicSmemBytes = AbDsCfg::SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static bool limit_set = false;
+    const size_t rb = (size_t)g.ring * 65536 * sizeof(float2);
+    if (!limit_set) {
+        int dev = 0, mx = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, rb < (size_t)mx ? rb : (size_t)mx);
+        limit_set = true;
+    }
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = ring;
+    attr[1].val.accessPolicyWindow.num_bytes = rb;
+    attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelExC(&cfg, (const void*)k, args);
+}
+
 template <bool INV, int NS, int MINB>
 cudaError_t ab8_t(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw, void* ws,
                   size_t ws_bytes, cudaStream_t st) {
@@ -719,6 +807,7 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
         case 44: return ab_tma_t<INV, true, 2>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 45: return ab8_t<INV, 4, 3>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 46: return ab8_t<INV, 3, 4>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
+        case 47: return ab_ds_t<INV>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
         case 29: return ab_pipe_t<float, 2, INV>(in, out, batch, scale, tw4, tw, st);
         case 30: return ab_pipe_t<float, 4, INV>(in, out, batch, scale, tw4, tw, st);
         case 22: return step_ab2_t<float, INV>(in, out, batch, scale, tw4, tw, st);
@@ -731,9 +820,10 @@ cudaError_t cluster_65536(int variant, const void* in, void* out, int64_t batch,
 }
 
 size_t cluster_workspace_bytes(int prec, int64_t n, int variant, int64_t batch) {
-    if (prec != 0 || n != 65536 || variant < 41 || variant > 46) return 0;
+    if (prec != 0 || n != 65536 || variant < 41 || variant > 47) return 0;
     AbGeom g;
-    cudaError_t e = variant == 45   ? ab8_geom<false, 4, 3>(&g)
+    cudaError_t e = variant == 47   ? ds_geom<false>(&g)
+                    : variant == 45 ? ab8_geom<false, 4, 3>(&g)
                     : variant == 46 ? ab8_geom<false, 3, 4>(&g)
                     : variant == 42 ? ab_geom<false, true>(&g)
                     : variant == 43 ? ab_geom<false, true, 6>(&g)

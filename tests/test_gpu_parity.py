@@ -389,7 +389,7 @@ def test_c5_config_single_gpu_sampled(fft):
 
 
 @pytest.mark.parametrize("batch", [1, 2, 5, 20, 27, 28, 37, 300])
-@pytest.mark.parametrize("variant", ["44", "45", "46", "23"])
+@pytest.mark.parametrize("variant", ["44", "45", "46", "47", "23"])
 def test_c2_kernel_batches_and_inplace(fft, batch, variant, monkeypatch):
     """The 65536-point one-HBM-pass kernels (default task pipeline 44, the
     8-line pipelines 45 / 46 and cluster variant 23) at batch sizes that
