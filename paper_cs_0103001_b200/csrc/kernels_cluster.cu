@@ -588,14 +588,22 @@ cudaError_t ab_tma_t(const void* in, void* out, int64_t batch, double scale, con
             int dev = 0, mx = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, rb < (size_t)mx ? rb : (size_t)mx);
+            // B200FFT_AB_PERSIST_FRAC: set-aside as a fraction of the ring (1 = all of it)
+            const char* fv = getenv("B200FFT_AB_PERSIST_FRAC");
+            const double fr = fv ? atof(fv) : 1.0;
+            const size_t want = (size_t)((double)rb * (fr > 0 ? fr : 1.0));
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want < (size_t)mx ? want : (size_t)mx);
             if (getenv("B200FFT_VERBOSE")) fprintf(stderr, "persisting L2 max %d, ring %zu\n", mx, rb);
             limit_set = true;
         }
         attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
         attr[1].val.accessPolicyWindow.base_ptr = ring;
         attr[1].val.accessPolicyWindow.num_bytes = rb;
-        attr[1].val.accessPolicyWindow.hitRatio = 1.0f;
+        static const float hit = [] {
+            const char* hv = getenv("B200FFT_AB_HIT");
+            return hv ? (float)atof(hv) : 1.0f;
+        }();
+        attr[1].val.accessPolicyWindow.hitRatio = hit;
         attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.numAttrs = 2;
