@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(288, NSV == 2 ? 3 : (NSV == 3 ? 2 : 1))
                 }
                 asm volatile("fence.proxy.async.global;\n" ::: "memory");
                 bk_arrive_expect(bar, (uint32_t)G::STAGE);
-                tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
+                tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, (opts & 1024) ? pol_stream : pol_keep);
             }
         };
         int64_t pend_a = -1;  // transform whose A store is the newest bulk group, signalled once complete
