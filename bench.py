@@ -253,10 +253,18 @@ def bench_c2(args, ws, rank, local):
             plan.execute_host(-1, out_h, back_h)
         dt = time.perf_counter() - t0
         dt = allreduce_max(ws, dt)
+        # the e2e result must be the round trip of the input (rel-L2 over the
+        # whole batch, on the device) -- else the e2e number is not reported
+        zd.copy_(back_h)
+        e2e_err = float(torch.linalg.vector_norm(zd - xd) / torch.linalg.vector_norm(xd))
+        if not e2e_err <= 1e-5:
+            raise RuntimeError(f"execute_host round trip rel-L2 {e2e_err:.3e} > 1e-5")
         e2e = {"value": round(flops_1d(n, batch * ws) * e2e_steps / dt / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": 2 * 8 * n * batch, "d2h_bytes_per_step": 2 * 8 * n * batch,
-               "steps": e2e_steps, "timer": "host wall clock around synchronous execute_host"}
-        # parity spot check of the timed buffers (first row) on the device
+               "steps": e2e_steps, "timer": "host wall clock around synchronous execute_host",
+               "roundtrip_rel_l2": e2e_err}
+        plan.inverse(yd, zd)  # restore zd for the device spot check below
+        torch.cuda.synchronize()
     err = float(torch.linalg.vector_norm(zd[:64] - xd[:64]) / torch.linalg.vector_norm(xd[:64]))
     res = {
         "metric": "FFT GFLOP/s (5N*log2N), forward(1/N)+inverse",

@@ -188,9 +188,15 @@ fft_status fft_forward_paper_tree(fft_plan plan, const void* in, void* out);
 
 /* End-to-end call on HOST buffers (pageable or pinned): copies the input
  * host->device, transforms, copies the result device->host, pipelined over
- * batch chunks on the plan's streams; returns after the result is in
- * host_out.  direction: +1 forward, -1 inverse, 0 filter pipeline with
- * (filter, param). */
+ * batch chunks (B200FFT_HOST_CHUNK_MB, default 64 MiB) on two plan-owned
+ * streams: chunk c's copies overlap chunk c - 1's compute, while the computes
+ * run one after another (they share the plan's workspace); returns after the
+ * result is in host_out.  direction: +1 forward, -1 inverse, 0 filter
+ * pipeline with (filter, param).  Ordered after the work already queued on
+ * the plan's stream.  Same results as the device-pointer calls.
+ * Errors: FFT_E_INVALID_ARG (null pointers, bad direction, pipeline on a
+ * rank-1 plan), FFT_E_UNSUPPORTED (distributed or real-output plans),
+ * FFT_E_ALLOC (the two device staging buffers per stream), FFT_E_CUDA. */
 fft_status fft_execute_host(fft_plan plan, int direction, const void* host_in, void* host_out,
                             fft_filter filter, double param);
 
@@ -208,7 +214,11 @@ fft_status fft_execute_host(fft_plan plan, int direction, const void* host_in, v
  * CUDA IPC (handles exchanged over the communicator; a collective decision,
  * so either all ranks use peer memory or none), and the row / transpose
  * kernels store into (and the final pass loads from) the other ranks' slabs
- * directly over NVLink, with two stream-ordered NCCL barriers per transform.
+ * directly over NVLink, with stream-ordered NCCL barriers between the
+ * phases (two per 2D grid; three per 1D four-step transform in natural
+ * order, two with FFT_OUT_TRANSPOSED).  Asynchronous communicator errors
+ * (ncclCommGetAsyncError) are polled after every distributed call and
+ * returned as FFT_E_NCCL.
  * If any rank cannot map a peer, or B200FFT_P2P=0, the ncclSend/ncclRecv
  * all-to-all schedule runs instead (in the caller-visible workspace). */
 fft_status fft_nccl_unique_id(unsigned char id[128]); /* on one rank; broadcast it */

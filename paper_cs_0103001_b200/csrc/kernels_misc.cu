@@ -5,7 +5,7 @@
 //                 contiguous block q), 32 x 32 tiles through padded smem,
 //                 coalesced on both sides.
 //   k_twiddle4  : Y[row][k2] *= W_N^{(row0 + row) k2} (the four-step twiddle,
-//                 step (T) of fft_cluster.cuh), W_N^x = A[x >> sh] * B[x & mask]
+//                 step (T) of fft_c2.cuh), W_N^x = A[x >> sh] * B[x & mask]
 //                 from two fp64-generated tables (x < N, no wrap).
 #include "fft_common.cuh"
 #include "launch.h"

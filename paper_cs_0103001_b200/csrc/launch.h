@@ -127,14 +127,13 @@ cudaError_t launch_image_rows(bool inv, int64_t M, const void* in, void* out, in
 cudaError_t launch_tree_combine(int prec, const void* e, const void* o, void* y, int64_t M, int64_t nb, int64_t es,
                                 int64_t ys, int64_t xstep, const void* ta, const void* tb, int sh, cudaStream_t st);
 
-// One-pass cluster FFT (fft_cluster.cuh): n = n1 * n2 in one thread-block
-// cluster per transform.  tw4: W_n^{n1 k2} laid out [k2][n1].
-bool cluster_supported(int prec, int64_t n, int* n1, int* n2);
-// Variants 41 / 42 (fft_abbulk.cuh) need caller-provided scratch of
-// cluster_workspace_bytes (the L2-resident Y ring and the task counters).
-size_t cluster_workspace_bytes(int prec, int64_t n, int variant, int64_t batch);
-cudaError_t launch_cluster(int prec, bool inv, int64_t n, const void* in, void* out, int64_t batch,
-                           double scale, const void* tw4, const void* tw, int variant, cudaStream_t st,
-                           void* ws = nullptr, size_t ws_bytes = 0);
+// One-pass 65536-point complex64 transform (fft_c2.cuh, C2): n = 256 * 256
+// four-step through an L2-resident ring.  tw4: W_n^{n1 k2} laid out
+// [k2][n1]; caller-provided scratch of c2_workspace_bytes (the ring and the
+// task counters).
+bool c2_supported(int prec, int64_t n, int* n1, int* n2);
+size_t c2_workspace_bytes(int64_t batch);
+cudaError_t launch_c2(bool inv, const void* in, void* out, int64_t batch, double scale, const void* tw4,
+                      const void* tw, void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace b200fft

@@ -135,9 +135,8 @@ struct fft_plan_s {
     std::vector<int64_t> radices;
     std::vector<void*> pa, pb;  // per pass twiddle tables [r][k_lo], [r][k_hi]
     std::vector<int> klo_sh;
-    // one-pass cluster 1D (n = cn1 * cn2): four-step twiddles [k2][n1]
+    // one-pass 65536-point 1D (fft_c2.cuh, n = cn1 * cn2): four-step twiddles [k2][n1]
     void* tw4 = nullptr;
-    int cvariant = 0;  // tuning knob (B200FFT_CLUSTER_VARIANT), see kernels_cluster.cu
     // filter tables (Gaussian)
     void* gu = nullptr;
     void* gv = nullptr;
@@ -152,6 +151,7 @@ struct fft_plan_s {
     size_t hbuf_bytes = 0;
     cudaStream_t hstream[2] = {nullptr, nullptr};
     cudaEvent_t hev = nullptr;
+    cudaEvent_t hcomp[2] = {nullptr, nullptr};  // end of a chunk's compute (fft_execute_host)
     int last_launches = 0;
     // distributed (slab decomposition of rank-2 plans)
     int nranks = 1, my_rank = 0;
@@ -163,6 +163,7 @@ struct fft_plan_s {
     void* p2p_buf = nullptr;           // this rank's 2 receive slabs (owned)
     void* peer_buf[kMaxBlocks] = {};   // rank q's p2p_buf as mapped here
     void* bar_buf = nullptr;           // 1 float: the stream-ordered barrier
+    void* ctl_buf = nullptr;           // 4 KiB for collective handshakes (allocated with the communicator)
     int64_t dist_phase = 0;            // receive slab of the next grid = phase & 1
     cudaEvent_t dev_ev = nullptr;
     // distributed four-step 1D (one transform of n = fs1 * fs2 over the ranks)
@@ -202,7 +203,7 @@ size_t workspace_need(const fft_plan_s* p) {
     if (p->dist()) return 2 * (size_t)p->elems() * p->elem_bytes();  // send + recv slabs
     if (p->rank == 2)  // the transposed grid of the Gaussian pipeline (allocated on first use)
         return (size_t)p->n0 * p->n1 * p->elem_bytes();
-    if (p->rank == 1 && p->tw4) return cluster_workspace_bytes(p->prec, p->n0, p->cvariant, p->batch);
+    if (p->rank == 1 && p->tw4) return c2_workspace_bytes(p->batch);
     if (p->rank == 1 && !p->radices.empty()) {
         size_t one = (size_t)p->elems() * p->elem_bytes();
         return p->radices.size() % 2 == 1 ? 2 * one : one;  // odd pass counts may need ws1 (run_1d)
@@ -278,14 +279,13 @@ fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream
     const double scale = p->scale_override != 0.0 ? p->scale_override : (inv ? 1.0 : 1.0 / (double)L);
     cudaError_t e;
     if (p->tw4) {
-        // one HBM pass: the cluster kernel reads each transform fully before
+        // one HBM pass: the task pipeline reads each transform fully before
         // it writes it, so out == in is safe
-        fft_status s = ensure_workspace(p);  // variants 41 / 42: the Y ring and counters
+        fft_status s = ensure_workspace(p);  // the Y ring and the task counters
         if (s != FFT_OK) return s;
-        e = launch_cluster(p->prec, inv, L, in, out, p->batch, scale, p->tw4, p->tw, p->cvariant, st, p->ws,
-                           p->ws_bytes);
+        e = launch_c2(inv, in, out, p->batch, scale, p->tw4, p->tw, p->ws, p->ws_bytes, st);
         p->last_launches = 1;
-        if (e != cudaSuccess) return cuda_fail(e, "k_cluster launch");
+        if (e != cudaSuccess) return cuda_fail(e, "k_ab_ws launch");
         return FFT_OK;
     }
     if (p->radices.empty()) {
@@ -677,11 +677,12 @@ fft_status p2p_prepare(fft_plan_s* p, cudaStream_t st) {
     if (ok && cudaIpcGetMemHandle(&mine.h, p->p2p_buf) != cudaSuccess) ok = 0;
     cudaGetLastError();
     mine.ok = ok;
-    char* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, sizeof(Rec) * (P + 1));
-    if (e != cudaSuccess) return cuda_fail(e, "p2p handle exchange buffer");
+    // the handshake buffer was allocated by fft_plan_set_comm, so no local
+    // failure can make this rank skip the all-gather the others are in
+    static_assert(sizeof(Rec) * (kMaxBlocks + 1) <= 4096, "handshake buffer");
+    char* d = (char*)p->ctl_buf;
     std::vector<Rec> all(P);
-    e = cudaMemcpyAsync(d + P * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, st);
+    cudaError_t e = cudaMemcpyAsync(d + P * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, st);
     ncclResult_t r = ncclAllGather(d + P * sizeof(Rec), d, sizeof(Rec), ncclChar, comm, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(all.data(), d, sizeof(Rec) * P, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -706,10 +707,21 @@ fft_status p2p_prepare(fft_plan_s* p, cudaStream_t st) {
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         all_ok = e == cudaSuccess && r == ncclSuccess && opened == 1;
     }
-    cudaFree(d);
     if (!all_ok) p2p_release(p);
     p->p2p = all_ok ? 1 : -1;
     if (getenv("B200FFT_VERBOSE")) fprintf(stderr, "rank %d: fused peer all-to-alls %s\n", me, all_ok ? "on" : "off");
+    return FFT_OK;
+}
+
+// asynchronous communicator errors (a failed peer, a broken connection)
+// surface here, after each distributed call's work is enqueued
+fft_status nccl_async_check(fft_plan_s* p) {
+    if (!p->comm) return FFT_OK;
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError((ncclComm_t)p->comm, &ar);
+    if (r != ncclSuccess) return fail(FFT_E_NCCL, std::string("ncclCommGetAsyncError: ") + ncclGetErrorString(r));
+    if (ar != ncclSuccess && ar != ncclInProgress)
+        return fail(FFT_E_NCCL, std::string("communicator error: ") + ncclGetErrorString(ar));
     return FFT_OK;
 }
 
@@ -888,7 +900,7 @@ fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_f
 
 // ---- distributed four-step 1D (one transform of n = N1 N2 over P ranks) ----
 // Rank r owns x[r n/P, (r+1) n/P) = rows n2 in [r S2, (r+1) S2) of the view
-// A[n2][n1] = x[n1 + N1 n2] (S2 = N2/P).  Four-step (fft_cluster.cuh):
+// A[n2][n1] = x[n1 + N1 n2] (S2 = N2/P).  Four-step (as fft_c2.cuh):
 //   (A) FFT over n2 for each n1, (T) * W_n^{n1 k2}, (B) FFT over n1 for each
 //   k2, X[k2 + N2 k1].
 // Schedule per rank: transpose (pack) -> a2a -> unpack to [S1][N2] -> (A)
@@ -900,7 +912,14 @@ fft_status fs_prepare(fft_plan_s* p) {
     const int m = ilog2(p->n0);
     const int64_t N1 = (int64_t)1 << (m - m / 2), N2 = (int64_t)1 << (m / 2);
     if (N1 % P || N2 % P) return fail(FFT_E_INVALID_SIZE, "transform too small for the rank count");
-    if (p->sub_a && p->fs1 == N1) return FFT_OK;
+    if (p->sub_a && p->fs1 == N1 && p->sub_a->batch == N1 / P && p->sub_b->batch == N2 / P) return FFT_OK;
+    // first use, or the rank count changed (fft_plan_set_virtual_ranks): rebuild
+    if (p->sub_a) fft_plan_destroy(p->sub_a);
+    if (p->sub_b) fft_plan_destroy(p->sub_b);
+    if (p->fta) cudaFree(p->fta);
+    if (p->ftb) cudaFree(p->ftb);
+    p->sub_a = p->sub_b = nullptr;
+    p->fta = p->ftb = nullptr;
     p->fs1 = N1;
     p->fs2 = N2;
     fft_precision prec = p->prec == 0 ? FFT_C64 : FFT_C128;
@@ -954,8 +973,7 @@ fft_status tree_prepare(fft_plan_s* p) {
     const int64_t n = p->n0, L = n / P;
     const int nloc = p->comm ? 1 : P;
     if (!p->tree_sub || p->tree_sub->n0 != L || p->tree_sub->batch != nloc) {
-        if (p->twl) cudaFree(p->twl);
-    if (p->tree_sub) fft_plan_destroy(p->tree_sub);
+        if (p->tree_sub) fft_plan_destroy(p->tree_sub);
         p->tree_sub = nullptr;
         int64_t d = L;
         fft_status s = fft_plan_create_ex(&p->tree_sub, &d, 1, nloc, p->prec == 0 ? FFT_C64 : FFT_C128, 0);
@@ -1088,9 +1106,12 @@ fft_status run_paper_tree(fft_plan_s* p, const void* in, void* out, cudaStream_t
 // phases: A ([S1][N2] after the first transpose) and B ([S2][N1]).  A rank
 // pushes into phase A only after the previous call's barrier 2 (all ranks
 // done with their phase-A work) and into phase B only after this call's
-// barrier 1 (all ranks done pulling from phase B in the previous call), so
-// two stream-ordered barriers per transform suffice.  Virtual ranks: one
-// launch per transpose for all P ranks, no barriers.
+// barrier 1 (all ranks done pulling from phase B in the previous call); the
+// natural-order pull of step 5 reads the peers' phase-B slabs after their
+// in-place (B) FFTs, so it follows barrier 3 -- three stream-ordered
+// barriers per transform (two with FFT_OUT_TRANSPOSED, whose step 4 reads
+// only the local slab).  Virtual ranks: one launch per transpose for all P
+// ranks, no barriers.
 fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream_t st) {
     const int P = p->P();
     const char* ex = getenv("B200FFT_DIST_EXCHANGE");
@@ -1171,6 +1192,11 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
         launches += p->sub_b->last_launches;
     }
     if (!transposed_out) {
+#ifdef B200FFT_WITH_NCCL
+        // every rank's (B) FFTs ran in place in its phase-B slab: they must
+        // all be complete before this rank pulls from the peers' slabs
+        if (p->comm && (s = dist_barrier(p, st)) != FFT_OK) return s;
+#endif
         // 5. natural order: Z [N2][N1] -> X as [N1][N2] slabs of S1 rows
         //    (rank r: rows k1 in [r S1, ..) = X[r n/P, ..)); pull own rows
         e = launch_dist_transpose(p->prec, bb, bout, S2, N1, S1, P, 0, N2, (int64_t)r0 * S1, nloc * S1, st);
@@ -1263,6 +1289,15 @@ fft_status run_dist_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaS
     return FFT_OK;
 }
 
+fft_status dist_check(fft_plan_s* p) {
+#ifdef B200FFT_WITH_NCCL
+    return nccl_async_check(p);
+#else
+    (void)p;
+    return FFT_OK;
+#endif
+}
+
 fft_status check_ptrs(fft_plan_s* p, const void* in, void* out, bool real_in) {
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (!in || !out) return fail(FFT_E_INVALID_ARG, "null data pointer");
@@ -1337,9 +1372,8 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
         return cuda_fail(e, "twiddle table upload");
     }
     int cn1 = 0, cn2 = 0;
-    const char* no_cluster = getenv("B200FFT_NO_CLUSTER");
-    if (rank == 1 && p->n0 > kRowsMax && !(no_cluster && no_cluster[0] == '1') &&
-        cluster_supported(ip, p->n0, &cn1, &cn2)) {
+    const char* no_c2 = getenv("B200FFT_NO_C2");
+    if (rank == 1 && p->n0 > kRowsMax && !(no_c2 && no_c2[0] == '1') && c2_supported(ip, p->n0, &cn1, &cn2)) {
         // W_N^{n1 k2}, [k2][n1]
         std::vector<double> t(2 * (size_t)p->n0);
         for (int64_t k2 = 0; k2 < cn2; ++k2)
@@ -1349,15 +1383,6 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
                 t[2 * (k2 * cn1 + n1)] = std::cos(ang);
                 t[2 * (k2 * cn1 + n1) + 1] = std::sin(ang);
             }
-        const char* var = getenv("B200FFT_CLUSTER_VARIANT");
-        // default 44: the warp-specialised TMA task pipeline (fft_abbulk.cuh:
-        // column / row tasks through an L2-resident ring, 3 CTAs/SM x 2
-        // in-place stages, 1.19 ms vs 1.43 ms for the best cluster variant
-        // 23, profiles/README.md); 8/9 are timing-only
-        p->cvariant = var ? atoi(var) : 44;
-        if (p->cvariant == 8 || p->cvariant == 9) p->cvariant = 44;
-        if (var && atoi(var) == 8 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 8;
-        if (var && atoi(var) == 9 && getenv("B200FFT_ALLOW_WRONG")) p->cvariant = 9;
         e = upload(t, ip, &p->tw4);
         if (e != cudaSuccess) {
             fft_plan_destroy(p);
@@ -1436,9 +1461,11 @@ static fft_status exec(fft_plan p, const void* in, void* out, bool inv) {
     if (p->elems() == 0) return FFT_OK;
     // rank 1 on several ranks: the batch is sharded (each rank's plan holds its
     // own rows), so the local schedule is the whole job -- no collective
-    if (p->rank == 1) return p->dist() ? run_dist_1d(p, in, out, inv, p->stream) : run_1d(p, in, out, inv, p->stream);
-    if (p->dist()) return run_dist_2d(p, in, out, inv ? 1 : 0, FFT_FILTER_NONE, 0.0, p->stream);
-    return run_2d(p, in, out, inv, p->stream);
+    if (p->rank == 1 && !p->dist()) return run_1d(p, in, out, inv, p->stream);
+    if (!p->dist()) return run_2d(p, in, out, inv, p->stream);
+    s = p->rank == 1 ? run_dist_1d(p, in, out, inv, p->stream)
+                     : run_dist_2d(p, in, out, inv ? 1 : 0, FFT_FILTER_NONE, 0.0, p->stream);
+    return s == FFT_OK ? dist_check(p) : s;
 }
 
 fft_status fft_forward(fft_plan p, const void* in, void* out) { return exec(p, in, out, false); }
@@ -1454,7 +1481,8 @@ fft_status fft_forward_paper_tree(fft_plan p, const void* in, void* out) {
     if (master && !out) return fail(FFT_E_INVALID_ARG, "rank 0 needs an n-element output");
     if (!aligned(in, p->elem_bytes()) || (out && !aligned(out, p->elem_bytes())))
         return fail(FFT_E_INVALID_ARG, "data pointer not aligned to the element size");
-    return run_paper_tree(p, in, master ? out : nullptr, p->stream);
+    fft_status s = run_paper_tree(p, in, master ? out : nullptr, p->stream);
+    return s == FFT_OK ? dist_check(p) : s;
 }
 fft_status fft_inverse(fft_plan p, const void* in, void* out) { return exec(p, in, out, true); }
 
@@ -1472,7 +1500,10 @@ fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filt
     if (p->elems() == 0) return FFT_OK;
     if (p->dist() && (p->flags & FFT_OUT_REAL_F32))
         return fail(FFT_E_UNSUPPORTED, "real-output pipeline on a distributed plan");
-    if (p->dist()) return run_dist_2d(p, in, out, 2, filter, param, p->stream);
+    if (p->dist()) {
+        s = run_dist_2d(p, in, out, 2, filter, param, p->stream);
+        return s == FFT_OK ? dist_check(p) : s;
+    }
     return run_pipeline(p, in, out, filter, param, p->stream);
 }
 
@@ -1575,6 +1606,7 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
         }
     if (!p->hev) {
         e = cudaEventCreateWithFlags(&p->hev, cudaEventDisableTiming);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&p->hcomp[i], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
     }
     // order after the work already queued on the plan stream
@@ -1596,6 +1628,17 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
             s = cuda_fail(e, "H2D copy");
             break;
         }
+        // the chunks' computes share the plan's workspace (the C2 ring and
+        // counters, the 2D intermediate grid, the pass ping-pong buffer):
+        // chunk c's compute starts after chunk c - 1's, on the other stream;
+        // only the copies overlap the compute
+        if (c > 0) {
+            e = cudaStreamWaitEvent(st, p->hcomp[(c - 1) & 1], 0);
+            if (e != cudaSuccess) {
+                s = cuda_fail(e, "chunk ordering");
+                break;
+            }
+        }
         p->batch = nu;
         if (direction == 0)
             s = run_pipeline(p, din, d, filter, param, st);
@@ -1604,6 +1647,11 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
         launches += p->last_launches;
         p->batch = saved_batch;
         if (s != FFT_OK) break;
+        e = cudaEventRecord(p->hcomp[c & 1], st);
+        if (e != cudaSuccess) {
+            s = cuda_fail(e, "chunk ordering");
+            break;
+        }
         e = cudaMemcpyAsync((char*)host_out + (size_t)(u0 * unit) * eb, d, (size_t)(nu * unit) * eb,
                             cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) s = cuda_fail(e, "D2H copy");
@@ -1652,6 +1700,12 @@ fft_status fft_plan_set_comm(fft_plan p, const unsigned char id[128], int nranks
     ncclComm_t comm = nullptr;
     ncclResult_t r = ncclCommInitRank(&comm, nranks, u, my_rank);
     if (r != ncclSuccess) return fail(FFT_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    cudaError_t ce = cudaMalloc(&p->ctl_buf, 4096);
+    if (ce != cudaSuccess) {
+        p->ctl_buf = nullptr;
+        ncclCommDestroy(comm);
+        return fail(FFT_E_ALLOC, std::string("communicator handshake buffer: ") + cudaGetErrorString(ce));
+    }
     p->comm = comm;
     p->nranks = nranks;
     p->my_rank = my_rank;
@@ -1688,6 +1742,7 @@ fft_status fft_plan_destroy(fft_plan p) {
     if (!p) return FFT_OK;
     cudaError_t e = cudaSuccess;
     if (p->tw4) cudaFree(p->tw4);
+    if (p->twl) cudaFree(p->twl);
     if (p->fta) cudaFree(p->fta);
     if (p->ftb) cudaFree(p->ftb);
     if (p->tree_sub) fft_plan_destroy(p->tree_sub);
@@ -1709,8 +1764,11 @@ fft_status fft_plan_destroy(fft_plan p) {
         if (p->hstream[i]) cudaStreamDestroy(p->hstream[i]);
     }
     if (p->hev) cudaEventDestroy(p->hev);
+    for (int i = 0; i < 2; ++i)
+        if (p->hcomp[i]) cudaEventDestroy(p->hcomp[i]);
 #ifdef B200FFT_WITH_NCCL
     p2p_release(p);
+    if (p->ctl_buf) cudaFree(p->ctl_buf);
     if (p->comm) ncclCommDestroy((ncclComm_t)p->comm);
 #endif
     e = cudaGetLastError();

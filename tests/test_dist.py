@@ -175,7 +175,9 @@ def test_virtual_ranks_four_step_transposed_output(P, m, sched, monkeypatch):
 @pytest.mark.gpu
 def test_virtual_ranks_c5_shape():
     """BASELINE configs[4] layout: N = 2^30 over 8 virtual ranks (32768 x
-    32768 four-step); 16 sampled bins against the oracle's direct sums."""
+    32768 four-step, the fused distributed transposes): forward on seed 5 and
+    inverse on the independent seed-105 input, each on 64 bins against the
+    oracle's direct compensated sums."""
     b = _lib()
     n = 1 << 30
     x = np.empty(n, np.complex64)
@@ -186,9 +188,16 @@ def test_virtual_ranks_c5_shape():
     yd = torch.empty_like(xd)
     p.forward(xd, yd)
     torch.cuda.synchronize()
-    bins = np.concatenate([[0, 1, n // 2, n - 1], np.random.default_rng(55).integers(0, n, 12)])
+    bins = np.concatenate([[0, 1, n // 2, n - 1], np.random.default_rng(55).integers(0, n, 60)])
     got = yd[torch.from_numpy(bins).cuda()].cpu().numpy()
     assert oracle.rel_l2(got, oracle.dft_bins(x, bins)) <= 1e-5
+    fixtures.complex_input(n, fixtures.NORMAL, seed=105, out=x)
+    xd.copy_(torch.from_numpy(x))
+    p.inverse(xd, yd)
+    torch.cuda.synchronize()
+    bins = np.concatenate([[0, 1, n // 2, n - 1], np.random.default_rng(155).integers(0, n, 60)])
+    got = yd[torch.from_numpy(bins).cuda()].cpu().numpy()
+    assert oracle.rel_l2(got, oracle.dft_bins(x, bins, inverse=True)) <= 1e-5
     p.destroy()
 
 

@@ -241,15 +241,21 @@ def spatial_gauss_pipeline(f, sigma_px, radius=40):
     return res
 
 
-@pytest.mark.parametrize("N", [64, 256, 2048])
-def test_gauss_pipeline_equals_spatial_convolution(N):
+@pytest.mark.parametrize("N,M", [(64, 64), (256, 256), (2048, 2048), (64, 256), (256, 64)])
+def test_gauss_pipeline_equals_spatial_convolution(N, M):
+    """SURVEY F3 / DESIGN.md R7: with sigma_k = 0.05 x (the axis length) per
+    axis, the pipeline is a circular convolution with the same sampled
+    Gaussian of sigma = 10/pi px along BOTH axes, whatever N and M.  The
+    rectangular cases pin the N != M branch of oracle_gauss_filter: a
+    swapped sigma_N / sigma_M (or sigma from the wrong axis length) gives a
+    4x wider / narrower spatial kernel along one axis and fails by O(1)."""
     rows = read_golden("gauss_sigma.txt")
     sigma_px = float(rows[1].split()[1])
     assert abs(sigma_px - 10 / np.pi) < 1e-15
     if N == 2048:
         f = fixtures.sky_image(2048, 2048, seed=3).astype(np.complex128)  # the C3 input
     else:
-        f = rnd(N * N).reshape(N, N)
+        f = rnd(N * M).reshape(N, M)
     got = oracle.gauss_pipeline(f, 0.1)
     ref = spatial_gauss_pipeline(f, sigma_px)
     assert oracle.rel_l2(got, ref) < 1e-12
