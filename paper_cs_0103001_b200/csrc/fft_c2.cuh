@@ -275,4 +275,181 @@ __global__ void __launch_bounds__(288, 3)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_ab_st: the same tasks and task order, with the outputs stored straight
+// from registers.  8 compute warps + 1 producer warp, MINB CTAs/SM, NS
+// stages of 32 KiB.  A stage holds its task only from the TMA load until the
+// compute warps have read their step-1 inputs: the step-0 results are
+// exchanged IN the stage (after a compute-group barrier), then the stage is
+// released (mbarrier "empty") and the producer refills it while step 1, the
+// twiddles and the stores run from registers.  So there is no output
+// staging, no store-completion wait holding a stage, and no smem traffic for
+// the outputs (32 B of smem per element and task instead of 48).
+//   A(b, p): thread (t, l) = (tid % 16, tid / 16) holds column n1 = 16p + t,
+//            elements n2 = l + 16 r (the dense [256 n2][16 n1] box); step 0
+//            (radix 16) -> exchange (element x of line t at x * 16 + t) ->
+//            step 1 -> k2 = l + 16 q; Y[k2][n1] = . * W_N^{n1 k2} * scale
+//            stored as 128-B row segments (16 adjacent t); then every
+//            compute warp makes its stores visible at gpu scope (fence) and
+//            counts itself in done_a (8 per task, 128 per transform).
+//   B(b, p): step 0 with (line r, lane l') = (tid / 16, tid % 16) on the 16
+//            dense Y rows k2 = 16p + r; exchange in the XOR layout x * 16 +
+//            (line ^ (x / 16 mod 16)), conflict-free for both mappings; step
+//            1 with (line t, lane l) = (tid % 16, tid / 16): k1 = l + 16 q;
+//            X[k2 + 256 k1] stored as 128-B segments (16 adjacent k2).
+// The scale (the paper's 1/N, a power of two: exact) is folded
+// into the A twiddle, i.e. applied to Y: bit-identical to scaling X.
+// Deadlock freedom: an A task is signalled as soon as its own stores are
+// done; no signal waits for a later load, so every wait points strictly
+// back in the global task order (no grid cap needed).
+// ---------------------------------------------------------------------------
+template <int NS_>
+struct AbStCfg {
+    static constexpr int NS = NS_;
+    static constexpr size_t STAGE = 16 * 256 * 8;
+    static constexpr size_t BAR_OFF = NS * STAGE;  // full[NS], empty[NS]
+    static constexpr size_t SMEM = BAR_OFF + 16 * NS;
+};
+
+template <bool INV>
+__device__ __forceinline__ void st_step1_twiddle(float2* v, int l, const float2* __restrict__ tw256) {
+    // step 1 of the 256-point Stockham (span 16): v[r] *= W_256^{l r}, r < 16,
+    // as powers of the one table entry W_256^l (fp32, ~15 ulp)
+    const float2 w1 = __ldg(tw256 + tw_off(256, 1, 4) + l);
+    float2 w = w1;
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+        v[r] = cmul_dir<INV>(v[r], w);
+        if (r < 15) w = cmul(w, w1);
+    }
+}
+
+template <bool INV, int NS, int MINB>
+__global__ void __launch_bounds__(288, MINB)
+    k_ab_st(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yld,
+            float2* __restrict__ ring, float2* __restrict__ out, int64_t batch, float scale,
+            const float2* __restrict__ tw4, const float2* __restrict__ tw256, AbCtl ctl, int opts) {
+    using G = AbStCfg<NS>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t full0 = s_base + (uint32_t)G::BAR_OFF, empty0 = full0 + 8 * NS;
+    const int tid = threadIdx.x;
+    const int64_t Dp = batch < ctl.D ? batch : ctl.D;
+    const int64_t ntasks = 32 * batch;
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            bk_mbar_init(full0 + 8 * s, 1);
+            bk_mbar_init(empty0 + 8 * s, 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t my_tasks = ntasks > blockIdx.x ? (ntasks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (tid >= 256) {  // ---- producer: lane 0 of warp 8 drives the TMA ----
+        if (tid != 256) return;
+        const uint64_t pol_stream = tmaops::policy_evict_first();
+        const uint64_t pol_keep = tmaops::policy_evict_last();
+        const int pf = (opts >> 4) & 7;  // L2 prefetch distance (tasks) for A tiles, 0 = off
+        for (int64_t k = 0; k < my_tasks; ++k) {
+            const int s = (int)(k % NS);
+            if (k >= NS) bk_wait(empty0 + 8 * s, (uint32_t)(((k / NS) - 1) & 1));
+            bool isb;
+            int64_t b;
+            int part;
+            ab_decode(blockIdx.x + k * gridDim.x, batch, Dp, isb, b, part);
+            const uint32_t st = s_base + (uint32_t)(s * G::STAGE), bar = full0 + 8 * s;
+            if (!isb) {
+                // the ring slot this A task's Y rows go to: its previous
+                // transform's B parts have all read theirs
+                if (b >= ctl.ring)
+                    while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
+                bk_arrive_expect(bar, (uint32_t)G::STAGE);
+                tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
+            } else {
+                while (bk_ld_acquire(ctl.done_a + b) < 128) __nanosleep(32);
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                bk_arrive_expect(bar, (uint32_t)G::STAGE);
+                tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
+            }
+            if (pf && k + pf < my_tasks) {  // warm L2 with a later A task's HBM tile
+                bool pb;
+                int64_t pbb;
+                int ppart;
+                ab_decode(blockIdx.x + (k + pf) * gridDim.x, batch, Dp, pb, pbb, ppart);
+                if (!pb) tmaops::prefetch3(&map_x, ppart * 16, 0, (int)pbb);
+            }
+        }
+        return;
+    }
+
+    // ---- compute warps (256 threads) ----
+    const int lo = tid & 15, hi = tid >> 4;
+    for (int64_t k = 0; k < my_tasks; ++k) {
+        bool isb;
+        int64_t b;
+        int part;
+        ab_decode(blockIdx.x + k * gridDim.x, batch, Dp, isb, b, part);
+        const int s = (int)(k % NS);
+        float2* st = reinterpret_cast<float2*>(smem_raw + s * G::STAGE);
+        bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));
+        float2 v[16];
+        if (!isb) {
+            // (t, l) = (lo, hi): column n1 = 16 part + t
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
+            dft<16, INV>(v);
+            asm volatile("bar.sync 1, 256;\n" ::: "memory");
+#pragma unroll
+            for (int q = 0; q < 16; ++q) st[(16 * hi + q) * 16 + lo] = v[q];
+            asm volatile("bar.sync 1, 256;\n" ::: "memory");
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
+            bk_arrive(empty0 + 8 * s);
+            st_step1_twiddle<INV>(v, hi, tw256);
+            dft<16, INV>(v);
+            // Y[k2][n1] = v[q] * W_N^{n1 k2} * scale, k2 = hi + 16 q:
+            // W_N^{n1 hi} (W_N^{16 n1})^q from two table entries
+            const int n1 = part * 16 + lo;
+            float2 wm = cscale(__ldg(tw4 + (int64_t)hi * 256 + n1), scale);
+            const float2 ws = __ldg(tw4 + (int64_t)16 * 256 + n1);
+            float2* y = ring + (b % ctl.ring) * 65536 + (int64_t)hi * 256 + n1;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                y[q * 16 * 256] = cmul_dir<INV>(v[q], wm);
+                if (q < 15) wm = cmul(wm, ws);
+            }
+            // make this warp's Y rows visible at gpu scope, then count it
+            asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+            __syncwarp();
+            if ((tid & 31) == 0) bk_red_release(ctl.done_a + b, 1);
+        } else {
+            // the stage's Y rows landed: the ring slot rows are read
+            if (tid == 0) bk_red_release(ctl.done_b + b, 1);
+            // step 0: (line r, lane l') = (hi, lo) on dense row r
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = st[hi * 256 + lo + 16 * r];
+            dft<16, INV>(v);
+            asm volatile("bar.sync 1, 256;\n" ::: "memory");
+            // element x = 16 lo + q of line hi at x * 16 + (hi ^ lo)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) st[(16 * lo + q) * 16 + (hi ^ lo)] = v[q];
+            asm volatile("bar.sync 1, 256;\n" ::: "memory");
+            // step 1: (line t, lane l) = (lo, hi): element x = hi + 16 r at
+            // x * 16 + (lo ^ r)
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + (lo ^ r)];
+            bk_arrive(empty0 + 8 * s);
+            st_step1_twiddle<INV>(v, hi, tw256);
+            dft<16, INV>(v);
+            // X[k2 + 256 k1], k2 = 16 part + lo, k1 = hi + 16 q
+            float2* x = out + b * 65536 + part * 16 + lo + (int64_t)hi * 256;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) x[q * 16 * 256] = v[q];
+        }
+    }
+}
+
 }  // namespace b200fft

@@ -4,6 +4,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 
@@ -40,9 +41,36 @@ bool encode3(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2
 // distance D (transforms) and ring slots; also whether the device's
 // persisting-L2 set-aside has been sized for the ring.  Guarded by a mutex:
 // plans on different threads / devices may launch concurrently.
+// The kernel: k_ab_ws (TMA stores from the stage) or k_ab_st (direct stores
+// from registers, NS stages, MINB CTAs/SM), B200FFT_C2 = "ws" | "st3x2" |
+// "st2x3" (read at each launch, so tests can cover every kernel).
+enum C2Kind { C2_WS = 0, C2_ST32 = 1, C2_ST23 = 2 };
+int c2_kind() {
+    const char* v = getenv("B200FFT_C2");
+    if (v && !strcmp(v, "ws")) return (int)C2_WS;
+    if (v && !strcmp(v, "st3x2")) return (int)C2_ST32;
+    if (v && !strcmp(v, "st2x3")) return (int)C2_ST23;
+    return (int)C2_WS;
+}
+const void* c2_kernel(int kind, bool inv) {
+    switch (kind) {
+        case C2_ST32: return inv ? (const void*)k_ab_st<true, 3, 2> : (const void*)k_ab_st<false, 3, 2>;
+        case C2_ST23: return inv ? (const void*)k_ab_st<true, 2, 3> : (const void*)k_ab_st<false, 2, 3>;
+        default: return inv ? (const void*)k_ab_ws<true> : (const void*)k_ab_ws<false>;
+    }
+}
+size_t c2_smem(int kind) {
+    return kind == C2_ST32 ? AbStCfg<3>::SMEM : (kind == C2_ST23 ? AbStCfg<2>::SMEM : AbWsCfg::SMEM);
+}
+
+// launch geometry per device: persistent grid per (kernel, direction), and
+// the dependency distance D (transforms) and ring slots shared by all of them
+// (one workspace size); also whether the device's persisting-L2 set-aside
+// has been sized for the ring.  Guarded by a mutex: plans on different
+// threads / devices may launch concurrently.
 struct AbGeom {
-    int grid[2] = {0, 0};  // forward, inverse
-    int D = 0, ring = 0;   // shared by both directions (one workspace size)
+    int grid[3][2] = {};  // [kind][inverse]
+    int D = 0, ring = 0;
     bool limit_set = false;
 };
 std::mutex g_geom_mu;
@@ -51,27 +79,29 @@ std::map<int, AbGeom> g_geom;
 cudaError_t ab_geom(int dev, AbGeom* g) {
     std::lock_guard<std::mutex> lk(g_geom_mu);
     AbGeom& c = g_geom[dev];
-    if (!c.grid[0]) {
+    if (!c.ring) {
         AbGeom t;
-        int sms = 0;
+        int sms = 0, gmax = 0;
         cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        for (int d = 0; d < 2 && e == cudaSuccess; ++d) {
-            const void* k = d ? (const void*)k_ab_ws<true> : (const void*)k_ab_ws<false>;
-            int occ = 0;
-            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AbWsCfg::SMEM);
-            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 288, AbWsCfg::SMEM);
-            t.grid[d] = sms * (occ > 0 ? occ : 1);
-        }
+        for (int kind = 0; kind < 3 && e == cudaSuccess; ++kind)
+            for (int d = 0; d < 2 && e == cudaSuccess; ++d) {
+                const void* k = c2_kernel(kind, d != 0);
+                int occ = 0;
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2_smem(kind));
+                if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 288, c2_smem(kind));
+                t.grid[kind][d] = sms * (occ > 0 ? occ : 1);
+                gmax = t.grid[kind][d] > gmax ? t.grid[kind][d] : gmax;
+            }
         if (e != cudaSuccess) return e;
-        const int gmax = t.grid[0] > t.grid[1] ? t.grid[0] : t.grid[1];
         // every wait must point at least (tasks in flight per CTA) x grid
-        // positions back in the task order: NS per CTA
-        t.D = (AbWsCfg::NS * gmax + 15) / 16 + 8;
+        // positions back in the task order: NS = 2 per CTA for k_ab_ws
+        t.D = (2 * gmax + 15) / 16 + 8;
         // ring = D + 24 slots: an A store waits on the B parts 24 transforms
         // (768 task positions) back, always an earlier task (24 measured best)
         t.ring = t.D + 24;
         if (getenv("B200FFT_VERBOSE"))
-            fprintf(stderr, "k_ab_ws: device %d grid %d / %d, D %d, ring %d\n", dev, t.grid[0], t.grid[1], t.D, t.ring);
+            fprintf(stderr, "c2: device %d grids ws %d st3x2 %d st2x3 %d, D %d, ring %d, kernel %d\n", dev,
+                    t.grid[0][0], t.grid[1][0], t.grid[2][0], t.D, t.ring, c2_kind());
         c = t;
     }
     *g = c;
@@ -137,6 +167,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     void* ring = ws;
     const size_t rb = (size_t)g.ring * 65536 * sizeof(float2);
     int* ctl = reinterpret_cast<int*>((char*)ws + rb);
+    const int kind = c2_kind();
     CUtensorMap m_x, m_out, m_yst, m_yld;
     if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, 0) ||
         !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, 128) ||
@@ -150,14 +181,23 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
     int64_t a_batch = batch;
     int a_opts = ab_opts();
-    void* args[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
+    float2* a_ring = reinterpret_cast<float2*>(ring);
+    float2* a_out = reinterpret_cast<float2*>(out);
+    void* args_ws[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
+    void* args_st[] = {&m_x, &m_yld, &a_ring, &a_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
+    const int grid = g.grid[kind][INV ? 1 : 0];
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
-    cfg.gridDim = dim3((unsigned)ab_launch_grid(g.grid[INV ? 1 : 0], batch, g.D, AbWsCfg::NS), 1, 1);
+    // k_ab_st signals an A task as soon as its own stores are done (no
+    // signal waits for a later load): no small-batch grid cap
+    const int64_t tasks = 32 * batch;
+    cfg.gridDim = dim3((unsigned)(kind == C2_WS ? ab_launch_grid(grid, batch, g.D, AbWsCfg::NS)
+                                                : (tasks < grid ? tasks : grid)),
+                       1, 1);
     cfg.blockDim = dim3(288, 1, 1);
-    cfg.dynamicSmemBytes = AbWsCfg::SMEM;
+    cfg.dynamicSmemBytes = c2_smem(kind);
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -179,7 +219,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
         attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.numAttrs = 2;
     }
-    return cudaLaunchKernelExC(&cfg, (const void*)k_ab_ws<INV>, args);
+    return cudaLaunchKernelExC(&cfg, c2_kernel(kind, INV), kind == C2_WS ? args_ws : args_st);
 }
 
 }  // namespace

@@ -418,8 +418,10 @@ def test_c5_config_single_gpu_sampled(fft):
 
 
 @pytest.mark.parametrize("batch", [1, 2, 5, 20, 27, 28, 37, 300])
-def test_c2_kernel_batches_and_inplace(fft, batch):
-    """The 65536-point one-HBM-pass task pipeline (fft_c2.cuh) at batch
+@pytest.mark.parametrize("kernel", ["ws", "st2x3", "st3x2"])
+def test_c2_kernel_batches_and_inplace(fft, batch, kernel, monkeypatch):
+    """The 65536-point one-HBM-pass task pipelines (fft_c2.cuh: k_ab_ws and
+    k_ab_st in both stage configurations) at batch
     sizes that leave the persistent grid partly idle or the task order
     without its steady A/B phase (batch < D), forward and inverse,
     out-of-place and in place, against the oracle.  27 / 28 put a B task
@@ -428,6 +430,7 @@ def test_c2_kernel_batches_and_inplace(fft, batch):
     the kernel hangs there)."""
     import paper_cs_0103001_b200 as b
 
+    monkeypatch.setenv("B200FFT_C2", kernel)
     n = 65536
     x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=900 + batch).reshape(batch, n)
     p = b.Plan((n,), batch=batch)
