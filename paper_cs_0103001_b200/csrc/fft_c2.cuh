@@ -25,9 +25,10 @@
 namespace b200fft {
 
 struct AbCtl {
-    int* done_a;  // [batch] A parts of transform b whose Y rows are in the ring
-    int* done_b;  // [batch] B parts of transform b that have read their Y rows
-    int D, ring;  // dependency distance (transforms), ring slots
+    int* done_a;                    // [batch] A parts of transform b whose Y rows are in the ring
+    int* done_b;                    // [batch] B parts of transform b that have read their Y rows
+    unsigned long long* next;       // next task position to take (k_ab_st)
+    int D, ring;                    // dependency distance (transforms), ring slots
 };
 
 // ---- mbarrier / bulk-copy / TMA primitives (sm_90+ PTX) ------------------
@@ -277,22 +278,20 @@ __global__ void __launch_bounds__(288, 3)
 
 
 // ---------------------------------------------------------------------------
-// k_ab_st: the same tasks and task order, with the outputs stored straight
-// from registers.  8 compute warps + 1 producer warp, MINB CTAs/SM, NS
-// stages of 32 KiB.  A stage holds its task only from the TMA load until the
-// compute warps have read their step-1 inputs: the step-0 results are
-// exchanged IN the stage (after a compute-group barrier), then the stage is
-// released (mbarrier "empty") and the producer refills it while step 1, the
-// twiddles and the stores run from registers.  So there is no output
-// staging, no store-completion wait holding a stage, and no smem traffic for
-// the outputs (32 B of smem per element and task instead of 48).
+// k_ab_st: the same tasks, with the outputs stored straight from registers
+// and the tasks handed out dynamically.  Per CTA: 8 compute warps, a
+// producer (warp 8, lane 0), a signaller (warp 9, lane 0); NS stages of
+// 32 KiB.  A stage holds its task only from the TMA load until the compute
+// warps have read their step-1 inputs: the step-0 results are exchanged IN
+// the stage (after a compute-group barrier), then the stage is released
+// (mbarrier "empty") and the producer refills it while step 1, the twiddles
+// and the stores run from registers -- no output staging, no store
+// completion holding a stage, 32 B of smem traffic per element and task.
 //   A(b, p): thread (t, l) = (tid % 16, tid / 16) holds column n1 = 16p + t,
 //            elements n2 = l + 16 r (the dense [256 n2][16 n1] box); step 0
 //            (radix 16) -> exchange (element x of line t at x * 16 + t) ->
 //            step 1 -> k2 = l + 16 q; Y[k2][n1] = . * W_N^{n1 k2} * scale
-//            stored as 128-B row segments (16 adjacent t); then every
-//            compute warp makes its stores visible at gpu scope (fence) and
-//            counts itself in done_a (8 per task, 128 per transform).
+//            stored as 128-B row segments (16 adjacent t).
 //   B(b, p): step 0 with (line r, lane l') = (tid / 16, tid % 16) on the 16
 //            dense Y rows k2 = 16p + r; exchange in the XOR layout x * 16 +
 //            (line ^ (x / 16 mod 16)), conflict-free for both mappings; step
@@ -300,16 +299,25 @@ __global__ void __launch_bounds__(288, 3)
 //            X[k2 + 256 k1] stored as 128-B segments (16 adjacent k2).
 // The scale (the paper's 1/N, a power of two: exact) is folded
 // into the A twiddle, i.e. applied to Y: bit-identical to scaling X.
-// Deadlock freedom: an A task is signalled as soon as its own stores are
-// done; no signal waits for a later load, so every wait points strictly
-// back in the global task order (no grid cap needed).
+// Signals: after an A task's Y stores every compute thread arrives on a
+// signal mbarrier (release, CTA scope); the signaller waits on it (acquire),
+// makes the stores visible at gpu scope (fence.acq_rel.gpu, cumulative) and
+// counts the task in done_a -- one fence per task, off the compute warps.
+// Scheduling: the producer takes the next position of the global task order
+// from an atomic counter (no static round robin: CTAs that run slower take
+// fewer tasks, so no transform's B parts wait on a straggler's A part).
+// Deadlock freedom: every wait (a B load on done_a, an A load on its ring
+// slot's done_b, a signal slot) points at tasks taken earlier, and no signal
+// waits for a later load; all CTAs are co-resident (cooperative launch).
 // ---------------------------------------------------------------------------
 template <int NS_>
 struct AbStCfg {
     static constexpr int NS = NS_;
+    static constexpr int NSIG = 4;  // A tasks a CTA may have computed but not yet signalled
     static constexpr size_t STAGE = 16 * 256 * 8;
-    static constexpr size_t BAR_OFF = NS * STAGE;  // full[NS], empty[NS]
-    static constexpr size_t SMEM = BAR_OFF + 16 * NS;
+    static constexpr size_t BAR_OFF = NS * STAGE;                       // full[NS], empty[NS], sig[NSIG]
+    static constexpr size_t INFO_OFF = BAR_OFF + 8 * (2 * NS + NSIG);   // task[NS], sigb[NSIG] (int64), sigdone
+    static constexpr size_t SMEM = INFO_OFF + 8 * (NS + NSIG) + 16;
 };
 
 template <bool INV>
@@ -326,14 +334,18 @@ __device__ __forceinline__ void st_step1_twiddle(float2* v, int l, const float2*
 }
 
 template <bool INV, int NS, int MINB>
-__global__ void __launch_bounds__(288, MINB)
+__global__ void __launch_bounds__(320, MINB)
     k_ab_st(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yld,
             float2* __restrict__ ring, float2* __restrict__ out, int64_t batch, float scale,
             const float2* __restrict__ tw4, const float2* __restrict__ tw256, AbCtl ctl, int opts) {
     using G = AbStCfg<NS>;
+    constexpr int NSIG = G::NSIG;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t full0 = s_base + (uint32_t)G::BAR_OFF, empty0 = full0 + 8 * NS;
+    const uint32_t full0 = s_base + (uint32_t)G::BAR_OFF, empty0 = full0 + 8 * NS, sig0 = empty0 + 8 * NS;
+    volatile int64_t* task = reinterpret_cast<volatile int64_t*>(smem_raw + G::INFO_OFF);
+    volatile int64_t* sigb = task + NS;
+    volatile int* sigdone = reinterpret_cast<volatile int*>(sigb + NSIG);
     const int tid = threadIdx.x;
     const int64_t Dp = batch < ctl.D ? batch : ctl.D;
     const int64_t ntasks = 32 * batch;
@@ -343,43 +355,60 @@ __global__ void __launch_bounds__(288, MINB)
             bk_mbar_init(full0 + 8 * s, 1);
             bk_mbar_init(empty0 + 8 * s, 256);
         }
+        for (int j = 0; j < NSIG; ++j) bk_mbar_init(sig0 + 8 * j, 256);
+        *sigdone = 0;
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const int64_t my_tasks = ntasks > blockIdx.x ? (ntasks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-    if (tid >= 256) {  // ---- producer: lane 0 of warp 8 drives the TMA ----
-        if (tid != 256) return;
-        const uint64_t pol_stream = tmaops::policy_evict_first();
-        const uint64_t pol_keep = tmaops::policy_evict_last();
-        const int pf = (opts >> 4) & 7;  // L2 prefetch distance (tasks) for A tiles, 0 = off
-        for (int64_t k = 0; k < my_tasks; ++k) {
-            const int s = (int)(k % NS);
-            if (k >= NS) bk_wait(empty0 + 8 * s, (uint32_t)(((k / NS) - 1) & 1));
-            bool isb;
-            int64_t b;
-            int part;
-            ab_decode(blockIdx.x + k * gridDim.x, batch, Dp, isb, b, part);
-            const uint32_t st = s_base + (uint32_t)(s * G::STAGE), bar = full0 + 8 * s;
-            if (!isb) {
-                // the ring slot this A task's Y rows go to: its previous
-                // transform's B parts have all read theirs
-                if (b >= ctl.ring)
-                    while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
-                bk_arrive_expect(bar, (uint32_t)G::STAGE);
-                tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
-            } else {
-                while (bk_ld_acquire(ctl.done_a + b) < 128) __nanosleep(32);
-                asm volatile("fence.proxy.async.global;\n" ::: "memory");
-                bk_arrive_expect(bar, (uint32_t)G::STAGE);
-                tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
+    if (tid >= 256) {
+        const int lane = tid & 31;
+        if (lane != 0) return;
+        if (tid < 288) {  // ---- producer ----
+            const uint64_t pol_stream = tmaops::policy_evict_first();
+            const uint64_t pol_keep = tmaops::policy_evict_last();
+            int na = 0;  // A tasks issued by this CTA
+            for (int64_t k = 0;; ++k) {
+                const int s = (int)(k % NS);
+                if (k >= NS) bk_wait(empty0 + 8 * s, (uint32_t)(((k / NS) - 1) & 1));
+                const int64_t i = (int64_t)atomicAdd(ctl.next, 1ull);
+                task[s] = i;
+                const uint32_t st = s_base + (uint32_t)(s * G::STAGE), bar = full0 + 8 * s;
+                if (i >= ntasks) {  // no more work: the compute warps exit on this stage
+                    bk_arrive(bar);
+                    break;
+                }
+                bool isb;
+                int64_t b;
+                int part;
+                ab_decode(i, batch, Dp, isb, b, part);
+                if (!isb) {
+                    // a free signal slot for this A task (the signaller is at most
+                    // NSIG A tasks behind the compute warps)
+                    while (*sigdone < na - NSIG + 1) __nanosleep(20);
+                    ++na;
+                    // the ring slot's previous transform: all its B parts have read it
+                    if (b >= ctl.ring)
+                        while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
+                    bk_arrive_expect(bar, (uint32_t)G::STAGE);
+                    tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
+                } else {
+                    while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
+                    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+                    bk_arrive_expect(bar, (uint32_t)G::STAGE);
+                    tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
+                }
             }
-            if (pf && k + pf < my_tasks) {  // warm L2 with a later A task's HBM tile
-                bool pb;
-                int64_t pbb;
-                int ppart;
-                ab_decode(blockIdx.x + (k + pf) * gridDim.x, batch, Dp, pb, pbb, ppart);
-                if (!pb) tmaops::prefetch3(&map_x, ppart * 16, 0, (int)pbb);
+        } else {  // ---- signaller ----
+            for (int j = 0;; ++j) {
+                bk_wait(sig0 + 8 * (j % NSIG), (uint32_t)((j / NSIG) & 1));
+                const int64_t b = sigb[j % NSIG];
+                if (b < 0) break;
+                // the compute threads' Y stores (ordered before their arrive)
+                // made visible at gpu scope, then counted
+                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+                asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;\n" ::"l"(ctl.done_a + b) : "memory");
+                *sigdone = j + 1;
             }
         }
         return;
@@ -387,14 +416,17 @@ __global__ void __launch_bounds__(288, MINB)
 
     // ---- compute warps (256 threads) ----
     const int lo = tid & 15, hi = tid >> 4;
-    for (int64_t k = 0; k < my_tasks; ++k) {
-        bool isb;
-        int64_t b;
-        int part;
-        ab_decode(blockIdx.x + k * gridDim.x, batch, Dp, isb, b, part);
+    int ja = 0;  // A tasks computed by this CTA
+    for (int64_t k = 0;; ++k) {
         const int s = (int)(k % NS);
         float2* st = reinterpret_cast<float2*>(smem_raw + s * G::STAGE);
         bk_wait(full0 + 8 * s, (uint32_t)((k / NS) & 1));
+        const int64_t i = task[s];
+        if (i >= ntasks) break;
+        bool isb;
+        int64_t b;
+        int part;
+        ab_decode(i, batch, Dp, isb, b, part);
         float2 v[16];
         if (!isb) {
             // (t, l) = (lo, hi): column n1 = 16 part + t
@@ -421,13 +453,13 @@ __global__ void __launch_bounds__(288, MINB)
                 y[q * 16 * 256] = cmul_dir<INV>(v[q], wm);
                 if (q < 15) wm = cmul(wm, ws);
             }
-            // make this warp's Y rows visible at gpu scope, then count it
-            asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-            __syncwarp();
-            if ((tid & 31) == 0) bk_red_release(ctl.done_a + b, 1);
+            if (tid == 0) sigb[ja % NSIG] = b;
+            bk_arrive(sig0 + 8 * (ja % NSIG));  // release: this thread's Y stores
+            ++ja;
         } else {
-            // the stage's Y rows landed: the ring slot rows are read
-            if (tid == 0) bk_red_release(ctl.done_b + b, 1);
+            // the stage's Y rows landed (the TMA read is complete): the ring
+            // slot's rows are free for the next transform
+            if (tid == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;\n" ::"l"(ctl.done_b + b) : "memory");
             // step 0: (line r, lane l') = (hi, lo) on dense row r
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = st[hi * 256 + lo + 16 * r];
@@ -450,6 +482,13 @@ __global__ void __launch_bounds__(288, MINB)
             for (int q = 0; q < 16; ++q) x[q * 16 * 256] = v[q];
         }
     }
+    // done: tell the signaller (once its slot is free)
+    if (tid == 0) {
+        while (*sigdone < ja - NSIG + 1) __nanosleep(20);
+        sigb[ja % NSIG] = -1;
+    }
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    bk_arrive(sig0 + 8 * (ja % NSIG));
 }
 
 }  // namespace b200fft

@@ -59,6 +59,7 @@ const void* c2_kernel(int kind, bool inv) {
         default: return inv ? (const void*)k_ab_ws<true> : (const void*)k_ab_ws<false>;
     }
 }
+int c2_threads(int kind) { return kind == C2_WS ? 288 : 320; }
 size_t c2_smem(int kind) {
     return kind == C2_ST32 ? AbStCfg<3>::SMEM : (kind == C2_ST23 ? AbStCfg<2>::SMEM : AbWsCfg::SMEM);
 }
@@ -88,7 +89,8 @@ cudaError_t ab_geom(int dev, AbGeom* g) {
                 const void* k = c2_kernel(kind, d != 0);
                 int occ = 0;
                 e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2_smem(kind));
-                if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 288, c2_smem(kind));
+                if (e == cudaSuccess)
+                    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c2_threads(kind), c2_smem(kind));
                 t.grid[kind][d] = sms * (occ > 0 ? occ : 1);
                 gmax = t.grid[kind][d] > gmax ? t.grid[kind][d] : gmax;
             }
@@ -123,7 +125,7 @@ void ab_persist_limit(int dev, size_t ring_bytes) {
 
 // caller-provided scratch: the Y ring (ring x 512 KiB) then the counters
 size_t ab_ws_bytes(int64_t ring, int64_t batch) {
-    return (size_t)ring * 65536 * sizeof(float2) + (size_t)2 * batch * sizeof(int);
+    return (size_t)ring * 65536 * sizeof(float2) + (size_t)2 * batch * sizeof(int) + 16;
 }
 
 // Grid of one launch.  A CTA's A task at local index k is signalled
@@ -173,9 +175,13 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
         !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, 128) ||
         !encode3(&m_yst, ring, 256, 256, g.ring, 16, 256, 0) || !encode3(&m_yld, ring, 256, 256, g.ring, 256, 16, 0))
         return cudaErrorInvalidValue;
-    e = cudaMemsetAsync(ctl, 0, sizeof(int) * 2 * batch, st);
+    // counters: done_a[batch], done_b[batch], then the 8-B task counter
+    // (8-B aligned: 2 batch ints after the 512 KiB-aligned ring, padded)
+    unsigned long long* next =
+        reinterpret_cast<unsigned long long*>((char*)ctl + ((sizeof(int) * 2 * batch + 7) & ~(size_t)7));
+    e = cudaMemsetAsync(ctl, 0, ((sizeof(int) * 2 * batch + 7) & ~(size_t)7) + 8, st);
     if (e != cudaSuccess) return e;
-    AbCtl c{ctl, ctl + batch, g.D, g.ring};
+    AbCtl c{ctl, ctl + batch, next, g.D, g.ring};
     float a_scale = (float)scale;
     const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
     const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
@@ -196,7 +202,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     cfg.gridDim = dim3((unsigned)(kind == C2_WS ? ab_launch_grid(grid, batch, g.D, AbWsCfg::NS)
                                                 : (tasks < grid ? tasks : grid)),
                        1, 1);
-    cfg.blockDim = dim3(288, 1, 1);
+    cfg.blockDim = dim3(c2_threads(kind), 1, 1);
     cfg.dynamicSmemBytes = c2_smem(kind);
     cfg.stream = st;
     cfg.attrs = attr;
