@@ -320,20 +320,27 @@ struct AbStCfg {
     static constexpr size_t SMEM = INFO_OFF + 8 * (NS + NSIG) + 16;
 };
 
-template <bool INV>
+template <bool INV, bool TABLE>
 __device__ __forceinline__ void st_step1_twiddle(float2* v, int l, const float2* __restrict__ tw256) {
-    // step 1 of the 256-point Stockham (span 16): v[r] *= W_256^{l r}, r < 16,
-    // as powers of the one table entry W_256^l (fp32, ~15 ulp)
-    const float2 w1 = __ldg(tw256 + tw_off(256, 1, 4) + l);
-    float2 w = w1;
+    // step 1 of the 256-point Stockham (span 16): v[r] *= W_256^{l r}, r < 16.
+    // TABLE: the step-major table's entries [r - 1][l] (fp64-generated, L1-
+    // resident: 240 values); else powers of the one entry W_256^l (fp32, ~15
+    // ulp, 2 more FP instructions per twiddle)
+    if constexpr (TABLE) {
 #pragma unroll
-    for (int r = 1; r < 16; ++r) {
-        v[r] = cmul_dir<INV>(v[r], w);
-        if (r < 15) w = cmul(w, w1);
+        for (int r = 1; r < 16; ++r) v[r] = cmul_dir<INV>(v[r], __ldg(tw256 + tw_off(256, 1, 4) + (r - 1) * 16 + l));
+    } else {
+        const float2 w1 = __ldg(tw256 + tw_off(256, 1, 4) + l);
+        float2 w = w1;
+#pragma unroll
+        for (int r = 1; r < 16; ++r) {
+            v[r] = cmul_dir<INV>(v[r], w);
+            if (r < 15) w = cmul(w, w1);
+        }
     }
 }
 
-template <bool INV, int NS, int MINB>
+template <bool INV, int NS, int MINB, int TW = 0>
 __global__ void __launch_bounds__(320, MINB)
     k_ab_st(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yld,
             float2* __restrict__ ring, float2* __restrict__ out, int64_t batch, float scale,
@@ -440,18 +447,25 @@ __global__ void __launch_bounds__(320, MINB)
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
             bk_arrive(empty0 + 8 * s);
-            st_step1_twiddle<INV>(v, hi, tw256);
+            st_step1_twiddle<INV, (TW & 1) != 0>(v, hi, tw256);
             dft<16, INV>(v);
             // Y[k2][n1] = v[q] * W_N^{n1 k2} * scale, k2 = hi + 16 q:
             // W_N^{n1 hi} (W_N^{16 n1})^q from two table entries
             const int n1 = part * 16 + lo;
-            float2 wm = cscale(__ldg(tw4 + (int64_t)hi * 256 + n1), scale);
-            const float2 ws = __ldg(tw4 + (int64_t)16 * 256 + n1);
             float2* y = ring + (b % ctl.ring) * 65536 + (int64_t)hi * 256 + n1;
+            if constexpr ((TW & 2) != 0) {
+                // W_N^{n1 k2} straight from the [k2][n1] table (L2-resident)
+                const float2* tp = tw4 + (int64_t)hi * 256 + n1;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                y[q * 16 * 256] = cmul_dir<INV>(v[q], wm);
-                if (q < 15) wm = cmul(wm, ws);
+                for (int q = 0; q < 16; ++q) y[q * 16 * 256] = cscale(cmul_dir<INV>(v[q], __ldg(tp + q * 16 * 256)), scale);
+            } else {
+                float2 wm = cscale(__ldg(tw4 + (int64_t)hi * 256 + n1), scale);
+                const float2 ws = __ldg(tw4 + (int64_t)16 * 256 + n1);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    y[q * 16 * 256] = cmul_dir<INV>(v[q], wm);
+                    if (q < 15) wm = cmul(wm, ws);
+                }
             }
             if (tid == 0) sigb[ja % NSIG] = b;
             bk_arrive(sig0 + 8 * (ja % NSIG));  // release: this thread's Y stores
@@ -474,7 +488,7 @@ __global__ void __launch_bounds__(320, MINB)
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + (lo ^ r)];
             bk_arrive(empty0 + 8 * s);
-            st_step1_twiddle<INV>(v, hi, tw256);
+            st_step1_twiddle<INV, (TW & 1) != 0>(v, hi, tw256);
             dft<16, INV>(v);
             // X[k2 + 256 k1], k2 = 16 part + lo, k1 = hi + 16 q
             float2* x = out + b * 65536 + part * 16 + lo + (int64_t)hi * 256;

@@ -42,27 +42,27 @@ bool encode3(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2
 // persisting-L2 set-aside has been sized for the ring.  Guarded by a mutex:
 // plans on different threads / devices may launch concurrently.
 // The kernel: k_ab_ws (TMA stores from the stage) or k_ab_st (direct stores
-// from registers, NS stages, MINB CTAs/SM), B200FFT_C2 = "ws" | "st3x2" |
-// "st2x3" (read at each launch, so tests can cover every kernel).
-enum C2Kind { C2_WS = 0, C2_ST32 = 1, C2_ST23 = 2 };
+// from registers, 2 stages, 3 CTAs/SM; TW: twiddle tables), B200FFT_C2 = "ws" | "st"
+// (default) | "st_t1" | "st_t3" (read at each launch, so tests can cover every kernel).
+enum C2Kind { C2_WS = 0, C2_ST = 1, C2_ST_T1 = 2, C2_ST_T3 = 3, C2_NKIND = 4 };
 int c2_kind() {
     const char* v = getenv("B200FFT_C2");
     if (v && !strcmp(v, "ws")) return (int)C2_WS;
-    if (v && !strcmp(v, "st3x2")) return (int)C2_ST32;
-    if (v && !strcmp(v, "st2x3")) return (int)C2_ST23;
-    return (int)C2_WS;
+    if (v && !strcmp(v, "st")) return (int)C2_ST;
+    if (v && !strcmp(v, "st_t1")) return (int)C2_ST_T1;
+    if (v && !strcmp(v, "st_t3")) return (int)C2_ST_T3;
+    return (int)C2_ST;
 }
 const void* c2_kernel(int kind, bool inv) {
     switch (kind) {
-        case C2_ST32: return inv ? (const void*)k_ab_st<true, 3, 2> : (const void*)k_ab_st<false, 3, 2>;
-        case C2_ST23: return inv ? (const void*)k_ab_st<true, 2, 3> : (const void*)k_ab_st<false, 2, 3>;
+        case C2_ST: return inv ? (const void*)k_ab_st<true, 2, 3, 0> : (const void*)k_ab_st<false, 2, 3, 0>;
+        case C2_ST_T1: return inv ? (const void*)k_ab_st<true, 2, 3, 1> : (const void*)k_ab_st<false, 2, 3, 1>;
+        case C2_ST_T3: return inv ? (const void*)k_ab_st<true, 2, 3, 3> : (const void*)k_ab_st<false, 2, 3, 3>;
         default: return inv ? (const void*)k_ab_ws<true> : (const void*)k_ab_ws<false>;
     }
 }
 int c2_threads(int kind) { return kind == C2_WS ? 288 : 320; }
-size_t c2_smem(int kind) {
-    return kind == C2_ST32 ? AbStCfg<3>::SMEM : (kind == C2_ST23 ? AbStCfg<2>::SMEM : AbWsCfg::SMEM);
-}
+size_t c2_smem(int kind) { return kind == C2_WS ? AbWsCfg::SMEM : AbStCfg<2>::SMEM; }
 
 // launch geometry per device: persistent grid per (kernel, direction), and
 // the dependency distance D (transforms) and ring slots shared by all of them
@@ -70,7 +70,7 @@ size_t c2_smem(int kind) {
 // has been sized for the ring.  Guarded by a mutex: plans on different
 // threads / devices may launch concurrently.
 struct AbGeom {
-    int grid[3][2] = {};  // [kind][inverse]
+    int grid[C2_NKIND][2] = {};  // [kind][inverse]
     int D = 0, ring = 0;
     bool limit_set = false;
 };
@@ -84,7 +84,7 @@ cudaError_t ab_geom(int dev, AbGeom* g) {
         AbGeom t;
         int sms = 0, gmax = 0;
         cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        for (int kind = 0; kind < 3 && e == cudaSuccess; ++kind)
+        for (int kind = 0; kind < C2_NKIND && e == cudaSuccess; ++kind)
             for (int d = 0; d < 2 && e == cudaSuccess; ++d) {
                 const void* k = c2_kernel(kind, d != 0);
                 int occ = 0;
@@ -97,13 +97,19 @@ cudaError_t ab_geom(int dev, AbGeom* g) {
         if (e != cudaSuccess) return e;
         // every wait must point at least (tasks in flight per CTA) x grid
         // positions back in the task order: NS = 2 per CTA for k_ab_ws
-        t.D = (2 * gmax + 15) / 16 + 8;
-        // ring = D + 24 slots: an A store waits on the B parts 24 transforms
-        // (768 task positions) back, always an earlier task (24 measured best)
-        t.ring = t.D + 24;
+        // (B200FFT_AB_D / B200FFT_AB_RING: tuning knobs for the margins)
+        const char* dv = getenv("B200FFT_AB_D");
+        const char* rv = getenv("B200FFT_AB_RING");
+        t.D = (2 * gmax + 15) / 16 + (dv ? atoi(dv) : 8);
+        // ring = D + 40 slots: an A load waits on the B parts 40 transforms
+        // (1280 task positions) back, always an earlier task and beyond the
+        // ~900 positions in flight (D + 8 / 24 / 40 / 56: 1.17 / 1.007 / 0.968
+        // / 0.971 ms; rings above ~110 slots (55 MB) exceed the persisting L2
+        // set-aside and spill: 1.26 ms)
+        t.ring = t.D + (rv ? atoi(rv) : 40);
         if (getenv("B200FFT_VERBOSE"))
-            fprintf(stderr, "c2: device %d grids ws %d st3x2 %d st2x3 %d, D %d, ring %d, kernel %d\n", dev,
-                    t.grid[0][0], t.grid[1][0], t.grid[2][0], t.D, t.ring, c2_kind());
+            fprintf(stderr, "c2: device %d grids ws %d st %d, D %d, ring %d, kernel %d\n", dev, t.grid[0][0],
+                    t.grid[1][0], t.D, t.ring, c2_kind());
         c = t;
     }
     *g = c;

@@ -1,5 +1,5 @@
 """Time the C2 kernel (4096 x 65536 complex64, forward + inverse) for the
-kernel named by B200FFT_C2 (read once per process), with a parity spot
+kernel named by B200FFT_C2, with a parity spot
 check of 64 rows against the oracle.  Usage: python scripts/time_c2.py [reps]"""
 import os
 import sys
