@@ -320,27 +320,80 @@ struct AbStCfg {
     static constexpr size_t SMEM = INFO_OFF + 8 * (NS + NSIG) + 16;
 };
 
-template <bool INV, bool TABLE>
+template <bool INV>
 __device__ __forceinline__ void st_step1_twiddle(float2* v, int l, const float2* __restrict__ tw256) {
-    // step 1 of the 256-point Stockham (span 16): v[r] *= W_256^{l r}, r < 16.
-    // TABLE: the step-major table's entries [r - 1][l] (fp64-generated, L1-
-    // resident: 240 values); else powers of the one entry W_256^l (fp32, ~15
-    // ulp, 2 more FP instructions per twiddle)
-    if constexpr (TABLE) {
+    // step 1 of the 256-point Stockham (span 16): v[r] *= W_256^{l r}, r < 16,
+    // as powers of the one step-major table entry W_256^l (fp32, ~15 ulp;
+    // loading the 15 entries instead measured 1% slower, a four-chain product
+    // 0.6% slower)
+    const float2 w1 = __ldg(tw256 + tw_off(256, 1, 4) + l);
+    float2 w = w1;
 #pragma unroll
-        for (int r = 1; r < 16; ++r) v[r] = cmul_dir<INV>(v[r], __ldg(tw256 + tw_off(256, 1, 4) + (r - 1) * 16 + l));
-    } else {
-        const float2 w1 = __ldg(tw256 + tw_off(256, 1, 4) + l);
-        float2 w = w1;
-#pragma unroll
-        for (int r = 1; r < 16; ++r) {
-            v[r] = cmul_dir<INV>(v[r], w);
-            if (r < 15) w = cmul(w, w1);
-        }
+    for (int r = 1; r < 16; ++r) {
+        v[r] = cmul_dir<INV>(v[r], w);
+        if (r < 15) w = cmul(w, w1);
     }
 }
 
-template <bool INV, int NS, int MINB, int TW = 0>
+// ---------------------------------------------------------------------------
+// The two task bodies of k_ab_st, for one compute group of 256 threads (lo, hi) = (tid % 16,
+// tid / 16) on the stage st; `bar` is the group's named barrier.  Each
+// releases the stage (arrive on `empty`) as soon as its step-1 inputs are in
+// registers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void grp_sync(int bar) { asm volatile("bar.sync %0, 256;\n" ::"r"(bar) : "memory"); }
+
+template <bool INV>
+__device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, uint32_t empty, int part, float2* y0,
+                                          float scale, const float2* __restrict__ tw4,
+                                          const float2* __restrict__ tw256) {
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
+    dft<16, INV>(v);
+    grp_sync(bar);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) st[(16 * hi + q) * 16 + lo] = v[q];
+    grp_sync(bar);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
+    bk_arrive(empty);
+    st_step1_twiddle<INV>(v, hi, tw256);
+    dft<16, INV>(v);
+    // Y[k2][n1] = v[q] * W_N^{n1 k2} * scale, k2 = hi + 16 q
+    const int n1 = part * 16 + lo;
+    float2 wm = cscale(__ldg(tw4 + (int64_t)hi * 256 + n1), scale);
+    const float2 ws = __ldg(tw4 + (int64_t)16 * 256 + n1);
+    float2* y = y0 + (int64_t)hi * 256 + n1;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        y[q * 16 * 256] = cmul_dir<INV>(v[q], wm);
+        if (q < 15) wm = cmul(wm, ws);
+    }
+}
+
+template <bool INV>
+__device__ __forceinline__ void st_task_b(float2* st, int lo, int hi, int bar, uint32_t empty, float2* x0,
+                                          const float2* __restrict__ tw256) {
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = st[hi * 256 + lo + 16 * r];
+    dft<16, INV>(v);
+    grp_sync(bar);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) st[(16 * lo + q) * 16 + (hi ^ lo)] = v[q];
+    grp_sync(bar);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + (lo ^ r)];
+    bk_arrive(empty);
+    st_step1_twiddle<INV>(v, hi, tw256);
+    dft<16, INV>(v);
+    float2* x = x0 + lo + (int64_t)hi * 256;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q * 16 * 256] = v[q];
+}
+
+template <bool INV, int NS, int MINB>
 __global__ void __launch_bounds__(320, MINB)
     k_ab_st(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yld,
             float2* __restrict__ ring, float2* __restrict__ out, int64_t batch, float scale,
@@ -375,10 +428,28 @@ __global__ void __launch_bounds__(320, MINB)
             const uint64_t pol_stream = tmaops::policy_evict_first();
             const uint64_t pol_keep = tmaops::policy_evict_last();
             int na = 0;  // A tasks issued by this CTA
+            // opts bit 0: take the next position (atomic) right after issuing a
+            // load, so its round trip overlaps the wait for the next stage;
+            // bit 1: poll the dependency counters relaxed (no L1 invalidation
+            // per poll), one acquire once satisfied
+            const bool early = (opts & 1) != 0, relaxed = (opts & 2) != 0;
+            int64_t inext = early ? (int64_t)atomicAdd(ctl.next, 1ull) : 0;
+            auto wait_count = [&](const int* p, int target) {
+                if (relaxed) {
+                    int v;
+                    for (;;) {
+                        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+                        if (v >= target) break;
+                        __nanosleep(32);
+                    }
+                } else {
+                    while (bk_ld_acquire(p) < target) __nanosleep(32);
+                }
+            };
             for (int64_t k = 0;; ++k) {
                 const int s = (int)(k % NS);
                 if (k >= NS) bk_wait(empty0 + 8 * s, (uint32_t)(((k / NS) - 1) & 1));
-                const int64_t i = (int64_t)atomicAdd(ctl.next, 1ull);
+                const int64_t i = early ? inext : (int64_t)atomicAdd(ctl.next, 1ull);
                 task[s] = i;
                 const uint32_t st = s_base + (uint32_t)(s * G::STAGE), bar = full0 + 8 * s;
                 if (i >= ntasks) {  // no more work: the compute warps exit on this stage
@@ -395,15 +466,28 @@ __global__ void __launch_bounds__(320, MINB)
                     while (*sigdone < na - NSIG + 1) __nanosleep(20);
                     ++na;
                     // the ring slot's previous transform: all its B parts have read it
-                    if (b >= ctl.ring)
-                        while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
+                    if (b >= ctl.ring) wait_count(ctl.done_b + (b - ctl.ring), 16);
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
                 } else {
-                    while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
+                    wait_count(ctl.done_a + b, 16);
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
+                }
+                if (early) inext = (int64_t)atomicAdd(ctl.next, 1ull);
+                // opts bits 4..6 = d: warm L2 with the A tile of position i + 128 d
+                // (whichever CTA takes it: positions are taken in order)
+                const int pf = (opts >> 4) & 7;
+                if (pf) {
+                    bool pb;
+                    int64_t pbb;
+                    int ppart;
+                    const int64_t ip = i + 128 * pf;
+                    if (ip < ntasks) {
+                        ab_decode(ip, batch, Dp, pb, pbb, ppart);
+                        if (!pb) tmaops::prefetch3(&map_x, ppart * 16, 0, (int)pbb);
+                    }
                 }
             }
         } else {  // ---- signaller ----
@@ -421,7 +505,7 @@ __global__ void __launch_bounds__(320, MINB)
         return;
     }
 
-    // ---- compute warps (256 threads) ----
+    // ---- compute warps (256 threads, named barrier 1) ----
     const int lo = tid & 15, hi = tid >> 4;
     int ja = 0;  // A tasks computed by this CTA
     for (int64_t k = 0;; ++k) {
@@ -434,39 +518,8 @@ __global__ void __launch_bounds__(320, MINB)
         int64_t b;
         int part;
         ab_decode(i, batch, Dp, isb, b, part);
-        float2 v[16];
         if (!isb) {
-            // (t, l) = (lo, hi): column n1 = 16 part + t
-#pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
-            dft<16, INV>(v);
-            asm volatile("bar.sync 1, 256;\n" ::: "memory");
-#pragma unroll
-            for (int q = 0; q < 16; ++q) st[(16 * hi + q) * 16 + lo] = v[q];
-            asm volatile("bar.sync 1, 256;\n" ::: "memory");
-#pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
-            bk_arrive(empty0 + 8 * s);
-            st_step1_twiddle<INV, (TW & 1) != 0>(v, hi, tw256);
-            dft<16, INV>(v);
-            // Y[k2][n1] = v[q] * W_N^{n1 k2} * scale, k2 = hi + 16 q:
-            // W_N^{n1 hi} (W_N^{16 n1})^q from two table entries
-            const int n1 = part * 16 + lo;
-            float2* y = ring + (b % ctl.ring) * 65536 + (int64_t)hi * 256 + n1;
-            if constexpr ((TW & 2) != 0) {
-                // W_N^{n1 k2} straight from the [k2][n1] table (L2-resident)
-                const float2* tp = tw4 + (int64_t)hi * 256 + n1;
-#pragma unroll
-                for (int q = 0; q < 16; ++q) y[q * 16 * 256] = cscale(cmul_dir<INV>(v[q], __ldg(tp + q * 16 * 256)), scale);
-            } else {
-                float2 wm = cscale(__ldg(tw4 + (int64_t)hi * 256 + n1), scale);
-                const float2 ws = __ldg(tw4 + (int64_t)16 * 256 + n1);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    y[q * 16 * 256] = cmul_dir<INV>(v[q], wm);
-                    if (q < 15) wm = cmul(wm, ws);
-                }
-            }
+            st_task_a<INV>(st, lo, hi, 1, empty0 + 8 * s, part, ring + (b % ctl.ring) * 65536, scale, tw4, tw256);
             if (tid == 0) sigb[ja % NSIG] = b;
             bk_arrive(sig0 + 8 * (ja % NSIG));  // release: this thread's Y stores
             ++ja;
@@ -474,26 +527,7 @@ __global__ void __launch_bounds__(320, MINB)
             // the stage's Y rows landed (the TMA read is complete): the ring
             // slot's rows are free for the next transform
             if (tid == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;\n" ::"l"(ctl.done_b + b) : "memory");
-            // step 0: (line r, lane l') = (hi, lo) on dense row r
-#pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = st[hi * 256 + lo + 16 * r];
-            dft<16, INV>(v);
-            asm volatile("bar.sync 1, 256;\n" ::: "memory");
-            // element x = 16 lo + q of line hi at x * 16 + (hi ^ lo)
-#pragma unroll
-            for (int q = 0; q < 16; ++q) st[(16 * lo + q) * 16 + (hi ^ lo)] = v[q];
-            asm volatile("bar.sync 1, 256;\n" ::: "memory");
-            // step 1: (line t, lane l) = (lo, hi): element x = hi + 16 r at
-            // x * 16 + (lo ^ r)
-#pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + (lo ^ r)];
-            bk_arrive(empty0 + 8 * s);
-            st_step1_twiddle<INV, (TW & 1) != 0>(v, hi, tw256);
-            dft<16, INV>(v);
-            // X[k2 + 256 k1], k2 = 16 part + lo, k1 = hi + 16 q
-            float2* x = out + b * 65536 + part * 16 + lo + (int64_t)hi * 256;
-#pragma unroll
-            for (int q = 0; q < 16; ++q) x[q * 16 * 256] = v[q];
+            st_task_b<INV>(st, lo, hi, 1, empty0 + 8 * s, out + b * 65536 + part * 16, tw256);
         }
     }
     // done: tell the signaller (once its slot is free)
@@ -501,8 +535,9 @@ __global__ void __launch_bounds__(320, MINB)
         while (*sigdone < ja - NSIG + 1) __nanosleep(20);
         sigb[ja % NSIG] = -1;
     }
-    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    grp_sync(1);
     bk_arrive(sig0 + 8 * (ja % NSIG));
 }
+
 
 }  // namespace b200fft

@@ -41,25 +41,19 @@ bool encode3(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d2
 // distance D (transforms) and ring slots; also whether the device's
 // persisting-L2 set-aside has been sized for the ring.  Guarded by a mutex:
 // plans on different threads / devices may launch concurrently.
-// The kernel: k_ab_ws (TMA stores from the stage) or k_ab_st (direct stores
-// from registers, 2 stages, 3 CTAs/SM; TW: twiddle tables), B200FFT_C2 = "ws" | "st"
-// (default) | "st_t1" | "st_t3" (read at each launch, so tests can cover every kernel).
-enum C2Kind { C2_WS = 0, C2_ST = 1, C2_ST_T1 = 2, C2_ST_T3 = 3, C2_NKIND = 4 };
+// The kernel: k_ab_st (default: direct stores from registers, 2 stages,
+// 3 CTAs/SM, dynamic task order) or k_ab_ws (the round-1 kernel: TMA stores
+// from the stage, static order), B200FFT_C2 = "st" | "ws" (read at each
+// launch, so the tests cover both).
+enum C2Kind { C2_WS = 0, C2_ST = 1, C2_NKIND = 2 };
 int c2_kind() {
     const char* v = getenv("B200FFT_C2");
     if (v && !strcmp(v, "ws")) return (int)C2_WS;
-    if (v && !strcmp(v, "st")) return (int)C2_ST;
-    if (v && !strcmp(v, "st_t1")) return (int)C2_ST_T1;
-    if (v && !strcmp(v, "st_t3")) return (int)C2_ST_T3;
     return (int)C2_ST;
 }
 const void* c2_kernel(int kind, bool inv) {
-    switch (kind) {
-        case C2_ST: return inv ? (const void*)k_ab_st<true, 2, 3, 0> : (const void*)k_ab_st<false, 2, 3, 0>;
-        case C2_ST_T1: return inv ? (const void*)k_ab_st<true, 2, 3, 1> : (const void*)k_ab_st<false, 2, 3, 1>;
-        case C2_ST_T3: return inv ? (const void*)k_ab_st<true, 2, 3, 3> : (const void*)k_ab_st<false, 2, 3, 3>;
-        default: return inv ? (const void*)k_ab_ws<true> : (const void*)k_ab_ws<false>;
-    }
+    if (kind == C2_ST) return inv ? (const void*)k_ab_st<true, 2, 3> : (const void*)k_ab_st<false, 2, 3>;
+    return inv ? (const void*)k_ab_ws<true> : (const void*)k_ab_ws<false>;
 }
 int c2_threads(int kind) { return kind == C2_WS ? 288 : 320; }
 size_t c2_smem(int kind) { return kind == C2_WS ? AbWsCfg::SMEM : AbStCfg<2>::SMEM; }
@@ -150,15 +144,17 @@ int64_t ab_launch_grid(int64_t grid, int64_t batch, int64_t D, int NS) {
     return cap < 1 ? 1 : (cap < grid ? cap : grid);
 }
 
-int ab_opts() {
-    static const int o = [] {
-        // bits 4..6: L2 tensor prefetch of the A tile d tasks ahead (d = 1
-        // measured best, -1.3%); bit 7: A twiddles by a 15-step product from
-        // two table entries instead of 16 loads (-4.5%)
-        const char* v = getenv("B200FFT_AB_OPTS");
-        return v ? atoi(v) : (128 | 16);
-    }();
-    return o;
+// tuning bits (B200FFT_AB_OPTS; defaults = the measured best):
+//   k_ab_ws: bits 4..6 = L2 tensor prefetch of the A tile d tasks ahead (d = 1:
+//            -1.3%); bit 7 = A twiddles by a 15-step product from two table
+//            entries instead of 16 loads (-4.5%).  Default 144.
+//   k_ab_st: bit 0 = take the next position before the stage is free (+4%),
+//            bit 1 = relaxed dependency polling (+-0), bits 4..6 = L2 prefetch
+//            of the A tile 128 d positions ahead (+1.5%).  Default 0.
+int ab_opts(int kind) {
+    const char* v = getenv("B200FFT_AB_OPTS");
+    if (v) return atoi(v);
+    return kind == C2_WS ? (128 | 16) : 0;
 }
 
 template <bool INV>
@@ -192,7 +188,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
     const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
     int64_t a_batch = batch;
-    int a_opts = ab_opts();
+    int a_opts = ab_opts(kind);
     float2* a_ring = reinterpret_cast<float2*>(ring);
     float2* a_out = reinterpret_cast<float2*>(out);
     void* args_ws[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
