@@ -244,6 +244,19 @@ const char* fft_last_error(void); /* thread-local detail of the last failure */
 int fft_plan_last_launch_count(fft_plan plan);
 const char* fft_build_info(void);
 
+/* Diagnostics: per-phase device timing.  With on != 0, each later call of
+ * fft_forward / fft_inverse / fft2d_filter_pipeline records CUDA events on
+ * the plan's stream between its phases -- for a distributed plan each
+ * exchange (peer stores / loads or all-to-all), compute step and barrier
+ * (the NVLink-exchange timing of the sharded configs, BASELINE north_star);
+ * for a single-GPU call one phase.  fft_plan_phase_times waits for the last
+ * call's final event, writes up to `max` phase durations in ms to `ms` and
+ * their labels, ';'-separated and NUL-terminated, to `labels` (may be NULL),
+ * and returns the number of phases (0 when profiling is off or no call ran).
+ * Profiling adds one event record per phase; it is off by default. */
+fft_status fft_plan_set_profiling(fft_plan plan, int on);
+int fft_plan_phase_times(fft_plan plan, float* ms, int max, char* labels, size_t labels_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,7 @@ EXPORTS = [
     "fft_execute_host", "fft_nccl_unique_id", "fft_plan_set_comm", "fft_plan_set_virtual_ranks",
     "fft_plan_destroy",
     "fft_status_string", "fft_last_error", "fft_plan_last_launch_count", "fft_build_info",
+    "fft_plan_set_profiling", "fft_plan_phase_times",
 ]
 
 
@@ -81,6 +82,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fft_last_error": ([], ctypes.c_char_p),
         "fft_plan_last_launch_count": ([vp], ci),
         "fft_build_info": ([], ctypes.c_char_p),
+        "fft_plan_set_profiling": ([vp, ci], ci),
+        "fft_plan_phase_times": ([vp, ctypes.POINTER(ctypes.c_float), ci, ctypes.c_char_p, sz], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -192,6 +195,18 @@ class Plan:
         """Tests: emulate the slab decomposition over ``nranks`` virtual ranks on this GPU."""
         _check(load_library().fft_plan_set_virtual_ranks(self._h, int(nranks)),
                "fft_plan_set_virtual_ranks")
+
+    def set_profiling(self, on: bool = True) -> None:
+        """Per-phase CUDA-event timing of later calls (fft_plan_set_profiling)."""
+        _check(load_library().fft_plan_set_profiling(self._h, int(bool(on))), "fft_plan_set_profiling")
+
+    def phase_times(self, max_phases: int = 32):
+        """[(label, ms), ...] of the last call's phases (waits for it)."""
+        ms = (ctypes.c_float * max_phases)()
+        buf = ctypes.create_string_buffer(4096)
+        n = load_library().fft_plan_phase_times(self._h, ms, max_phases, buf, 4096)
+        labels = buf.value.decode().split(";") if n else []
+        return [(labels[k] if k < len(labels) else "", float(ms[k])) for k in range(n)]
 
     def last_launch_count(self) -> int:
         return int(load_library().fft_plan_last_launch_count(self._h))

@@ -185,6 +185,13 @@ struct fft_plan_s {
     void* tws = nullptr;             // tree buffers (owned)
     size_t tws_bytes = 0;
 
+    // per-phase device timing (fft_plan_set_profiling): event k marks the end
+    // of phase k - 1 of the last call
+    bool prof = false;
+    std::vector<cudaEvent_t> pev;
+    std::vector<std::string> plab;
+    int pn = 0;
+
     size_t elem_bytes() const { return prec == 0 ? 8 : 16; }
     int P() const { return comm ? nranks : virt; }
     // slab-decomposed schedule: a communicator (any size, 1 included) or virtual ranks
@@ -198,6 +205,29 @@ struct fft_plan_s {
 };
 
 namespace {
+
+// phase marks of the profiling mode (no-ops otherwise): prof_begin at the
+// start of a call, prof_mark(label) after each phase, on the call's stream
+void prof_mark(fft_plan_s* p, cudaStream_t st, const char* label) {
+    if (!p->prof) return;
+    if ((int)p->pev.size() <= p->pn) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) {
+            p->prof = false;
+            return;
+        }
+        p->pev.push_back(e);
+        p->plab.emplace_back();
+    }
+    cudaEventRecord(p->pev[p->pn], st);
+    if (p->pn > 0 && label) p->plab[p->pn - 1] = label;
+    ++p->pn;
+}
+void prof_begin(fft_plan_s* p, cudaStream_t st) {
+    if (!p->prof) return;
+    p->pn = 0;
+    prof_mark(p, st, nullptr);
+}
 
 size_t workspace_need(const fft_plan_s* p) {
     if (p->dist()) return 2 * (size_t)p->elems() * p->elem_bytes();  // send + recv slabs
@@ -782,10 +812,12 @@ fft_status run_dist_2d_fused(fft_plan_s* p, const void* in, void* out, int mode,
             if (e != cudaSuccess) return cuda_fail(e, "k_rows (peer-store) launch");
             ++launches;
         }
+        prof_mark(p, st, "rows+exchange(peer stores)");
 #ifdef B200FFT_WITH_NCCL
         if (p->comm) {
             fft_status s = dist_barrier(p, st);
             if (s != FFT_OK) return s;
+            prof_mark(p, st, "barrier");
         }
 #endif
         // 2. columns (length N) of every local column slab [N][SM], in place
@@ -793,10 +825,12 @@ fft_status run_dist_2d_fused(fft_plan_s* p, const void* in, void* out, int mode,
             e = dist_columns(p, rslab(r0 + l), mode, f, (int64_t)(r0 + l) * SM, SM, st, &launches);
             if (e != cudaSuccess) return cuda_fail(e, "column step launch");
         }
+        prof_mark(p, st, "columns");
 #ifdef B200FFT_WITH_NCCL
         if (p->comm) {
             fft_status s = dist_barrier(p, st);
             if (s != FFT_OK) return s;
+            prof_mark(p, st, "barrier");
         }
 #endif
         // 3. rows of every local slab, block q loaded from rank q's column slab
@@ -815,6 +849,7 @@ fft_status run_dist_2d_fused(fft_plan_s* p, const void* in, void* out, int mode,
             }
             if (e != cudaSuccess) return cuda_fail(e, "final row pass / unblock (peer loads)");
         }
+        prof_mark(p, st, mode == 2 ? "exchange(peer loads)+rows" : "exchange(peer loads)");
     }
     p->last_launches = launches;
     return FFT_OK;
@@ -867,15 +902,19 @@ fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_f
             if (e != cudaSuccess) return cuda_fail(e, "k_rows launch");
             ++launches;
         }
+        prof_mark(p, st, "rows");
         s = dist_exchange(p, ws0, ws1, blk, st);
         if (s != FFT_OK) return s;
+        prof_mark(p, st, "exchange(all-to-all)");
         // 2. columns (length N) of every local column slab [N][SM]
         for (int l = 0; l < nloc; ++l) {
             e = dist_columns(p, ws1 + (size_t)l * slab * eb, mode, f, (int64_t)(r0 + l) * SM, SM, st, &launches);
             if (e != cudaSuccess) return cuda_fail(e, "column step launch");
         }
+        prof_mark(p, st, "columns");
         s = dist_exchange(p, ws1, ws0, blk, st);
         if (s != FFT_OK) return s;
+        prof_mark(p, st, "exchange(all-to-all)");
         // 3. back to natural row slabs
         for (int l = 0; l < nloc; ++l) {
             const char* src = ws0 + (size_t)l * slab * eb;
@@ -893,6 +932,7 @@ fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_f
             }
             if (e != cudaSuccess) return cuda_fail(e, "unblock");
         }
+        prof_mark(p, st, mode == 2 ? "rows" : "unblock");
     }
     p->last_launches = launches;
     return FFT_OK;
@@ -1160,8 +1200,12 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
     e = launch_dist_transpose(p->prec, bin, ba, S2, N1, S1, P, (int64_t)r0 * S2, nloc * S2, 0, N1, st);
     if (e != cudaSuccess) return cuda_fail(e, "distributed transpose 1");
     ++launches;
+    prof_mark(p, st, "exchange 1 (transpose, peer stores)");
 #ifdef B200FFT_WITH_NCCL
-    if (p->comm && (s = dist_barrier(p, st)) != FFT_OK) return s;
+    if (p->comm) {
+        if ((s = dist_barrier(p, st)) != FFT_OK) return s;
+        prof_mark(p, st, "barrier");
+    }
 #endif
     // 2. (A) FFT over n2 (unnormalised) and (T) the four-step twiddle
     for (int l = 0; l < nloc; ++l) {
@@ -1173,12 +1217,17 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
         if (e != cudaSuccess) return cuda_fail(e, "twiddle");
         ++launches;
     }
+    prof_mark(p, st, "FFT over n2 + twiddle");
     // 3. phase A [N1][N2] (rows n1) -> phase B [N2][N1] slabs of S2 rows; push
     e = launch_dist_transpose(p->prec, ba, bb, S1, N2, S2, P, (int64_t)r0 * S1, nloc * S1, 0, N2, st);
     if (e != cudaSuccess) return cuda_fail(e, "distributed transpose 2");
     ++launches;
+    prof_mark(p, st, "exchange 2 (transpose, peer stores)");
 #ifdef B200FFT_WITH_NCCL
-    if (p->comm && (s = dist_barrier(p, st)) != FFT_OK) return s;
+    if (p->comm) {
+        if ((s = dist_barrier(p, st)) != FFT_OK) return s;
+        prof_mark(p, st, "barrier");
+    }
 #endif
     // 4. (B) FFT over n1 with the paper's 1/n (forward): Z[k2][k1] = X[k2 + N2 k1]
     const bool transposed_out = !inv && (p->flags & FFT_OUT_TRANSPOSED);
@@ -1191,17 +1240,22 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
         if (s != FFT_OK) return s;
         launches += p->sub_b->last_launches;
     }
+    prof_mark(p, st, "FFT over n1");
     if (!transposed_out) {
 #ifdef B200FFT_WITH_NCCL
         // every rank's (B) FFTs ran in place in its phase-B slab: they must
         // all be complete before this rank pulls from the peers' slabs
-        if (p->comm && (s = dist_barrier(p, st)) != FFT_OK) return s;
+        if (p->comm) {
+            if ((s = dist_barrier(p, st)) != FFT_OK) return s;
+            prof_mark(p, st, "barrier");
+        }
 #endif
         // 5. natural order: Z [N2][N1] -> X as [N1][N2] slabs of S1 rows
         //    (rank r: rows k1 in [r S1, ..) = X[r n/P, ..)); pull own rows
         e = launch_dist_transpose(p->prec, bb, bout, S2, N1, S1, P, 0, N2, (int64_t)r0 * S1, nloc * S1, st);
         if (e != cudaSuccess) return cuda_fail(e, "distributed transpose 3");
         ++launches;
+        prof_mark(p, st, "exchange 3 (transpose, peer loads)");
     }
     p->last_launches = launches;
     return FFT_OK;
@@ -1455,10 +1509,19 @@ fft_status fft_plan_set_workspace(fft_plan p, void* ptr, size_t bytes) {
     return FFT_OK;
 }
 
+static fft_status exec_body(fft_plan p, const void* in, void* out, bool inv);
 static fft_status exec(fft_plan p, const void* in, void* out, bool inv) {
     fft_status s = check_ptrs(p, in, out, false);
     if (s != FFT_OK) return s;
     if (p->elems() == 0) return FFT_OK;
+    prof_begin(p, p->stream);
+    s = exec_body(p, in, out, inv);
+    if (s == FFT_OK && p->prof && p->pn == 1) prof_mark(p, p->stream, inv ? "inverse" : "forward");
+    return s;
+}
+
+static fft_status exec_body(fft_plan p, const void* in, void* out, bool inv) {
+    fft_status s;
     // rank 1 on several ranks: the batch is sharded (each rank's plan holds its
     // own rows), so the local schedule is the whole job -- no collective
     if (p->rank == 1 && !p->dist()) return run_1d(p, in, out, inv, p->stream);
@@ -1500,11 +1563,14 @@ fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filt
     if (p->elems() == 0) return FFT_OK;
     if (p->dist() && (p->flags & FFT_OUT_REAL_F32))
         return fail(FFT_E_UNSUPPORTED, "real-output pipeline on a distributed plan");
+    prof_begin(p, p->stream);
     if (p->dist()) {
         s = run_dist_2d(p, in, out, 2, filter, param, p->stream);
         return s == FFT_OK ? dist_check(p) : s;
     }
-    return run_pipeline(p, in, out, filter, param, p->stream);
+    s = run_pipeline(p, in, out, filter, param, p->stream);
+    if (s == FFT_OK && p->prof && p->pn == 1) prof_mark(p, p->stream, "pipeline");
+    return s;
 }
 
 fft_status fft2d_image_filter_u8(fft_plan p, const uint8_t* in, int64_t h, int64_t w, uint8_t* out,
@@ -1738,6 +1804,35 @@ fft_status fft_plan_set_virtual_ranks(fft_plan p, int nranks) {
 
 int fft_plan_last_launch_count(fft_plan p) { return p ? p->last_launches : 0; }
 
+fft_status fft_plan_set_profiling(fft_plan p, int on) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    p->prof = on != 0;
+    p->pn = 0;
+    return FFT_OK;
+}
+
+int fft_plan_phase_times(fft_plan p, float* ms, int max, char* labels, size_t labels_bytes) {
+    if (!p || !p->prof || p->pn < 2) return 0;
+    if (cudaEventSynchronize(p->pev[p->pn - 1]) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    const int n = p->pn - 1 < max ? p->pn - 1 : max;
+    std::string all;
+    for (int k = 0; k < n; ++k) {
+        float t = 0.f;
+        if (ms && cudaEventElapsedTime(&t, p->pev[k], p->pev[k + 1]) == cudaSuccess) ms[k] = t;
+        if (k) all += ';';
+        all += p->plab[k];
+    }
+    if (labels && labels_bytes) {
+        const size_t c = all.size() < labels_bytes - 1 ? all.size() : labels_bytes - 1;
+        memcpy(labels, all.data(), c);
+        labels[c] = 0;
+    }
+    return n;
+}
+
 fft_status fft_plan_destroy(fft_plan p) {
     if (!p) return FFT_OK;
     cudaError_t e = cudaSuccess;
@@ -1764,6 +1859,7 @@ fft_status fft_plan_destroy(fft_plan p) {
         if (p->hstream[i]) cudaStreamDestroy(p->hstream[i]);
     }
     if (p->hev) cudaEventDestroy(p->hev);
+    for (cudaEvent_t ev : p->pev) cudaEventDestroy(ev);
     for (int i = 0; i < 2; ++i)
         if (p->hcomp[i]) cudaEventDestroy(p->hcomp[i]);
 #ifdef B200FFT_WITH_NCCL
