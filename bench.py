@@ -76,10 +76,26 @@ def roofline(alg_bytes, ms, kernel, tkey):
 
 
 # ------------------------------------------------------------------ clocks
+_NVML = {}
+
+
+def _nvml_handle(index):
+    """NVML initialised once per process (nvmlInit is slow: it must not
+    delay the sampler's first sample inside a short timed region)."""
+    if index not in _NVML:
+        import pynvml
+
+        pynvml.nvmlInit()
+        _NVML[index] = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+    return _NVML[index]
+
+
 class ClockSampler:
     """SM clock and clock-event (throttle) reasons sampled through NVML every
     ~2 ms while the timed region runs (the counters nvidia-smi reports as
-    clocks.sm / clocks_event_reasons.*)."""
+    clocks.sm / clocks_event_reasons.*).  The sampler runs until the region's
+    work has completed on the device (the caller synchronises inside the
+    `with` block), and always takes at least 5 samples."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
@@ -94,28 +110,29 @@ class ClockSampler:
 
     def __enter__(self):
         try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv, self.h = _nvml_handle(self.index)
+            self.mx = self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM)
             self.ok = True
+            self.started = threading.Event()
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
+            self.started.wait(1.0)
         except Exception:
             self.ok = False
         return self
 
     def _poll(self):
         nv = self.nv
-        while not self.stop.is_set():
+        while True:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 self.samples.append((sm, rs))
             except Exception:
                 pass
+            self.started.set()
+            if self.stop.is_set() and len(self.samples) >= 5:
+                break
             time.sleep(self.period)
 
     def __exit__(self, *a):
@@ -210,21 +227,23 @@ def cpu_model():
 def timed(stream, fn, reps, flush=None):
     """Per-rep CUDA-event times (ms) of fn() on `stream`; flush (a buffer
     larger than L2) is zeroed on the same stream before each rep, outside
-    the timed region."""
+    the timed region.  All reps are enqueued back to back and synchronised
+    once, so host-side launch jitter (e.g. the clock sampler's NVML calls)
+    never leaves the GPU idle inside a timed region."""
     import torch
 
-    ts = []
-    for _ in range(reps):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
+    evs = []
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if flush is not None:
                 flush.zero_()
             s.record(stream)
             fn()
             e.record(stream)
-        e.synchronize()
-        ts.append(s.elapsed_time(e))
-    return ts
+            evs.append((s, e))
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in evs]
 
 
 # ------------------------------------------------------------------- C2
