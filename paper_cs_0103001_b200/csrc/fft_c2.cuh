@@ -343,6 +343,12 @@ __device__ __forceinline__ void st_step1_twiddle(float2* v, int l, const float2*
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void grp_sync(int bar) { asm volatile("bar.sync %0, 256;\n" ::"r"(bar) : "memory"); }
 
+// 8-byte global store with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void st_pol(float2* p, float2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol)
+                 : "memory");
+}
+
 template <bool INV>
 __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, uint32_t empty, int part, float2* y0,
                                           float scale, const float2* __restrict__ tw4,
@@ -365,9 +371,11 @@ __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, u
     float2 wm = cscale(__ldg(tw4 + (int64_t)hi * 256 + n1), scale);
     const float2 ws = __ldg(tw4 + (int64_t)16 * 256 + n1);
     float2* y = y0 + (int64_t)hi * 256 + n1;
+    // the ring rows are read back soon (B tasks): keep them in L2
+    const uint64_t keep = tmaops::policy_evict_last();
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-        y[q * 16 * 256] = cmul_dir<INV>(v[q], wm);
+        st_pol(y + q * 16 * 256, cmul_dir<INV>(v[q], wm), keep);
         if (q < 15) wm = cmul(wm, ws);
     }
 }
@@ -389,8 +397,9 @@ __device__ __forceinline__ void st_task_b(float2* st, int lo, int hi, int bar, u
     st_step1_twiddle<INV>(v, hi, tw256);
     dft<16, INV>(v);
     float2* x = x0 + lo + (int64_t)hi * 256;
+    const uint64_t stream = tmaops::policy_evict_first();
 #pragma unroll
-    for (int q = 0; q < 16; ++q) x[q * 16 * 256] = v[q];
+    for (int q = 0; q < 16; ++q) st_pol(x + q * 16 * 256, v[q], stream);
 }
 
 template <bool INV, int NS, int MINB>

@@ -133,6 +133,10 @@ cudaError_t launch_tree_combine(int prec, const void* e, const void* o, void* y,
 // task counters).
 bool c2_supported(int prec, int64_t n, int* n1, int* n2);
 size_t c2_workspace_bytes(int64_t batch);
+// plan lifetime bookkeeping: the device's persisting-L2 set-aside for the
+// ring is released with its last 65536-point plan
+void c2_plan_acquire(int dev);
+void c2_plan_release(int dev);
 cudaError_t launch_c2(bool inv, const void* in, void* out, int64_t batch, double scale, const void* tw4,
                       const void* tw, void* ws, size_t ws_bytes, cudaStream_t st);
 

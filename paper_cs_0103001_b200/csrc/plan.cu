@@ -137,6 +137,7 @@ struct fft_plan_s {
     std::vector<int> klo_sh;
     // one-pass 65536-point 1D (fft_c2.cuh, n = cn1 * cn2): four-step twiddles [k2][n1]
     void* tw4 = nullptr;
+    bool c2_acq = false;  // counted in the device's live 65536-point plans (kernels_c2.cu)
     // filter tables (Gaussian)
     void* gu = nullptr;
     void* gv = nullptr;
@@ -1437,6 +1438,8 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
                 t[2 * (k2 * cn1 + n1)] = std::cos(ang);
                 t[2 * (k2 * cn1 + n1) + 1] = std::sin(ang);
             }
+        c2_plan_acquire(p->device);
+        p->c2_acq = true;
         e = upload(t, ip, &p->tw4);
         if (e != cudaSuccess) {
             fft_plan_destroy(p);
@@ -1837,6 +1840,7 @@ fft_status fft_plan_destroy(fft_plan p) {
     if (!p) return FFT_OK;
     cudaError_t e = cudaSuccess;
     if (p->tw4) cudaFree(p->tw4);
+    if (p->c2_acq) c2_plan_release(p->device);
     if (p->twl) cudaFree(p->twl);
     if (p->fta) cudaFree(p->fta);
     if (p->ftb) cudaFree(p->ftb);
