@@ -299,6 +299,75 @@ def paper_parallel_products(m: int, l: int) -> int:
     return (m - l) * 2 ** (m - l) + sum(2 ** (m - l + i) for i in range(1, l + 1))
 
 
+# ---- real input, half spectrum (R2C / C2R; SURVEY NEXT-3) -----------------
+# The paper's images are real, integer-valued rasters (P:352-363, Sec. 6).
+# For real f the DFT is Hermitian, F(u, v) = conj F(-u mod N, -v mod M), so
+# the columns v = 0 .. M/2 determine it; these functions are the paper's
+# transforms (eq5, P:313-316; 2D-IDFT, P:319-328; Eq. E2 / Sec. 3 in 1D)
+# written through that symmetry, on top of the pinned O2 / O4 above.
+
+def hermitian_extend(half, M: int) -> np.ndarray:
+    """[..., N, M/2 + 1] half spectrum -> the full [..., N, M] spectrum of a
+    real signal: F(u, v) for v > M/2 is conj F((N - u) mod N, M - v).  1D:
+    pass a [..., M/2 + 1] array with a trailing axis only (N absent)."""
+    half = np.asarray(half, dtype=np.complex128)
+    h = M // 2 + 1
+    assert half.shape[-1] == h
+    full = np.zeros(half.shape[:-1] + (M,), dtype=np.complex128)
+    full[..., :h] = half
+    v = np.arange(h, M)
+    if half.ndim >= 2:
+        N = half.shape[-2]
+        u = np.arange(N)
+        full[..., :, h:] = np.conj(half[..., (-u) % N, :][..., :, M - v])
+    else:
+        full[..., h:] = np.conj(half[..., M - v])
+    return full
+
+
+def rfft2d(f) -> np.ndarray:
+    """eq5 of a real N x M image (promoted exactly), columns v = 0 .. M/2."""
+    f = np.asarray(f)
+    M = f.shape[-1]
+    return fft2d(f.astype(np.complex128))[:, : M // 2 + 1]
+
+
+def irfft2d(half, M: int):
+    """2D-IDFT (1/M) of the Hermitian spectrum whose columns 0 .. M/2 are
+    `half`; returns (real part, max |imaginary part|) -- the latter ~1e-16
+    relative for a consistent half spectrum."""
+    g = ifft2d(hermitian_extend(half, M))
+    return g.real.copy(), float(np.max(np.abs(g.imag))) if g.size else 0.0
+
+
+def rfft_batch(x) -> np.ndarray:
+    """Eq. E2 (1/n) of each real row, bins k = 0 .. n/2."""
+    x = np.asarray(x)
+    n = x.shape[-1]
+    return fft_batch(x.astype(np.complex128).reshape(-1, n))[:, : n // 2 + 1].reshape(x.shape[:-1] + (n // 2 + 1,))
+
+
+def irfft_batch(half, n: int):
+    """Sec. 3 inverse (unscaled) of each Hermitian row given by bins 0 .. n/2;
+    returns (real part, max |imaginary part|)."""
+    half = np.asarray(half, dtype=np.complex128)
+    rows = half.reshape(-1, n // 2 + 1)
+    full = np.stack([hermitian_extend(r, n) for r in rows])  # 1D extension, row by row
+    g = fft_batch(full, inverse=True).reshape(half.shape[:-1] + (n,))
+    return g.real.copy(), float(np.max(np.abs(g.imag))) if g.size else 0.0
+
+
+def filter_pipeline_real(f, H):
+    """Sec. 6's pipeline on a real image through the half spectrum:
+    2D-IDFT(H .* eq5(f)) with H real and H(u, v) = H(-u, -v) (the Gaussian
+    and both readings of Eq. filtro), so the result is real; returns (real
+    output, max |imaginary part| of the full complex pipeline)."""
+    f = np.asarray(f)
+    M = f.shape[-1]
+    half = rfft2d(f) * np.asarray(H, dtype=np.float64)[:, : M // 2 + 1]
+    return irfft2d(half, M)
+
+
 def dft_bins(x, bins, inverse: bool = False) -> np.ndarray:
     """Selected bins of one transform by compensated direct sums (O7)."""
     bins = np.ascontiguousarray(bins, dtype=np.int64)
