@@ -91,14 +91,15 @@ enum {
      * local index (k2 - r N2/P) N1 + k1 -- one all-to-all less.  Ignored by
      * fft_inverse (its input is always in natural order). */
     FFT_OUT_TRANSPOSED = 1u << 0,
-    /* NEXT-3 (with FFT_IN_REAL_F32, FFT_FILTER_GAUSS, even N and M,
-     * 256 <= N, M <= 2048, single GPU): fft2d_filter_pipeline writes float32
-     * real [N][M] -- the pipeline's real part.  For real input and the real,
-     * even Gaussian H the pipeline preserves Hermitian symmetry, so its
-     * imaginary part is zero in exact arithmetic (nothing is dropped).  Runs
-     * as two real-to-real row passes that transform two real rows per
-     * complex row: half the bytes and flops of the complex pipeline.  Other
-     * filters / sizes: FFT_E_UNSUPPORTED. */
+    /* NEXT-3 (with FFT_IN_REAL_F32, single GPU): fft2d_filter_pipeline
+     * writes float32 real [N][M] -- the pipeline's real part.  For real
+     * input and a real H with H(u, v) = H(-u, -v) (the Gaussian and both
+     * readings of Eq. filtro) the pipeline preserves Hermitian symmetry, so
+     * its imaginary part is zero in exact arithmetic (nothing is dropped).
+     * The separable Gaussian on even sides 256..2048 runs as two real-to-real
+     * row passes (two real rows per complex row); every other filter / size
+     * (2 <= M, N, M <= 8192) goes through the half spectrum (the kernels of
+     * fft_forward_r2c: R2C rows -> columns fwd * H * inv -> C2R rows). */
     FFT_OUT_REAL_F32 = 1u << 2
 };
 
@@ -122,17 +123,44 @@ size_t fft_plan_workspace_bytes(fft_plan plan);
 fft_status fft_plan_set_workspace(fft_plan plan, void* dev_ptr, size_t bytes);
 
 /* Note (complex64, n = 65536): the one-HBM-pass kernel keeps an
- * intermediate ring (~44 MiB, in the plan's workspace) in L2 through an
+ * intermediate ring (~52 MiB, in the plan's workspace) in L2 through an
  * access-policy window and, on first use, sets the device's persisting-L2
- * set-aside (cudaLimitPersistingL2CacheSize) to the ring's size; other
- * kernels may still use that L2 portion while it holds no persisting lines.
- * Set B200FFT_AB_PERSIST=0 to leave the device limit alone. */
+ * set-aside (cudaLimitPersistingL2CacheSize) to the ring's size.  The
+ * set-aside and the ring's persisting lines are released when the device's
+ * last such plan is destroyed (cudaCtxResetPersistingL2Cache): until then
+ * other kernels see that much less L2.  B200FFT_AB_PERSIST=0 leaves the
+ * device limit alone (about 2.5% slower). */
 
 /* Forward (1/N, or eq5's 1/N for rank 2) and inverse (unscaled, or the
  * 2D-IDFT's 1/M) transforms.  in/out: device pointers to the local data
  * (batch * prod(dims) elements); out may equal in. */
 fft_status fft_forward(fft_plan plan, const void* in, void* out);
 fft_status fft_inverse(fft_plan plan, const void* in, void* out);
+
+/* Real data, Hermitian half spectrum (the paper's images are
+ * real rasters).  A real signal's DFT satisfies X(-k) = conj
+ * X(k), so bins 0 .. n/2 of each row determine it.
+ *   fft_forward_r2c: rank 1: `batch` real rows of n -> n/2 + 1 bins each,
+ *     X[k] = (1/n) sum_j x_j e^{-2 pi i jk/n} (Eq. E2), k = 0 .. n/2;
+ *     rank 2: `batch` real N x M grids -> N x (M/2 + 1), eq5 (1/N)
+ *     for columns v = 0 .. M/2.
+ *   fft_inverse_c2r: rank 1: f_j = sum_{k<n} c_k e^{+2 pi i jk/n} (Eq. E3,
+ *     unscaled) of the Hermitian spectrum with bins c_0 .. c_{n/2} (Im c_0
+ *     and Im c_{n/2} are ignored, as a real signal has none); rank 2: the
+ *     2D-IDFT (1/M) of the Hermitian grid given by its columns
+ *     0 .. M/2.
+ * Layouts (device, caller-owned, batch-major, contiguous): real rows of
+ * float32 (FFT_C64 plans) or float64 (FFT_C128); half spectra of complex64 /
+ * complex128 with row length n/2 + 1 (M/2 + 1).  The row length n (M) must
+ * be >= 2 (FFT_E_INVALID_SIZE); in and out must not overlap
+ * (FFT_E_INVALID_ARG if in == out); the 2D inverse uses the plan's workspace
+ * and leaves `in` unchanged.  Not for distributed plans
+ * (FFT_E_UNSUPPORTED).  Kernels: one R2C row kernel (a real row of n read as
+ * the complex row of n/2 points x[2j] + i x[2j+1], one n/2-point transform,
+ * the pairing of X[k] with X[n/2 - k] fused before its store) plus, for
+ * rank 2, one column pass over the M/2 + 1 columns; C2R in reverse. */
+fft_status fft_forward_r2c(fft_plan plan, const void* in_real, void* out_half);
+fft_status fft_inverse_c2r(fft_plan plan, const void* in_half, void* out_real);
 
 /* Rank-2 plans only: out = 2D-IDFT( H .* 2D-DFT(in) ) (Sec. 6).
  * The net scale of the round trip is 1/(N M) (eq5's 1/N times the

@@ -39,7 +39,7 @@ EXPORTS = [
     "fft_execute_host", "fft_nccl_unique_id", "fft_plan_set_comm", "fft_plan_set_virtual_ranks",
     "fft_plan_destroy",
     "fft_status_string", "fft_last_error", "fft_plan_last_launch_count", "fft_build_info",
-    "fft_plan_set_profiling", "fft_plan_phase_times",
+    "fft_plan_set_profiling", "fft_plan_phase_times", "fft_forward_r2c", "fft_inverse_c2r",
 ]
 
 
@@ -83,6 +83,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fft_plan_last_launch_count": ([vp], ci),
         "fft_build_info": ([], ctypes.c_char_p),
         "fft_plan_set_profiling": ([vp, ci], ci),
+        "fft_forward_r2c": ([vp, vp, vp], ci),
+        "fft_inverse_c2r": ([vp, vp, vp], ci),
         "fft_plan_phase_times": ([vp, ctypes.POINTER(ctypes.c_float), ci, ctypes.c_char_p, sz], ci),
     }
     for name, (args, res) in sig.items():
@@ -154,6 +156,16 @@ class Plan:
     def inverse(self, x, out=None):
         out = x if out is None else out
         _check(load_library().fft_inverse(self._h, _ptr(x), _ptr(out)), "fft_inverse")
+        return out
+
+    def forward_r2c(self, x, out):
+        """Real rows / grids -> Hermitian half spectrum (n/2 + 1 bins per row)."""
+        _check(load_library().fft_forward_r2c(self._h, _ptr(x), _ptr(out)), "fft_forward_r2c")
+        return out
+
+    def inverse_c2r(self, x, out):
+        """Hermitian half spectrum -> real rows / grids (unscaled / 1/M)."""
+        _check(load_library().fft_inverse_c2r(self._h, _ptr(x), _ptr(out)), "fft_inverse_c2r")
         return out
 
     def filter_pipeline(self, x, out, filter: int = FILTER_GAUSS, param: float = 0.1):

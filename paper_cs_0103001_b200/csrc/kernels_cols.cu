@@ -22,15 +22,10 @@ cudaError_t cols_pipe_t(const void* in, void* out, int64_t S, int64_t nimg, doub
     constexpr int E = 16, W = WF ? WF : pipe_w<R>();
     using G = ColsPipeCfg<float, R, W, NS>;
     auto kern = k_cols_pipe<float, R, E, W, MODE, NS>;
-    static int grid_max = 0;
-    if (!grid_max) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
-        int dev = 0, sms = 0, occ = 0;
-        if (e == cudaSuccess) e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * (R / E), G::SMEM_BYTES);
+    int grid_max = 0;
+    {
+        cudaError_t e = kernel_setup((const void*)kern, W * (R / E), G::SMEM_BYTES, &grid_max);
         if (e != cudaSuccess) return e;
-        grid_max = sms * (occ > 0 ? occ : 1);
     }
     if (S <= 0 || nimg <= 0) return cudaSuccess;
     const int64_t tiles = (S + W - 1) / W * nimg;
@@ -88,11 +83,9 @@ cudaError_t cols_t(const void* in, void* out, int64_t S, int64_t nimg, double sc
     constexpr size_t smem = sizeof(cpx<T>) * W * cols_ls<T, R, W>();
     static_assert(smem <= 227 * 1024, "column tile exceeds shared memory");
     auto kern = k_cols<T, R, E, W, MODE, MINB>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = kernel_setup((const void*)kern, 0, smem, nullptr);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     if (S <= 0 || nimg <= 0) return cudaSuccess;
     dim3 grid((unsigned)((S + W - 1) / W), (unsigned)nimg);

@@ -106,15 +106,10 @@ cudaError_t image_rows_t(bool inv, const void* in, void* out, int64_t nrows, int
     constexpr int E = img_e<R>(), W = img_w<R>(), TPL = R / E;
     using F = LineFFT<float, R, E, false>;
     constexpr size_t smem = sizeof(float2) * W * F::LS;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_image_rows_fwd<R, E, W>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_image_rows_inv<R, E, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
+    {
+        cudaError_t e = kernel_setup((const void*)k_image_rows_fwd<R, E, W>, 0, smem, nullptr);
+        if (e == cudaSuccess) e = kernel_setup((const void*)k_image_rows_inv<R, E, W>, 0, smem, nullptr);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     if (nrows <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((nrows + W - 1) / W);

@@ -7,10 +7,36 @@
 //   k_twiddle4  : Y[row][k2] *= W_N^{(row0 + row) k2} (the four-step twiddle,
 //                 step (T) of fft_c2.cuh), W_N^x = A[x >> sh] * B[x & mask]
 //                 from two fp64-generated tables (x < N, no wrap).
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "fft_common.cuh"
 #include "launch.h"
 
 namespace b200fft {
+
+cudaError_t kernel_setup(const void* kern, int threads, size_t smem, int* grid_max) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> persistent grid
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find({kern, dev});
+    if (it == done.end()) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int sms = 0, occ = 0;
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess && threads > 0)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (e != cudaSuccess) return e;
+        it = done.emplace(std::make_pair(kern, dev), sms * (occ > 0 ? occ : 1)).first;
+    }
+    if (grid_max) *grid_max = it->second;
+    return cudaSuccess;
+}
+
 
 namespace {
 

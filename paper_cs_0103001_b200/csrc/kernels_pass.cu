@@ -16,11 +16,9 @@ cudaError_t pass_t(const void* in, void* out, int64_t L, int64_t Ns, int64_t bat
     using F = LineFFT<T, R, E, INV>;
     constexpr size_t smem = sizeof(cpx<T>) * W * F::LS;
     auto kern = k_pass<T, R, E, W, INV>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = kernel_setup((const void*)kern, 0, smem, nullptr);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     if (batch <= 0) return cudaSuccess;
     const int64_t LR = L / R;
@@ -42,15 +40,10 @@ cudaError_t pass_pipe_t(const void* in, void* out, int64_t L, int64_t Ns, int64_
     constexpr int TPL = R / E;
     using G = PassPipeCfg<T, R, W>;
     auto kern = k_pass_pipe<T, R, E, W, INV>;
-    static int grid_max = 0;
-    if (!grid_max) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
-        int dev = 0, sms = 0, occ = 0;
-        if (e == cudaSuccess) e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * TPL, G::SMEM_BYTES);
+    int grid_max = 0;
+    {
+        cudaError_t e = kernel_setup((const void*)kern, W * TPL, G::SMEM_BYTES, &grid_max);
         if (e != cudaSuccess) return e;
-        grid_max = sms * (occ > 0 ? occ : 1);
     }
     if (batch <= 0) return cudaSuccess;
     const int64_t LR = L / R;
@@ -73,15 +66,10 @@ cudaError_t pass_tma_t(const void* in, void* out, int64_t L, int64_t Ns, int64_t
     constexpr int TPL = R / E;
     using G = PassTmaCfg<T, R, W>;
     auto kern = k_pass_tma<T, R, E, W, INV>;
-    static int grid_max = 0;
-    if (!grid_max) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
-        int dev = 0, sms = 0, occ = 0;
-        if (e == cudaSuccess) e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * TPL, G::SMEM_BYTES);
+    int grid_max = 0;
+    {
+        cudaError_t e = kernel_setup((const void*)kern, W * TPL, G::SMEM_BYTES, &grid_max);
         if (e != cudaSuccess) return e;
-        grid_max = sms * (occ > 0 ? occ : 1);
     }
     if (batch <= 0) return cudaSuccess;
     const int64_t LR = L / R;

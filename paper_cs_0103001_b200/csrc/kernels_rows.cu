@@ -33,11 +33,9 @@ cudaError_t rows_t(const void* in, void* out, int64_t batch, double scale, const
     using F = LineFFT<T, R, E, INV>;
     constexpr size_t smem = sizeof(cpx<T>) * W * F::LS;
     auto kern = k_rows<T, R, E, W, INV, REAL_IN, FILT>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = kernel_setup((const void*)kern, 0, smem, nullptr);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     if (batch <= 0) return cudaSuccess;
     // blocked layouts: the given block pointers, or local blocks of batch
@@ -91,15 +89,10 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     constexpr int STAGES = OCC == 3 ? 2 : (OCC > 1 ? 1 : 3);
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
     auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS, PAIR, OCC>;
-    static int grid_max = 0;
-    if (!grid_max) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
-        int dev = 0, sms = 0, occ = 0;
-        if (e == cudaSuccess) e = cudaGetDevice(&dev);
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * (R / E), G::SMEM_BYTES);
+    int grid_max = 0;
+    {
+        cudaError_t e = kernel_setup((const void*)kern, W * (R / E), G::SMEM_BYTES, &grid_max);
         if (e != cudaSuccess) return e;
-        grid_max = sms * (occ > 0 ? occ : 1);
     }
     if (batch <= 0) return cudaSuccess;
     const int64_t tiles = (batch + W - 1) / W;

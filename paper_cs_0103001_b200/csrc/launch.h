@@ -127,6 +127,21 @@ cudaError_t launch_image_rows(bool inv, int64_t M, const void* in, void* out, in
 cudaError_t launch_tree_combine(int prec, const void* e, const void* o, void* y, int64_t M, int64_t nb, int64_t es,
                                 int64_t ys, int64_t xstep, const void* ta, const void* tb, int sh, cudaStream_t st);
 
+// Real-input / real-output rows (kernels_real.cu, fft_real.cuh, NEXT-3):
+// batch rows of M reals (float for prec 0, double for 1) <-> rows of M/2 + 1
+// complex bins (Hermitian half spectrum), out = scale * (forward sum e^-,
+// or for C2R the unscaled inverse sum e^+).  rtw: W_M^k, k < M/2.  2 <= M <= 8192.
+cudaError_t launch_rows_r2c(int prec, int64_t M, const void* in, void* out, int64_t batch, double scale,
+                            const void* tw, const void* rtw, cudaStream_t st);
+cudaError_t launch_rows_c2r(int prec, int64_t M, const void* in, void* out, int64_t batch, double scale,
+                            const void* tw, const void* rtw, cudaStream_t st);
+
+// Per-device, thread-safe one-time kernel setup: sets `kern`'s dynamic
+// shared-memory limit on the current device (once per device) and, if
+// grid_max != nullptr, returns its persistent grid there (SM count x
+// occupancy at `threads` threads and `smem` bytes).  (kernels_misc.cu)
+cudaError_t kernel_setup(const void* kern, int threads, size_t smem, int* grid_max);
+
 // One-pass 65536-point complex64 transform (fft_c2.cuh, C2): n = 256 * 256
 // four-step through an L2-resident ring.  tw4: W_n^{n1 k2} laid out
 // [k2][n1]; caller-provided scratch of c2_workspace_bytes (the ring and the

@@ -175,6 +175,9 @@ struct fft_plan_s {
     void* ftb = nullptr;          // W_n^{i}
     int fsh = 0;
     double scale_override = 0.0;  // sub-plans: scale of the last pass (0 = the default)
+    // real rows (NEXT-3): W_M^k, k < M/2 for the row length M (rtw_n = M)
+    void* rtw = nullptr;
+    int64_t rtw_n = 0;
     // four-step column passes of the Gaussian pipeline: W_N^x, x < N
     void* twl = nullptr;
     int64_t twl_n = 0;
@@ -425,6 +428,95 @@ cudaError_t ensure_twl(fft_plan_s* p, int64_t N) {
     return e;
 }
 
+// W_M^k, k < M/2 (fp64-generated, rounded once): the R2C / C2R pairing twiddles
+cudaError_t ensure_rtw(fft_plan_s* p, int64_t M) {
+    if (p->rtw_n == M) return cudaSuccess;
+    if (p->rtw) cudaFree(p->rtw);
+    p->rtw = nullptr;
+    p->rtw_n = 0;
+    const int64_t h = M / 2 > 0 ? M / 2 : 1;
+    std::vector<double> t(2 * (size_t)h);
+    for (int64_t k = 0; k < h; ++k) {
+        const double ang = -2.0 * M_PI * (double)k / (double)M;
+        t[2 * k] = std::cos(ang);
+        t[2 * k + 1] = std::sin(ang);
+    }
+    cudaError_t e = upload(t, p->prec, &p->rtw);
+    if (e == cudaSuccess) p->rtw_n = M;
+    return e;
+}
+
+// NEXT-3: real input -> Hermitian half spectrum.  rank 1: Eq. E2 (1/n) of
+// each row, bins 0 .. n/2; rank 2: eq5 (rows unnormalised, columns 1/N) on
+// columns v = 0 .. M/2.
+fft_status run_r2c(fft_plan_s* p, const void* in, void* out, cudaStream_t st) {
+    const int64_t N = p->n0, M = p->rank == 2 ? p->n1 : p->n0;
+    cudaError_t e = ensure_rtw(p, M);
+    if (e != cudaSuccess) return cuda_fail(e, "R2C twiddle upload");
+    const int64_t rows = p->rank == 2 ? p->batch * N : p->batch;
+    e = launch_rows_r2c(p->prec, M, in, out, rows, p->rank == 2 ? 1.0 : 1.0 / (double)M, p->tw, p->rtw, st);
+    if (e != cudaSuccess) return cuda_fail(e, "k_rows_r2c launch");
+    p->last_launches = 1;
+    if (p->rank == 2) {
+        FilterArgs f{};
+        e = launch_cols(p->prec, 0, N, out, out, M / 2 + 1, p->batch, 1.0 / (double)N, p->tw, f, st);
+        if (e != cudaSuccess) return cuda_fail(e, "k_cols launch");
+        p->last_launches = 2;
+    }
+    return FFT_OK;
+}
+
+// NEXT-3: Hermitian half spectrum -> real.  rank 1: Eq. E3 (unscaled);
+// rank 2: 2D-IDFT (columns unscaled, rows 1/M).  `in` is not modified for
+// rank 1; rank 2 uses the workspace for the column pass.
+fft_status run_c2r(fft_plan_s* p, const void* in, void* out, cudaStream_t st) {
+    const int64_t N = p->n0, M = p->rank == 2 ? p->n1 : p->n0;
+    cudaError_t e = ensure_rtw(p, M);
+    if (e != cudaSuccess) return cuda_fail(e, "C2R twiddle upload");
+    if (p->rank == 1) {
+        e = launch_rows_c2r(p->prec, M, in, out, p->batch, 1.0, p->tw, p->rtw, st);
+        if (e != cudaSuccess) return cuda_fail(e, "k_rows_c2r launch");
+        p->last_launches = 1;
+        return FFT_OK;
+    }
+    fft_status s = ensure_workspace(p);
+    if (s != FFT_OK) return s;
+    const size_t half = (size_t)N * (M / 2 + 1) * p->elem_bytes();
+    for (int64_t g = 0; g < p->batch; ++g) {
+        FilterArgs f{};
+        e = launch_cols(p->prec, 1, N, (const char*)in + g * half, p->ws, M / 2 + 1, 1, 1.0, p->tw, f, st);
+        if (e == cudaSuccess)
+            e = launch_rows_c2r(p->prec, M, p->ws, (char*)out + g * (size_t)N * M * (p->prec == 0 ? 4 : 8), N,
+                                1.0 / (double)M, p->tw, p->rtw, st);
+        if (e != cudaSuccess) return cuda_fail(e, "C2R launch");
+    }
+    p->last_launches = (int)(2 * p->batch);
+    return FFT_OK;
+}
+
+// NEXT-3: real in, real out through the half spectrum for ANY filter whose H
+// is real with H(u, v) = H(-u, -v) (the Gaussian and both readings of Eq.
+// filtro): R2C rows -> columns fwd (1/N) x H x inv -> C2R rows (1/M); half
+// the bytes and flops of the complex pipeline.
+fft_status run_pipeline_half(fft_plan_s* p, const void* in, void* out, const FilterArgs& f, cudaStream_t st) {
+    const int64_t N = p->n0, M = p->n1;
+    cudaError_t e = ensure_rtw(p, M);
+    if (e != cudaSuccess) return cuda_fail(e, "R2C twiddle upload");
+    fft_status s = ensure_workspace(p);
+    if (s != FFT_OK) return s;
+    const size_t grid_r = (size_t)N * M * sizeof(float);
+    for (int64_t g = 0; g < p->batch; ++g) {
+        e = launch_rows_r2c(p->prec, M, (const char*)in + g * grid_r, p->ws, N, 1.0, p->tw, p->rtw, st);
+        if (e == cudaSuccess)
+            e = launch_cols(p->prec, 2, N, p->ws, p->ws, M / 2 + 1, 1, 1.0 / ((double)N * (double)M), p->tw, f, st);
+        if (e == cudaSuccess)
+            e = launch_rows_c2r(p->prec, M, p->ws, (char*)out + g * grid_r, N, 1.0, p->tw, p->rtw, st);
+        if (e != cudaSuccess) return cuda_fail(e, "half-spectrum pipeline launch");
+    }
+    p->last_launches = (int)(3 * p->batch);
+    return FFT_OK;
+}
+
 fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter filter, double param,
                         cudaStream_t st) {
     const int64_t N = p->n0, M = p->n1;
@@ -448,11 +540,15 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
     // fwd*g*inv), 32 B/point of HBM instead of 48 (DESIGN.md "Separable
     // pipeline").  B200FFT_PIPE_LITERAL=1 keeps the three-pass order.
     if (p->flags & FFT_OUT_REAL_F32) {
-        // NEXT-3: real in, real out; two real rows per complex line in both
-        // passes (the Gaussian row / column operators are real and even)
-        if (!real_in || filter != FFT_FILTER_GAUSS || N % 2 || M % 2 || !rows_filter_transposed_supported(p->prec, M) ||
-            !rows_filter_transposed_supported(p->prec, N))
-            return fail(FFT_E_UNSUPPORTED, "real-output pipeline needs real input, the Gaussian, even 256..2048 sides");
+        // NEXT-3: real in, real out.  The separable Gaussian on sides
+        // 256..2048 takes two real rows per complex line in both passes (the
+        // Gaussian row / column operators are real and even: two launches);
+        // every other filter and size goes through the half spectrum.
+        const char* hs = getenv("B200FFT_PIPE_HALF");
+        if (!real_in || M < 2) return fail(FFT_E_UNSUPPORTED, "real-output pipeline needs real input and M >= 2");
+        if (filter != FFT_FILTER_GAUSS || N % 2 || M % 2 || !rows_filter_transposed_supported(p->prec, M) ||
+            !rows_filter_transposed_supported(p->prec, N) || (hs && hs[0] == '1'))
+            return run_pipeline_half(p, in, out, f, st);
         fft_status s = ensure_workspace(p);
         if (s != FFT_OK) return s;
         const size_t grid = (size_t)N * M * sizeof(float);
@@ -1552,6 +1648,39 @@ fft_status fft_forward_paper_tree(fft_plan p, const void* in, void* out) {
 }
 fft_status fft_inverse(fft_plan p, const void* in, void* out) { return exec(p, in, out, true); }
 
+static fft_status check_real(fft_plan p, const void* in, void* out, bool c2r) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (!in || !out) return fail(FFT_E_INVALID_ARG, "null data pointer");
+    if (p->dist()) return fail(FFT_E_UNSUPPORTED, "real transforms of a distributed plan");
+    const int64_t M = p->rank == 2 ? p->n1 : p->n0;
+    if (M < 2) return fail(FFT_E_INVALID_SIZE, "real transforms need a row length >= 2");
+    const size_t rb = p->prec == 0 ? 4 : 8;
+    if (!aligned(c2r ? in : out, p->elem_bytes()) || !aligned(c2r ? out : in, rb))
+        return fail(FFT_E_INVALID_ARG, "data pointer not aligned");
+    if (in == out) return fail(FFT_E_INVALID_ARG, "real transforms are out of place");
+    return FFT_OK;
+}
+
+fft_status fft_forward_r2c(fft_plan p, const void* in, void* out) {
+    fft_status s = check_real(p, in, out, false);
+    if (s != FFT_OK) return s;
+    if (p->elems() == 0) return FFT_OK;
+    prof_begin(p, p->stream);
+    s = run_r2c(p, in, out, p->stream);
+    if (s == FFT_OK && p->prof && p->pn == 1) prof_mark(p, p->stream, "r2c");
+    return s;
+}
+
+fft_status fft_inverse_c2r(fft_plan p, const void* in, void* out) {
+    fft_status s = check_real(p, in, out, true);
+    if (s != FFT_OK) return s;
+    if (p->elems() == 0) return FFT_OK;
+    prof_begin(p, p->stream);
+    s = run_c2r(p, in, out, p->stream);
+    if (s == FFT_OK && p->prof && p->pn == 1) prof_mark(p, p->stream, "c2r");
+    return s;
+}
+
 fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filter filter, double param) {
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (p->rank != 2) return fail(FFT_E_INVALID_ARG, "fft2d_filter_pipeline needs a rank-2 plan");
@@ -1842,6 +1971,7 @@ fft_status fft_plan_destroy(fft_plan p) {
     if (p->tw4) cudaFree(p->tw4);
     if (p->c2_acq) c2_plan_release(p->device);
     if (p->twl) cudaFree(p->twl);
+    if (p->rtw) cudaFree(p->rtw);
     if (p->fta) cudaFree(p->fta);
     if (p->ftb) cudaFree(p->ftb);
     if (p->tree_sub) fft_plan_destroy(p->tree_sub);
