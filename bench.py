@@ -538,6 +538,39 @@ def bench_c4_single(args, local):
             "launches": launches, "l2": "512 MiB grid >> L2", "clocks": clk.summary()}
 
 
+def bench_c4_real(args, local):
+    """NEXT-3 at the C4 size: an 8192^2 float32 sky image -> Gaussian ->
+    float32, through the half spectrum (R2C rows, columns fwd*H*inv over the
+    4097 columns, C2R rows); 16 B/pt (float in + out for two transforms)."""
+    import torch
+
+    import paper_cs_0103001_b200 as b
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    N = 8192
+    x = torch.from_numpy(fixtures.sky_image(N, N, seed=4, nsrc=2000)).to(dev)
+    y = torch.empty_like(x)
+    plan = b.Plan((N, N), flags=b.IN_REAL_F32 | b.OUT_REAL_F32, stream=stream)
+
+    def step():
+        plan.filter_pipeline(x, y, b.FILTER_GAUSS, 0.1)
+
+    for _ in range(3):
+        step()
+    with ClockSampler(local) as clk:
+        ts = timed(stream, step, max(args.steps, 40))
+    med = statistics.median(ts)
+    launches = plan.last_launch_count()
+    plan.destroy()
+    return {"workload": "NEXT-3 at the C4 size: 8192^2 float32 image, Gaussian pipeline real-to-real through the "
+                        "Hermitian half spectrum",
+            "ms_median": round(med, 4), "ms_min": round(min(ts), 4),
+            "GFLOP/s": round(2 * 5 * N * N * math.log2(N * N) / (med / 1e3) / 1e9, 1),
+            "roofline": roofline(16.0 * N * N, med, f"the pipeline's {launches} launches", "C4_real"),
+            "launches": launches, "clocks": clk.summary()}
+
+
 def bench_c5_single(args, local):
     """C5 (BASELINE configs[4]) at P = 1: one N = 2^30 complex64 transform
     (N(0,1), seed 5), forward (1/N) + inverse, multi-pass on one GPU."""
@@ -877,6 +910,7 @@ def main():
                                 "C3_real": _extra("C3_real", bench_c3, args, local, True),
                                 "NEXT1": _extra("NEXT1", bench_next1, args, local),
                                 "C4": _extra("C4", bench_c4_single, args, local),
+                                "C4_real": _extra("C4_real", bench_c4_real, args, local),
                                 "C5": _extra("C5", bench_c5_single, args, local)}
             else:
                 res["extra"] = {"sharded": sharded_extras(args, ws)}

@@ -7,7 +7,7 @@ import sys
 
 src, dst = sys.argv[1], sys.argv[2]
 out = {}
-for cfg in ("C2", "C3", "C3_real", "C4", "C5"):
+for cfg in ("C2", "C3", "C3_real", "C4", "C4_real", "C5"):
     path = os.path.join(src, f"traffic_{cfg}.csv")
     if not os.path.exists(path):
         continue

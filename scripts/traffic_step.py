@@ -30,6 +30,11 @@ elif cfg == "C4":
     out = torch.empty_like(x)
     p = b.Plan((8192, 8192))
     step = lambda: p.filter_pipeline(x, out, b.FILTER_GAUSS, 0.1)  # noqa: E731
+elif cfg == "C4_real":
+    img = torch.from_numpy(fixtures.sky_image(8192, 8192, seed=4, nsrc=2000)).to(dev)
+    out = torch.empty_like(img)
+    p = b.Plan((8192, 8192), flags=b.IN_REAL_F32 | b.OUT_REAL_F32)
+    step = lambda: p.filter_pipeline(img, out, b.FILTER_GAUSS, 0.1)  # noqa: E731
 elif cfg == "C5":
     n = 1 << 30
     xh = np.empty(n, np.complex64)
