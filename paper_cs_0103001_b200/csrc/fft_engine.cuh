@@ -35,6 +35,8 @@ __device__ __forceinline__ int swz16(int i) { return i ^ ((i >> 4) & 15); }
 // x * 16 + t: a dense [R][16] TMA box of 16 columns); with the 16 lines as
 // the thread-fastest index every exchange is conflict-free
 
+// LAYOUT 5: 64 lines interleaved element by element (element x of line t at
+// x * 64 + t: a dense [R][64] TMA box), lines the thread-fastest index
 // LAYOUT 3: one warp per 256-point line, E = 8 (steps 8, 8, 4): XOR the low
 // 4 index bits with g(bits 4..7), g(c) = c ^ (bit 2 of c) << 3 -- every
 // exchange of that schedule hits 16 distinct 8-B bank pairs per half-warp
@@ -151,6 +153,9 @@ struct LineFFT {
             } else if constexpr (LAYOUT == 2) {
 #pragma unroll
                 for (int q = 0; q < rho; ++q) line[(base + q * Ns) * 16] = v[b * rho + q];
+            } else if constexpr (LAYOUT == 5) {
+#pragma unroll
+                for (int q = 0; q < rho; ++q) line[(base + q * Ns) * 64] = v[b * rho + q];
             } else if constexpr (LAYOUT == 3) {
 #pragma unroll
                 for (int q = 0; q < rho; ++q) line[swz8(base + q * Ns)] = v[b * rho + q];
@@ -185,6 +190,9 @@ struct LineFFT {
             } else if constexpr (LAYOUT == 2) {
 #pragma unroll
                 for (int r = 0; r < rho; ++r) v[b * rho + r] = line[(j + r * st) * 16];
+            } else if constexpr (LAYOUT == 5) {
+#pragma unroll
+                for (int r = 0; r < rho; ++r) v[b * rho + r] = line[(j + r * st) * 64];
             } else if constexpr (LAYOUT == 3) {
 #pragma unroll
                 for (int r = 0; r < rho; ++r) v[b * rho + r] = line[swz8(j + r * st)];
@@ -206,6 +214,7 @@ struct LineFFT {
     __device__ __forceinline__ static int bpos(int lt, int m) {
         if constexpr (LAYOUT == 1) return swz16(lt + TPL * m);
         else if constexpr (LAYOUT == 2) return (lt + TPL * m) * 16;
+        else if constexpr (LAYOUT == 5) return (lt + TPL * m) * 64;
         else if constexpr (LAYOUT == 3) return swz8(lt + TPL * m);
         else if constexpr (LAYOUT == 4) return il8(lt + TPL * m);
         else if constexpr (TPL % 16 == 0) return pad16(lt) + m * (TPL + TPL / 16);

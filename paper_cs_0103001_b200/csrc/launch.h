@@ -136,6 +136,16 @@ cudaError_t launch_rows_r2c(int prec, int64_t M, const void* in, void* out, int6
 cudaError_t launch_rows_c2r(int prec, int64_t M, const void* in, void* out, int64_t batch, double scale,
                             const void* tw, const void* rtw, cudaStream_t st);
 
+// One-pass column filter of the 8192-row Gaussian pipeline (kernels_colpipe.cu,
+// fft_colpipe.cuh): in place on [nimg][8192][M] complex64 (M % 16 == 0),
+// column operator IDFT_N(g_N(u) * scale * [g_M(v + col_off)] * DFT_N); tl =
+// W_N^x (x < N), gu = g_N (N floats), gv = g_M or null; ws: counters.
+bool colfilt_supported(int64_t N, int64_t M);
+size_t colfilt_workspace_bytes(int64_t M, int64_t nimg);
+cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, const void* tw, const void* tl,
+                           const void* gu, const void* gv, int64_t col_off, void* ws, size_t ws_bytes,
+                           cudaStream_t st);
+
 // Per-device, thread-safe one-time kernel setup: sets `kern`'s dynamic
 // shared-memory limit on the current device (once per device) and, if
 // grid_max != nullptr, returns its persistent grid there (SM count x

@@ -235,8 +235,11 @@ void prof_begin(fft_plan_s* p, cudaStream_t st) {
 
 size_t workspace_need(const fft_plan_s* p) {
     if (p->dist()) return 2 * (size_t)p->elems() * p->elem_bytes();  // send + recv slabs
-    if (p->rank == 2)  // the transposed grid of the Gaussian pipeline (allocated on first use)
-        return (size_t)p->n0 * p->n1 * p->elem_bytes();
+    if (p->rank == 2) {  // the transposed grid of the Gaussian pipeline (allocated on first use)
+        const size_t g = (size_t)p->n0 * p->n1 * p->elem_bytes();
+        const size_t c = colfilt_workspace_bytes(p->n1, p->batch);
+        return g > c ? g : c;
+    }
     if (p->rank == 1 && p->tw4) return c2_workspace_bytes(p->batch);
     if (p->rank == 1 && !p->radices.empty()) {
         size_t one = (size_t)p->elems() * p->elem_bytes();
@@ -629,6 +632,21 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
         fb.kind = 6;
         fb.gu = p->gu;
         fb.n1 = N1;
+        if (colfilt_supported(N, M)) {
+            // the three column phases as ONE task-pipeline kernel, each group
+            // of 16 columns staying in L2 between them (fft_colpipe.cuh):
+            // rows pass + 1 column pass = one HBM read + write per pass
+            fft_status s = ensure_workspace(p);
+            if (s != FFT_OK) return s;
+            e = launch_rows(p->prec, false, real_in, M, in, out, p->batch * N, 1.0 / (double)M, p->tw, st, -1, -1,
+                            p->gv);
+            if (e == cudaSuccess)
+                e = launch_colfilt(out, M, p->batch, 1.0 / (double)N, p->tw, p->twl, p->gu, nullptr, 0, p->ws,
+                                   p->ws_bytes, st);
+            if (e != cudaSuccess) return cuda_fail(e, "one-pass column pipeline launch");
+            p->last_launches = 2;
+            return FFT_OK;
+        }
         for (int64_t g = 0; g < p->batch; ++g) {
             char* o = (char*)out + g * grid;
             e = launch_rows(p->prec, false, real_in, M, (const char*)in + g * in_grid, o, N, 1.0 / (double)M, p->tw,
