@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(320, 3)
     k_colfilt(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               float2* __restrict__ grid, int64_t M, int64_t nimg, float scale, const float2* __restrict__ tw64,
               const float2* __restrict__ tw128, const float2* __restrict__ tl, const float* __restrict__ gu,
-              const float* __restrict__ gv, int64_t col_off, ColPipeCtl ctl) {
+              const float* __restrict__ gv, int64_t col_off, int cg_sh, ColPipeCtl ctl) {
     using G = ColPipeCfg;
     constexpr int NS = G::NS, NSIG = G::NSIG;
     constexpr int64_t N = 64 * N2;
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(320, 3)
     volatile int64_t* sigb = task + NS;
     volatile int* sigdone = reinterpret_cast<volatile int*>(sigb + NSIG);
     const int tid = threadIdx.x;
-    const int64_t CG = M / 16;  // column groups per image
+    const int64_t CG = M / 16;  // column groups per image (a power of two, 2^cg_sh)
     const int64_t groups = CG * nimg;
     const int64_t npos = (groups + 2 * (int64_t)ctl.D) * 96;
 
@@ -111,8 +111,8 @@ __global__ void __launch_bounds__(320, 3)
                     break;
                 }
                 task[s] = i;
-                const int img = (int)(g / CG);
-                const int c0 = (int)(g % CG) * 16;
+                const int img = (int)(g >> cg_sh);
+                const int c0 = (int)(g & (CG - 1)) * 16;
                 if (phase != 2) {
                     while (*sigdone < na - NSIG + 1) __nanosleep(20);
                     ++na;
@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(320, 3)
         int phase, part;
         int64_t g;
         cp_decode(i, groups, ctl.D, phase, g, part);
-        const int64_t img = g / CG;
-        const int64_t c0 = (g % CG) * 16;
+        const int64_t img = g >> cg_sh;
+        const int64_t c0 = (g & (CG - 1)) * 16;
         float2 v[16];
         if (phase != 1) {
             // line (n2l, col) = tid % 64, 4 lanes of 16 elements (n1 or k1)

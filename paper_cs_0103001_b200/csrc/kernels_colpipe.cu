@@ -36,7 +36,7 @@ bool encode3d(CUtensorMap* map, void* base, uint64_t d0, uint64_t d1, uint64_t d
 bool colfilt_supported(int64_t N, int64_t M) {
     const char* v = getenv("B200FFT_PIPE_COLS1");
     if (v && v[0] == '0') return false;
-    return N == 8192 && M >= 16 && M % 16 == 0;
+    return N == 8192 && M >= 16 && (M & (M - 1)) == 0;
 }
 
 size_t colfilt_workspace_bytes(int64_t M, int64_t nimg) {
@@ -67,7 +67,7 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
     // phase distance: B(g) is 96 D positions after A(g), beyond the ~900
     // positions in flight; 2 D + ~10 groups (1 MiB each) live in L2
     const char* dv = getenv("B200FFT_COLS1_D");
-    ColPipeCtl c{ctr, ctr + groups, next, dv ? atoi(dv) : 16};
+    ColPipeCtl c{ctr, ctr + groups, next, dv ? atoi(dv) : 32};
     float2* a_grid = reinterpret_cast<float2*>(grid);
     int64_t a_M = M, a_nimg = nimg;
     float a_scale = (float)scale;
@@ -77,7 +77,10 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
     const float* a_gu = reinterpret_cast<const float*>(gu);
     const float* a_gv = reinterpret_cast<const float*>(gv);
     int64_t a_off = col_off;
-    void* args[] = {&ma, &mb, &a_grid, &a_M, &a_nimg, &a_scale, &a_tw64, &a_tw128, &a_tl, &a_gu, &a_gv, &a_off, &c};
+    int cg_sh = 0;
+    while (((int64_t)1 << cg_sh) < M / 16) ++cg_sh;
+    void* args[] = {&ma, &mb, &a_grid, &a_M, &a_nimg, &a_scale, &a_tw64, &a_tw128, &a_tl, &a_gu, &a_gv, &a_off,
+                    &cg_sh, &c};
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
