@@ -122,10 +122,16 @@ def test_real_to_real_gauss_pipeline(b, batch, N, M):
     assert oracle.rel_l2(o.cpu().numpy(), ref) <= 1e-5
 
 
-def test_real_to_real_rejects_other_filters(b):
+def test_real_to_real_other_filters_use_the_half_spectrum(b):
+    """Since NEXT-3's R2C / C2R: a real-output plan runs the ideal filters too
+    (through the half spectrum: 3 launches), matching the oracle."""
+    img = fixtures.sky_image(256, 256, seed=77, nsrc=20)
     p = b.Plan((256, 256), flags=b.IN_REAL_F32 | b.OUT_REAL_F32)
-    x = torch.zeros((256, 256), dtype=torch.float32, device="cuda")
+    x = torch.from_numpy(img).cuda()
     o = torch.empty_like(x)
-    with pytest.raises(b.FFTError):
-        p.filter_pipeline(x, o, b.FILTER_IDEAL_LOWPASS, 10.0)
+    p.filter_pipeline(x, o, b.FILTER_IDEAL_LOWPASS, 10.0)
+    torch.cuda.synchronize()
+    assert p.last_launch_count() == 3
+    ref, _ = oracle.filter_pipeline_real(img, oracle.ideal_filter(256, 256, 10.0, literal=False))
+    assert oracle.rel_l2(o.cpu().numpy(), ref) <= 1e-5
     p.destroy()
