@@ -175,6 +175,9 @@ struct fft_plan_s {
     void* ftb = nullptr;          // W_n^{i}
     int fsh = 0;
     double scale_override = 0.0;  // sub-plans: scale of the last pass (0 = the default)
+    // k_colfilt's task counters (plan-owned, grown on demand)
+    void* cws = nullptr;
+    size_t cws_bytes = 0;
     // real rows (NEXT-3): W_M^k, k < M/2 for the row length M (rtw_n = M)
     void* rtw = nullptr;
     int64_t rtw_n = 0;
@@ -235,11 +238,8 @@ void prof_begin(fft_plan_s* p, cudaStream_t st) {
 
 size_t workspace_need(const fft_plan_s* p) {
     if (p->dist()) return 2 * (size_t)p->elems() * p->elem_bytes();  // send + recv slabs
-    if (p->rank == 2) {  // the transposed grid of the Gaussian pipeline (allocated on first use)
-        const size_t g = (size_t)p->n0 * p->n1 * p->elem_bytes();
-        const size_t c = colfilt_workspace_bytes(p->n1, p->batch);
-        return g > c ? g : c;
-    }
+    if (p->rank == 2)  // the transposed grid of the Gaussian pipeline (allocated on first use)
+        return (size_t)p->n0 * p->n1 * p->elem_bytes();
     if (p->rank == 1 && p->tw4) return c2_workspace_bytes(p->batch);
     if (p->rank == 1 && !p->radices.empty()) {
         size_t one = (size_t)p->elems() * p->elem_bytes();
@@ -435,6 +435,7 @@ cudaError_t ensure_twl(fft_plan_s* p, int64_t N) {
 cudaError_t ensure_rtw(fft_plan_s* p, int64_t M) {
     if (p->rtw_n == M) return cudaSuccess;
     if (p->rtw) cudaFree(p->rtw);
+    if (p->cws) cudaFree(p->cws);
     p->rtw = nullptr;
     p->rtw_n = 0;
     const int64_t h = M / 2 > 0 ? M / 2 : 1;
@@ -518,6 +519,25 @@ fft_status run_pipeline_half(fft_plan_s* p, const void* in, void* out, const Fil
     }
     p->last_launches = (int)(3 * p->batch);
     return FFT_OK;
+}
+
+// the one-pass column filter (k_colfilt) on [nimg][8192][SM] with its own
+// counter buffer; scale and g_M (gv, with the slab's column offset) as the
+// caller's schedule needs
+cudaError_t colfilt(fft_plan_s* p, void* grid, int64_t SM, int64_t nimg, double scale, const void* gv,
+                    int64_t col_off, cudaStream_t st) {
+    cudaError_t e = ensure_twl(p, p->n0);
+    if (e != cudaSuccess) return e;
+    const size_t need = colfilt_workspace_bytes(SM, nimg);
+    if (p->cws_bytes < need) {
+        if (p->cws) cudaFree(p->cws);
+        p->cws = nullptr;
+        p->cws_bytes = 0;
+        e = cudaMalloc(&p->cws, need);
+        if (e != cudaSuccess) return e;
+        p->cws_bytes = need;
+    }
+    return launch_colfilt(grid, SM, nimg, scale, p->tw, p->twl, p->gu, gv, col_off, p->cws, p->cws_bytes, st);
 }
 
 fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter filter, double param,
@@ -636,13 +656,9 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
             // the three column phases as ONE task-pipeline kernel, each group
             // of 16 columns staying in L2 between them (fft_colpipe.cuh):
             // rows pass + 1 column pass = one HBM read + write per pass
-            fft_status s = ensure_workspace(p);
-            if (s != FFT_OK) return s;
             e = launch_rows(p->prec, false, real_in, M, in, out, p->batch * N, 1.0 / (double)M, p->tw, st, -1, -1,
                             p->gv);
-            if (e == cudaSuccess)
-                e = launch_colfilt(out, M, p->batch, 1.0 / (double)N, p->tw, p->twl, p->gu, nullptr, 0, p->ws,
-                                   p->ws_bytes, st);
+            if (e == cudaSuccess) e = colfilt(p, out, M, p->batch, 1.0 / (double)N, nullptr, 0, st);
             if (e != cudaSuccess) return cuda_fail(e, "one-pass column pipeline launch");
             p->last_launches = 2;
             return FFT_OK;
@@ -753,6 +769,12 @@ cudaError_t dist_columns(fft_plan_s* p, char* cs, int mode, const FilterArgs& f,
                          cudaStream_t st, int* launches) {
     const int64_t N = p->n0, M = p->n1;
     const char* c4 = getenv("B200FFT_PIPE_COLS4");
+    if (mode == 2 && f.kind == FFT_FILTER_GAUSS && p->prec == 0 && colfilt_supported(N, SM) &&
+        !(c4 && c4[0] == '0')) {
+        // the three column phases in one kernel, the slab's groups in L2
+        *launches += 1;
+        return colfilt(p, cs, SM, 1, 1.0 / ((double)N * (double)M), f.gv, col_off, st);
+    }
     if (mode == 2 && f.kind == FFT_FILTER_GAUSS && p->prec == 0 && N >= 4096 && N <= 8192 && SM >= 16 &&
         !(c4 && c4[0] == '0')) {
         cudaError_t e = ensure_twl(p, N);
@@ -1990,6 +2012,7 @@ fft_status fft_plan_destroy(fft_plan p) {
     if (p->c2_acq) c2_plan_release(p->device);
     if (p->twl) cudaFree(p->twl);
     if (p->rtw) cudaFree(p->rtw);
+    if (p->cws) cudaFree(p->cws);
     if (p->fta) cudaFree(p->fta);
     if (p->ftb) cudaFree(p->ftb);
     if (p->tree_sub) fft_plan_destroy(p->tree_sub);
