@@ -146,6 +146,15 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
                            const void* gu, const void* gv, int64_t col_off, void* ws, size_t ws_bytes,
                            cudaStream_t st);
 
+// Two-pass 2^30-point complex64 transform (kernels_big.cu, fft_big.cuh, C5 on
+// one GPU): in -> mid (pass 1: column FFTs + four-step twiddle) -> out (pass 2:
+// row FFTs, x scale); mid must not alias in or out; twl = W_32768^x, whi /
+// wlo = W_n^{i 32768} / W_n^i (i < 32768); ws: the L2 ring and counters.
+bool big_supported(int prec, int64_t n);
+size_t big_workspace_bytes();
+cudaError_t launch_big(bool inv, const void* in, void* mid, void* out, double scale, const void* tw, const void* twl,
+                       const void* whi, const void* wlo, void* ws, size_t ws_bytes, cudaStream_t st);
+
 // Per-device, thread-safe one-time kernel setup: sets `kern`'s dynamic
 // shared-memory limit on the current device (once per device) and, if
 // grid_max != nullptr, returns its persistent grid there (SM count x

@@ -175,6 +175,10 @@ struct fft_plan_s {
     void* ftb = nullptr;          // W_n^{i}
     int fsh = 0;
     double scale_override = 0.0;  // sub-plans: scale of the last pass (0 = the default)
+    // two-pass 2^30 (fft_big.cuh): W_32768^x, W_n^{i 32768}, W_n^i (i < 32768)
+    void* big_twl = nullptr;
+    void* big_hi = nullptr;
+    void* big_lo = nullptr;
     // k_colfilt's task counters (plan-owned, grown on demand)
     void* cws = nullptr;
     size_t cws_bytes = 0;
@@ -243,6 +247,8 @@ size_t workspace_need(const fft_plan_s* p) {
     if (p->rank == 1 && p->tw4) return c2_workspace_bytes(p->batch);
     if (p->rank == 1 && !p->radices.empty()) {
         size_t one = (size_t)p->elems() * p->elem_bytes();
+        if (big_supported(p->prec, p->n0) && p->batch == 1 && !p->dist())
+            return one + big_workspace_bytes();  // the two-pass 2^30: mid grid + L2 ring
         return p->radices.size() % 2 == 1 ? 2 * one : one;  // odd pass counts may need ws1 (run_1d)
     }
     return 0;
@@ -323,6 +329,37 @@ fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream
         e = launch_c2(inv, in, out, p->batch, scale, p->tw4, p->tw, p->ws, p->ws_bytes, st);
         p->last_launches = 1;
         if (e != cudaSuccess) return cuda_fail(e, "k_ab_ws launch");
+        return FFT_OK;
+    }
+    if (big_supported(p->prec, L) && p->batch == 1 && !p->dist() && !p->radices.empty()) {
+        // 2^30 in two HBM passes (fft_big.cuh): in -> ws (Y) -> out
+        fft_status s = ensure_workspace(p);
+        if (s != FFT_OK) return s;
+        if (!p->big_twl) {
+            const int64_t Lh = 32768;
+            std::vector<double> a(2 * Lh), hi(2 * Lh), lo(2 * Lh);
+            for (int64_t x = 0; x < Lh; ++x) {
+                const double t0 = -2.0 * M_PI * (double)x / (double)Lh;
+                a[2 * x] = std::cos(t0);
+                a[2 * x + 1] = std::sin(t0);
+                const double t1 = -2.0 * M_PI * (double)(x * Lh) / (double)L;  // (x 2^15) / 2^30, exact
+                hi[2 * x] = std::cos(t1);
+                hi[2 * x + 1] = std::sin(t1);
+                const double t2 = -2.0 * M_PI * (double)x / (double)L;
+                lo[2 * x] = std::cos(t2);
+                lo[2 * x + 1] = std::sin(t2);
+            }
+            e = upload(a, 0, &p->big_twl);
+            if (e == cudaSuccess) e = upload(hi, 0, &p->big_hi);
+            if (e == cudaSuccess) e = upload(lo, 0, &p->big_lo);
+            if (e != cudaSuccess) return cuda_fail(e, "2^30 twiddle upload");
+        }
+        const size_t one = (size_t)L * p->elem_bytes();
+        char* mid = (char*)p->ws;
+        e = launch_big(inv, in, mid, out, scale, p->tw, p->big_twl, p->big_hi, p->big_lo, mid + one, p->ws_bytes - one,
+                       st);
+        p->last_launches = 2;
+        if (e != cudaSuccess) return cuda_fail(e, "k_big launch");
         return FFT_OK;
     }
     if (p->radices.empty()) {
@@ -436,6 +473,9 @@ cudaError_t ensure_rtw(fft_plan_s* p, int64_t M) {
     if (p->rtw_n == M) return cudaSuccess;
     if (p->rtw) cudaFree(p->rtw);
     if (p->cws) cudaFree(p->cws);
+    if (p->big_twl) cudaFree(p->big_twl);
+    if (p->big_hi) cudaFree(p->big_hi);
+    if (p->big_lo) cudaFree(p->big_lo);
     p->rtw = nullptr;
     p->rtw_n = 0;
     const int64_t h = M / 2 > 0 ? M / 2 : 1;
@@ -2013,6 +2053,9 @@ fft_status fft_plan_destroy(fft_plan p) {
     if (p->twl) cudaFree(p->twl);
     if (p->rtw) cudaFree(p->rtw);
     if (p->cws) cudaFree(p->cws);
+    if (p->big_twl) cudaFree(p->big_twl);
+    if (p->big_hi) cudaFree(p->big_hi);
+    if (p->big_lo) cudaFree(p->big_lo);
     if (p->fta) cudaFree(p->fta);
     if (p->ftb) cudaFree(p->ftb);
     if (p->tree_sub) fft_plan_destroy(p->tree_sub);
