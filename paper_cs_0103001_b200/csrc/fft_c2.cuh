@@ -57,6 +57,16 @@ __device__ __forceinline__ void bk_wait(uint32_t bar, uint32_t parity) {
         "r"(parity), "r"(20000u)
         : "memory");
 }
+// one contiguous global -> shared bulk copy (the TMA engine, no tensor map),
+// completing on an mbarrier; with an L2 eviction-priority policy
+__device__ __forceinline__ void bk_load_pol(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                            uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void bk_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ int bk_ld_acquire(const int* p) {
     int v;

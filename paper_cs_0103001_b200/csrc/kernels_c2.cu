@@ -67,7 +67,8 @@ struct AbGeom {
     int grid[C2_NKIND][2] = {};  // [kind][inverse]
     int D = 0, ring = 0;
     bool limit_set = false;
-    int plans = 0;  // live 65536-point plans on the device (c2_plan_acquire / release)
+    size_t limit = 0;  // the persisting set-aside requested so far (the largest ring)
+    int plans = 0;     // live plans with an L2 ring on the device (c2_plan_acquire / release)
 };
 std::mutex g_geom_mu;
 std::map<int, AbGeom> g_geom;
@@ -112,17 +113,26 @@ cudaError_t ab_geom(int dev, AbGeom* g) {
 }
 
 // The persisting-L2 set-aside of a device, sized once for the ring
-void ab_persist_limit(int dev, size_t ring_bytes) {
+}  // namespace
+
+// The device's persisting-L2 set-aside, sized for the largest ring asked for
+// (the 65536-point ring, the 2^30 transform's ring); set on first use.
+void l2_persist_request(int dev, size_t ring_bytes) {
     std::lock_guard<std::mutex> lk(g_geom_mu);
     AbGeom& c = g_geom[dev];
-    if (c.limit_set) return;
+    if (c.limit_set && c.limit >= ring_bytes) return;
     int mx = 0;
     cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
     int cur = -1;
     cudaGetDevice(&cur);
     if (cur == dev) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ring_bytes < (size_t)mx ? ring_bytes : (size_t)mx);
     c.limit_set = true;
+    c.limit = ring_bytes;
 }
+
+namespace {
+
+void ab_persist_limit(int dev, size_t ring_bytes) { l2_persist_request(dev, ring_bytes); }
 
 // caller-provided scratch: the Y ring (ring x 512 KiB), then the counters
 size_t ab_ws_bytes(int64_t ring, int64_t batch) {
@@ -259,6 +269,7 @@ void c2_plan_release(int dev) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
     if (cur != dev && cur >= 0) cudaSetDevice(cur);
     c.limit_set = false;
+    c.limit = 0;
 }
 
 size_t c2_workspace_bytes(int64_t batch) {

@@ -171,6 +171,9 @@ size_t c2_workspace_bytes(int64_t batch);
 // ring is released with its last 65536-point plan
 void c2_plan_acquire(int dev);
 void c2_plan_release(int dev);
+// the device's persisting-L2 set-aside for an L2 ring of ring_bytes (the
+// largest requested; released with the last acquiring plan)
+void l2_persist_request(int dev, size_t ring_bytes);
 cudaError_t launch_c2(bool inv, const void* in, void* out, int64_t batch, double scale, const void* tw4,
                       const void* tw, void* ws, size_t ws_bytes, cudaStream_t st);
 

@@ -336,6 +336,10 @@ fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream
         fft_status s = ensure_workspace(p);
         if (s != FFT_OK) return s;
         if (!p->big_twl) {
+            if (!p->c2_acq) {  // the ring's persisting set-aside is released with the plan
+                c2_plan_acquire(p->device);
+                p->c2_acq = true;
+            }
             const int64_t Lh = 32768;
             std::vector<double> a(2 * Lh), hi(2 * Lh), lo(2 * Lh);
             for (int64_t x = 0; x < Lh; ++x) {
