@@ -490,11 +490,11 @@ __global__ void __launch_bounds__(320, MINB)
                     while (*sigdone < na - NSIG + 1) __nanosleep(20);
                     ++na;
                     // the ring slot's previous transform: all its B parts have read it
-                    if (b >= ctl.ring) wait_count(ctl.done_b + (b - ctl.ring), 16);
+                    if (b >= ctl.ring && !(opts & 256)) wait_count(ctl.done_b + (b - ctl.ring), 16);
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
                 } else {
-                    wait_count(ctl.done_a + b, 16);
+                    if (!(opts & 256)) wait_count(ctl.done_a + b, 16);
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);

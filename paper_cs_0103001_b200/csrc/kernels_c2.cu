@@ -164,8 +164,11 @@ int64_t ab_launch_grid(int64_t grid, int64_t batch, int64_t D, int NS) {
 //            of the A tile 128 d positions ahead (+1.5%).  Default 0.
 int ab_opts(int kind) {
     const char* v = getenv("B200FFT_AB_OPTS");
-    if (v) return atoi(v);
-    return kind == C2_WS ? (128 | 16) : 0;
+    int o = v ? atoi(v) : (kind == C2_WS ? (128 | 16) : 0);
+    // bit 8 (k_ab_st): no dependency waits -- a timing experiment with WRONG
+    // results, honoured only with B200FFT_ALLOW_WRONG set
+    if ((o & 256) && !getenv("B200FFT_ALLOW_WRONG")) o &= ~256;
+    return o;
 }
 
 template <bool INV>
