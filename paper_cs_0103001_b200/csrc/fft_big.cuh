@@ -41,8 +41,6 @@ struct BigCtl {
     int* done_b;               // [groups] B tasks that have read their ring rows
     unsigned long long* next;  // next position
     int D, ring;               // phase distance (groups), ring slots
-    int pf;                    // L2 prefetch distance (positions) of A boxes, 0 = off
-    int bulk;                  // B loads as one bulk copy (1) or a tensor box (0)
 };
 
 struct BigCfg {
@@ -126,19 +124,6 @@ __global__ void __launch_bounds__(320, 3)
                 }
                 task[s] = i;
                 const int slot = (int)(g % ctl.ring);
-                if (ctl.pf > 0) {
-                    // warm L2 with the HBM box of the A task pf positions ahead
-                    // (taken by whichever CTA: positions go out in order)
-                    bool pb;
-                    int pp;
-                    int64_t pg;
-                    if (big_decode(i + ctl.pf, GROUPS, ctl.D, pb, pg, pp) && !pb) {
-                        if (PASS == 1)
-                            tmaops::prefetch3(&map_in, (int)(16 * pg), pp, 0);
-                        else
-                            tmaops::prefetch3(&map_in, 16 * (pp & 7), 0, (int)(16 * pg + (pp >> 3)));
-                    }
-                }
                 if (!isb) {
                     while (*sigdone < na - NSIG + 1) __nanosleep(20);
                     ++na;
@@ -153,13 +138,9 @@ __global__ void __launch_bounds__(320, 3)
                     while (bk_ld_acquire(ctl.done_a + g) < 128) __nanosleep(32);
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
-                    // kc = 2 part, 2 part + 1 of the slot: 32 KiB contiguous, one
-                    // bulk copy (a tensor box would be 256 row requests of 128 B)
-                    if (ctl.bulk)
-                        bk_load_pol(st, ring + (int64_t)slot * G::SLOT + (int64_t)part * 4096, (uint32_t)G::STAGE,
-                                    bar, pol_keep);
-                    else
-                        tmaops::load3(st, &map_ring, 0, 0, slot * 256 + 2 * part, bar, pol_keep);
+                    // kc = 2 part, 2 part + 1 of the slot: 32 KiB contiguous
+                    // (view {16 | 128, 128 | 16, 256 ring}: box [2 kc][..][..])
+                    tmaops::load3(st, &map_ring, 0, 0, slot * 256 + 2 * part, bar, pol_keep);
                 }
             }
         } else {  // ---- signaller ----

@@ -57,16 +57,6 @@ __device__ __forceinline__ void bk_wait(uint32_t bar, uint32_t parity) {
         "r"(parity), "r"(20000u)
         : "memory");
 }
-// one contiguous global -> shared bulk copy (the TMA engine, no tensor map),
-// completing on an mbarrier; with an L2 eviction-priority policy
-__device__ __forceinline__ void bk_load_pol(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
-                                            uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
-            dst),
-        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
-        : "memory");
-}
 __device__ __forceinline__ void bk_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ int bk_ld_acquire(const int* p) {
     int v;
@@ -452,28 +442,13 @@ __global__ void __launch_bounds__(320, MINB)
             const uint64_t pol_stream = tmaops::policy_evict_first();
             const uint64_t pol_keep = tmaops::policy_evict_last();
             int na = 0;  // A tasks issued by this CTA
-            // opts bit 0: take the next position (atomic) right after issuing a
-            // load, so its round trip overlaps the wait for the next stage;
-            // bit 1: poll the dependency counters relaxed (no L1 invalidation
-            // per poll), one acquire once satisfied
-            const bool early = (opts & 1) != 0, relaxed = (opts & 2) != 0;
-            int64_t inext = early ? (int64_t)atomicAdd(ctl.next, 1ull) : 0;
-            auto wait_count = [&](const int* p, int target) {
-                if (relaxed) {
-                    int v;
-                    for (;;) {
-                        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-                        if (v >= target) break;
-                        __nanosleep(32);
-                    }
-                } else {
-                    while (bk_ld_acquire(p) < target) __nanosleep(32);
-                }
-            };
+            // (taking the next position before the stage is free, relaxed
+            // flag polling and L2 prefetches of later A boxes measured +4%,
+            // +-0 and +1.5%: profiles/README.md)
             for (int64_t k = 0;; ++k) {
                 const int s = (int)(k % NS);
                 if (k >= NS) bk_wait(empty0 + 8 * s, (uint32_t)(((k / NS) - 1) & 1));
-                const int64_t i = early ? inext : (int64_t)atomicAdd(ctl.next, 1ull);
+                const int64_t i = (int64_t)atomicAdd(ctl.next, 1ull);
                 task[s] = i;
                 const uint32_t st = s_base + (uint32_t)(s * G::STAGE), bar = full0 + 8 * s;
                 if (i >= ntasks) {  // no more work: the compute warps exit on this stage
@@ -490,28 +465,15 @@ __global__ void __launch_bounds__(320, MINB)
                     while (*sigdone < na - NSIG + 1) __nanosleep(20);
                     ++na;
                     // the ring slot's previous transform: all its B parts have read it
-                    if (b >= ctl.ring && !(opts & 256)) wait_count(ctl.done_b + (b - ctl.ring), 16);
+                    if (b >= ctl.ring)
+                        while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
                 } else {
-                    if (!(opts & 256)) wait_count(ctl.done_a + b, 16);
+                    while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
-                }
-                if (early) inext = (int64_t)atomicAdd(ctl.next, 1ull);
-                // opts bits 4..6 = d: warm L2 with the A tile of position i + 128 d
-                // (whichever CTA takes it: positions are taken in order)
-                const int pf = (opts >> 4) & 7;
-                if (pf) {
-                    bool pb;
-                    int64_t pbb;
-                    int ppart;
-                    const int64_t ip = i + 128 * pf;
-                    if (ip < ntasks) {
-                        ab_decode(ip, batch, Dp, pb, pbb, ppart);
-                        if (!pb) tmaops::prefetch3(&map_x, ppart * 16, 0, (int)pbb);
-                    }
                 }
             }
         } else {  // ---- signaller ----

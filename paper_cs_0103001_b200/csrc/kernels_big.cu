@@ -69,9 +69,7 @@ cudaError_t big_pass(const void* in, void* out, double scale, const void* tw, co
              enc3(&mr, ring, 128, 16, (uint64_t)256 * R, 128, 2048, 128, 16, 2);
     }
     if (!ok) return cudaErrorInvalidValue;
-    const char* pv2 = getenv("B200FFT_BIG_PF");
-    const char* bv = getenv("B200FFT_BIG_BULK");
-    BigCtl c{ctr, ctr + GROUPS, next, D, R, pv2 ? atoi(pv2) : 0, bv ? atoi(bv) : 1};
+    BigCtl c{ctr, ctr + GROUPS, next, D, R};
     float a_scale = (float)scale;
     float2* a_ring = ring;
     float2* a_out = reinterpret_cast<float2*>(out);

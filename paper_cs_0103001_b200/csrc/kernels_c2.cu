@@ -155,20 +155,13 @@ int64_t ab_launch_grid(int64_t grid, int64_t batch, int64_t D, int NS) {
     return cap < 1 ? 1 : (cap < grid ? cap : grid);
 }
 
-// tuning bits (B200FFT_AB_OPTS; defaults = the measured best):
-//   k_ab_ws: bits 4..6 = L2 tensor prefetch of the A tile d tasks ahead (d = 1:
-//            -1.3%); bit 7 = A twiddles by a 15-step product from two table
-//            entries instead of 16 loads (-4.5%).  Default 144.
-//   k_ab_st: bit 0 = take the next position before the stage is free (+4%),
-//            bit 1 = relaxed dependency polling (+-0), bits 4..6 = L2 prefetch
-//            of the A tile 128 d positions ahead (+1.5%).  Default 0.
+// k_ab_ws's tuning bits (B200FFT_AB_OPTS; default = the measured best, 144):
+// bits 4..6 = L2 tensor prefetch of the A tile d tasks ahead (d = 1: -1.3%);
+// bit 7 = A twiddles by a 15-step product from two table entries instead of
+// 16 loads (-4.5%).  k_ab_st takes none.
 int ab_opts(int kind) {
     const char* v = getenv("B200FFT_AB_OPTS");
-    int o = v ? atoi(v) : (kind == C2_WS ? (128 | 16) : 0);
-    // bit 8 (k_ab_st): no dependency waits -- a timing experiment with WRONG
-    // results, honoured only with B200FFT_ALLOW_WRONG set
-    if ((o & 256) && !getenv("B200FFT_ALLOW_WRONG")) o &= ~256;
-    return o;
+    return kind == C2_WS ? (v ? atoi(v) : (128 | 16)) : 0;
 }
 
 template <bool INV>

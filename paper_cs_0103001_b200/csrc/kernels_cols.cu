@@ -65,16 +65,6 @@ template <typename T, int R> constexpr int cols_w() {
     return cols_budget<T>() / R > 16 ? 16 : (cols_budget<T>() / R < 2 ? 2 : cols_budget<T>() / R);
 }
 
-// tuning knob (B200FFT_COLS_VARIANT, read once): alternative tile widths /
-// registers per thread for the C3 and C4 column lengths
-int cols_variant() {
-    static int v = [] {
-        const char* e = getenv("B200FFT_COLS_VARIANT");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
-
 template <typename T, int R, int MODE, int W = cols_w<T, R>(), int E = cols_e<T, R>(), int MINB = 0>
 cudaError_t cols_t(const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
                    const FilterArgs& f, cudaStream_t st) {
@@ -103,21 +93,9 @@ cudaError_t cols_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg
         B200_COLS_CASE(32) B200_COLS_CASE(64) B200_COLS_CASE(128) B200_COLS_CASE(256)
         B200_COLS_CASE(512) B200_COLS_CASE(1024) B200_COLS_CASE(4096)
 #undef B200_COLS_CASE
-        case 2048:
-            if constexpr (sizeof(T) == 4) {
-                switch (cols_variant()) {
-                    case 1: return cols_t<T, 2048, MODE, 4, 32>(in, out, S, nimg, scale, tw, f, st);
-                    case 2: return cols_t<T, 2048, MODE, 4, 16>(in, out, S, nimg, scale, tw, f, st);
-                    case 3: return cols_t<T, 2048, MODE, 8, 16>(in, out, S, nimg, scale, tw, f, st);
-                    default: break;
-                }
-            }
-            return cols_t<T, 2048, MODE>(in, out, S, nimg, scale, tw, f, st);
+        case 2048: return cols_t<T, 2048, MODE>(in, out, S, nimg, scale, tw, f, st);
         case 8192:
-            if constexpr (sizeof(T) == 4) {
-                if (cols_variant() == 2) return cols_t<T, 8192, MODE, 2, 16>(in, out, S, nimg, scale, tw, f, st);
-                return cols_t<T, 8192, MODE>(in, out, S, nimg, scale, tw, f, st);
-            }
+            if constexpr (sizeof(T) == 4) return cols_t<T, 8192, MODE>(in, out, S, nimg, scale, tw, f, st);
             return cudaErrorInvalidValue;
         default: return cudaErrorInvalidValue;
     }
@@ -125,39 +103,15 @@ cudaError_t cols_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg
 
 }  // namespace
 
-// four-step column passes: short columns, so narrower tiles and a deeper
-// ring keep more HBM bytes in flight per SM (B200FFT_COLS4_CFG picks one)
+// four-step column passes (N = 4096 columns, and column slabs whose width is
+// not a power of two): per-CTA k_cols tiles of 16 columns, E = 16; the
+// 128-point fwd * g * inv pass capped at 56 registers (9 CTAs/SM) -- the
+// measured best of the tile / ring / register configurations (profiles/README.md)
 template <int MODE>
 cudaError_t cols4_r(int64_t R, const void* in, void* out, int64_t S, int64_t nimg, double scale, const void* tw,
                     const FilterArgs& f, cudaStream_t st) {
-    static const int cfg = [] {
-        const char* v = getenv("B200FFT_COLS4_CFG");
-        return v ? atoi(v) : 8;  // 8: k_cols, E = 16, 16-column tiles, the 128-point pass at 9 CTAs/SM (measured best)
-    }();
-    if (cfg == 0) {  // per-CTA tiles (k_cols): many CTAs per SM, twiddles by recurrence
-        if (R == 64) return cols_t<float, 64, MODE>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128) return cols_t<float, 128, MODE>(in, out, S, nimg, scale, tw, f, st);
-    } else if (cfg == 5) {  // E = 16 (8 threads per 128-point line)
-        if (R == 64) return cols_t<float, 64, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128) return cols_t<float, 128, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
-    } else if (cfg >= 7 && cfg <= 9) {  // as 5, the 128-point pass capped at 64 / 56 / 48 registers (8 / 9 / 10 CTAs/SM)
-        if (R == 64) return cols_t<float, 64, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128 && cfg == 7) return cols_t<float, 128, MODE, 16, 16, 8>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128 && cfg == 8) return cols_t<float, 128, MODE, 16, 16, 9>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128) return cols_t<float, 128, MODE, 16, 16, 10>(in, out, S, nimg, scale, tw, f, st);
-    } else if (cfg == 6) {  // E = 16, 32 columns per tile
-        if (R == 64) return cols_t<float, 64, MODE, 32, 16>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128) return cols_t<float, 128, MODE, 32, 16>(in, out, S, nimg, scale, tw, f, st);
-    } else if (cfg == 1) {
-        if (R == 64) return cols_pipe_t<64, MODE, 32, 4>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128) return cols_pipe_t<128, MODE, 16, 4>(in, out, S, nimg, scale, tw, f, st);
-    } else if (cfg == 2) {
-        if (R == 64) return cols_pipe_t<64, MODE, 16, 4>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128) return cols_pipe_t<128, MODE, 16, 3>(in, out, S, nimg, scale, tw, f, st);
-    } else if (cfg == 3) {
-        if (R == 64) return cols_pipe_t<64, MODE, 32, 6>(in, out, S, nimg, scale, tw, f, st);
-        if (R == 128) return cols_pipe_t<128, MODE, 32, 4>(in, out, S, nimg, scale, tw, f, st);
-    }
+    if (R == 64) return cols_t<float, 64, MODE, 16, 16>(in, out, S, nimg, scale, tw, f, st);
+    if (R == 128) return cols_t<float, 128, MODE, 16, 16, 9>(in, out, S, nimg, scale, tw, f, st);
     return cols_pipe_r<MODE>(R, in, out, S, nimg, scale, tw, f, st);
 }
 
@@ -168,17 +122,6 @@ cudaError_t launch_cols_fourstep(int mode, int64_t R, const void* in, void* out,
         case 2: return cols4_r<2>(R, in, out, S, nimg, scale, tw, f, st);
         case 3: return cols4_r<3>(R, in, out, S, nimg, scale, tw, f, st);
         case 4: return cols4_r<4>(R, in, out, S, nimg, scale, tw, f, st);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-cudaError_t launch_cols_fourstep_default(int mode, int64_t R, const void* in, void* out, int64_t S, int64_t nimg,
-                                         double scale, const void* tw, const FilterArgs& f, cudaStream_t st) {
-    if (R < 64 || R > 4096) return cudaErrorInvalidValue;
-    switch (mode) {
-        case 2: return cols_pipe_r<2>(R, in, out, S, nimg, scale, tw, f, st);
-        case 3: return cols_pipe_r<3>(R, in, out, S, nimg, scale, tw, f, st);
-        case 4: return cols_pipe_r<4>(R, in, out, S, nimg, scale, tw, f, st);
         default: return cudaErrorInvalidValue;
     }
 }

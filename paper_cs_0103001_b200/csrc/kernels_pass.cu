@@ -1,6 +1,6 @@
 // kernels_pass.cu -- instantiations and launcher of kernel family C (one
 // global Stockham pass of a multi-pass transform, L > 8192).
-#include "fft_pass_pipe.cuh"
+#include "fft_engine.cuh"
 #include "launch.h"
 
 namespace b200fft {
@@ -32,113 +32,10 @@ cudaError_t pass_t(const void* in, void* out, int64_t L, int64_t Ns, int64_t bat
     return cudaGetLastError();
 }
 
-// persistent cp.async double-buffered form (fft_pass_pipe.cuh); complex64
-template <typename T, int R, int W, bool INV>
-cudaError_t pass_pipe_t(const void* in, void* out, int64_t L, int64_t Ns, int64_t batch, double scale,
-                        const void* tw, const void* pa, const void* pb, int klo_sh, cudaStream_t st) {
-    constexpr int E = 16;
-    constexpr int TPL = R / E;
-    using G = PassPipeCfg<T, R, W>;
-    auto kern = k_pass_pipe<T, R, E, W, INV>;
-    int grid_max = 0;
-    {
-        cudaError_t e = kernel_setup((const void*)kern, W * TPL, G::SMEM_BYTES, &grid_max);
-        if (e != cudaSuccess) return e;
-    }
-    if (batch <= 0) return cudaSuccess;
-    const int64_t LR = L / R;
-    if (LR % W != 0 || (Ns > 1 && Ns < W)) return cudaErrorInvalidValue;
-    const int64_t nlines = batch * LR;
-    const int64_t ntiles = nlines / W;
-    const int64_t grid = ntiles < grid_max ? ntiles : grid_max;
-    kern<<<(unsigned)grid, W * TPL, G::SMEM_BYTES, st>>>(
-        reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<cpx<T>*>(out), L, Ns, nlines, (T)scale,
-        reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), reinterpret_cast<const cpx<T>*>(pa),
-        reinterpret_cast<const cpx<T>*>(pb), klo_sh);
-    return cudaGetLastError();
-}
-
-// TMA-bulk-fed form (fft_pass_pipe.cuh k_pass_tma); complex64
-template <typename T, int R, int W, bool INV>
-cudaError_t pass_tma_t(const void* in, void* out, int64_t L, int64_t Ns, int64_t batch, double scale,
-                       const void* tw, const void* pa, const void* pb, int klo_sh, cudaStream_t st) {
-    constexpr int E = 16;
-    constexpr int TPL = R / E;
-    using G = PassTmaCfg<T, R, W>;
-    auto kern = k_pass_tma<T, R, E, W, INV>;
-    int grid_max = 0;
-    {
-        cudaError_t e = kernel_setup((const void*)kern, W * TPL, G::SMEM_BYTES, &grid_max);
-        if (e != cudaSuccess) return e;
-    }
-    if (batch <= 0) return cudaSuccess;
-    const int64_t LR = L / R;
-    if (LR % W != 0 || (Ns > 1 && Ns < W)) return cudaErrorInvalidValue;
-    const int64_t nlines = batch * LR;
-    const int64_t ntiles = nlines / W;
-    const int64_t grid = ntiles < grid_max ? ntiles : grid_max;
-    kern<<<(unsigned)grid, W * TPL, G::SMEM_BYTES, st>>>(
-        reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<cpx<T>*>(out), L, Ns, nlines, (T)scale,
-        reinterpret_cast<const cpx<T>*>(tw) + tw_base(R), reinterpret_cast<const cpx<T>*>(pa),
-        reinterpret_cast<const cpx<T>*>(pb), klo_sh);
-    return cudaGetLastError();
-}
-
 template <typename T, bool INV>
 cudaError_t pass_r(int64_t R, const void* in, void* out, int64_t L, int64_t Ns, int64_t batch,
                    double scale, const void* tw, const void* pa, const void* pb, int klo_sh,
                    cudaStream_t st) {
-    static const int pipe = [] {
-        const char* v = getenv("B200FFT_PASS_PIPE");
-        return v ? atoi(v) : 4;  // 4: k_pass everywhere (with twiddle recurrences it streams at 5-6 TB/s)
-    }();
-    if constexpr (sizeof(T) == 4) {
-        if (pipe == 5) {  // TMA-bulk-fed tiles
-            switch (R) {
-                case 256: return pass_tma_t<T, 256, 32, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                case 512: return pass_tma_t<T, 512, 16, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                case 1024: return pass_tma_t<T, 1024, 8, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                default: break;
-            }
-        }
-        // radix <= 256 passes: pipelined, 32 / 64 lines per tile (256-B / 512-B runs)
-        if (pipe != 4 && pipe != 6 && pipe != 7) {
-            switch (R) {
-                case 128: return pass_pipe_t<T, 128, 64, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                case 256: return pass_pipe_t<T, 256, 32, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                case 512: return pass_pipe_t<T, 512, 16, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                default: break;
-            }
-        }
-        if (pipe == 6 || pipe == 7) {  // per-CTA k_pass with 32 lines per tile (256-B runs); 7: 64 for radix 128
-            switch (R) {
-                case 128:
-                    if (pipe == 7) return pass_t<T, 128, INV, 64>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                    return pass_t<T, 128, INV, 32>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                case 256: return pass_t<T, 256, INV, 32>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                default: break;
-            }
-        }
-        if (pipe == 1) {
-            switch (R) {
-                case 512: return pass_pipe_t<T, 512, 16, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                case 1024: return pass_pipe_t<T, 1024, 8, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                default: break;
-            }
-        } else if (pipe == 3) {
-            switch (R) {
-                case 512: return pass_t<T, 512, INV, 32>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                case 1024: return pass_t<T, 1024, INV, 16>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                default: break;
-            }
-        } else if (pipe == 2) {
-            switch (R) {
-                case 512: return pass_pipe_t<T, 512, 8, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                case 1024: return pass_pipe_t<T, 1024, 4, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
-                default: break;
-            }
-        }
-    }
     switch (R) {
         case 128: return pass_t<T, 128, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);
         case 256: return pass_t<T, 256, INV>(in, out, L, Ns, batch, scale, tw, pa, pb, klo_sh, st);

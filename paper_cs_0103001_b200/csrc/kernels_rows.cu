@@ -117,26 +117,6 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     return cudaGetLastError();
 }
 
-// B200FFT_ROWS_E=8: the 2048- and 8192-point row kernels with 8 values per
-// thread (radix-8 steps, twice the threads per row) -- a tuning knob
-int rows_e() {
-    static const int v = [] {
-        const char* e = getenv("B200FFT_ROWS_E");
-        return e ? atoi(e) : 16;
-    }();
-    return v;
-}
-
-// B200FFT_ROWS_STAGE_KB=16|32: smaller stages for the 2048-point transposed
-// filter rows (measured slower; 64 KiB default)
-int rows_stage_kb() {
-    static const int v = [] {
-        const char* e = getenv("B200FFT_ROWS_STAGE_KB");
-        return e ? atoi(e) : 64;
-    }();
-    return v;
-}
-
 template <bool INV, bool REAL_IN, bool FILT>
 cudaError_t rows_tma_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw,
                        const void* rowfilt, cudaStream_t st) {
@@ -144,20 +124,9 @@ cudaError_t rows_tma_r(int64_t R, const void* in, void* out, int64_t batch, doub
         case 256: return rows_tma_t<float, 256, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         case 512: return rows_tma_t<float, 512, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         case 1024: return rows_tma_t<float, 1024, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
-        case 2048:
-            if (rows_e() == 8)
-                return rows_tma_t<float, 2048, INV, REAL_IN, FILT, false, false, 8>(in, out, batch, scale, tw, rowfilt,
-                                                                                 st);
-            return rows_tma_t<float, 2048, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 2048: return rows_tma_t<float, 2048, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         case 4096: return rows_tma_t<float, 4096, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
-        case 8192:
-            if (rows_e() == 8)
-                return rows_tma_t<float, 8192, INV, REAL_IN, FILT, false, false, 8>(in, out, batch, scale, tw, rowfilt,
-                                                                                 st);
-            if (rows_e() == 2)
-                return rows_tma_t<float, 8192, INV, REAL_IN, FILT, false, false, 16, 2>(in, out, batch, scale, tw,
-                                                                                     rowfilt, st);
-            return rows_tma_t<float, 8192, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
+        case 8192: return rows_tma_t<float, 8192, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -181,16 +150,6 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
         case 1024:
             return rows_tma_t<float, 1024, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st, pdl);
         case 2048:
-            if (rows_e() == 8)
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 8>(in, out, batch, scale, tw, rowfilt, st, pdl);
-            if (rows_e() == 2)
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 2>(in, out, batch, scale, tw, rowfilt, st, pdl);
-            if (rows_stage_kb() == 323)  // 3 CTAs/SM x 2 stages of 32 KiB (2 rows)
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 3, 32>(in, out, batch, scale, tw, rowfilt, st, pdl);
-            if (rows_stage_kb() == 32)  // 32 KiB stages (2 rows): two CTAs per SM
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 32>(in, out, batch, scale, tw, rowfilt, st, pdl);
-            if (rows_stage_kb() == 16)  // 16 KiB stages (1 row): four CTAs per SM by shared memory
-                return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR, 16, 1, 16>(in, out, batch, scale, tw, rowfilt, st, pdl);
             return rows_tma_t<float, 2048, false, REAL_IN, true, true, PAIR>(in, out, batch, scale, tw, rowfilt, st, pdl);
         default: return cudaErrorInvalidValue;
     }

@@ -33,7 +33,7 @@ def run(N, real, reps=20, real_out=False):
     ts.sort()
     med = ts[len(ts) // 2]
     alg = (16.0 if real_out else 32.0) * N * N
-    print(f"N={N} real={real} real_out={real_out} cols_variant={os.environ.get('B200FFT_COLS_VARIANT', '0')}: "
+    print(f"N={N} real={real} real_out={real_out}: "
           f"median {med * 1e3:.1f} us  min {ts[0] * 1e3:.1f} us  hbm_frac {alg / (med / 1e3) / 1e9 / 6554.6:.3f}",
           flush=True)
 
