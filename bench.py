@@ -163,10 +163,24 @@ def _free_port():
 
 
 def torchrun(n, argv, timeout=None):
-    """Run bench.py with `argv` under torch.distributed.run, n ranks."""
+    """Run bench.py with `argv` under torch.distributed.run, n ranks.  With a
+    timeout the job runs in its own process group, killed whole (launcher and
+    ranks) when the timeout expires, so no rank keeps a GPU afterwards."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *argv]
-    return subprocess.run(cmd, cwd=ROOT, capture_output=timeout is not None, text=True, timeout=timeout)
+    if timeout is None:
+        return subprocess.run(cmd, cwd=ROOT)
+    proc = subprocess.Popen(cmd, cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                            start_new_session=True)
+    try:
+        out, err = proc.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        import signal
+
+        os.killpg(proc.pid, signal.SIGKILL)
+        proc.communicate()
+        raise
+    return subprocess.CompletedProcess(cmd, proc.returncode, out, err)
 
 
 def dist_init():
@@ -846,17 +860,18 @@ def _extra(name, fn, *a):
 
 def sharded_extras(args, ws):
     """N > 1: the sharded C4 / C5 in a child torchrun job over the same GPUs
-    (bounded by a timeout, so a failure there cannot void the C2 line)."""
+    (bounded by a 240 s timeout that kills the whole job, so a failure there
+    can neither void the C2 line nor leave a rank holding a GPU)."""
     out = {}
     for cfg in ("C4", "C5"):
         try:
             r = torchrun(ws, ["--config", cfg, "--gpus", str(ws), "--steps", str(max(3, min(args.steps, 10))),
-                              "--warmup", "3"], timeout=600)
+                              "--warmup", "3"], timeout=240)
             lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
             out[cfg] = json.loads(lines[-1]) if (r.returncode == 0 and lines) else \
                 {"error": f"rc={r.returncode}: {r.stderr[-400:]}"}
         except subprocess.TimeoutExpired:
-            out[cfg] = {"error": "timed out after 600 s"}
+            out[cfg] = {"error": "timed out after 240 s (job killed)"}
     return out
 
 
