@@ -567,3 +567,58 @@ def test_gloo_paper_tree_protocol(world):
         pr.join(timeout=60)
         assert pr.exitcode == 0
     assert res[0] <= 1e-13, res
+
+
+@pytest.mark.gpu
+def test_virtual_rank_count_change_rebuilds_the_four_step():
+    """Changing the rank count after a first distributed call rebuilds the
+    four-step sub-plans (their batches are N1 / P and N2 / P): P = 2, then 4,
+    then 1 (the local path), each against the oracle."""
+    b = _lib()
+    n = 1 << 16
+    x = fixtures.complex_input(n, fixtures.NORMAL, seed=640, dtype=np.complex64)
+    ref = oracle.fft(x)
+    p = b.Plan((n,), batch=1)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    for P in (2, 4, 1):
+        p.set_virtual_ranks(P)
+        p.forward(xd, yd)
+        torch.cuda.synchronize()
+        assert oracle.rel_l2(yd.cpu().numpy(), ref) <= 1e-5, P
+    p.destroy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["2d", "1d"])
+def test_phase_timing(kind):
+    """fft_plan_set_profiling / fft_plan_phase_times: one labelled device time
+    per phase of the distributed schedules (the exchange phases carry
+    "exchange"), one phase for a local call, none when profiling is off."""
+    b = _lib()
+    if kind == "2d":
+        N = M = 1024
+        p = b.Plan((N, M), batch=1)
+        p.set_virtual_ranks(4)
+        x = torch.from_numpy(fixtures.complex_input(N * M, 0, seed=650).reshape(N, M)).cuda()
+        run = lambda: p.filter_pipeline(x, torch.empty_like(x), b.FILTER_GAUSS, 0.1)  # noqa: E731
+    else:
+        n = 1 << 20
+        p = b.Plan((n,), batch=1)
+        p.set_virtual_ranks(4)
+        x = torch.from_numpy(fixtures.complex_input(n, 1, seed=651)).cuda()
+        run = lambda: p.forward(x, torch.empty_like(x))  # noqa: E731
+    run()
+    assert p.phase_times() == []
+    p.set_profiling(True)
+    run()
+    ph = p.phase_times()
+    assert len(ph) >= 3 and all(t >= 0.0 for _, t in ph)
+    assert any("exchange" in lab for lab, _ in ph) and all(lab for lab, _ in ph)
+    q = b.Plan((4096,), batch=8)
+    q.set_profiling(True)
+    y = torch.from_numpy(fixtures.complex_input(8 * 4096, 1, seed=652)).cuda()
+    q.forward(y, torch.empty_like(y))
+    assert [lab for lab, _ in q.phase_times()] == ["forward"]
+    p.destroy()
+    q.destroy()
