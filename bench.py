@@ -239,11 +239,14 @@ def cpu_model():
 
 
 def timed(stream, fn, reps, flush=None):
-    """Per-rep CUDA-event times (ms) of fn() on `stream`; flush (a buffer
-    larger than L2) is zeroed on the same stream before each rep, outside
-    the timed region.  All reps are enqueued back to back and synchronised
-    once, so host-side launch jitter (e.g. the clock sampler's NVML calls)
-    never leaves the GPU idle inside a timed region."""
+    """Per-rep CUDA-event times (ms) of fn() on `stream`.  Cold L2: before
+    each rep, outside the timed region, a 512 MiB buffer (> 126 MB L2) is
+    zeroed on the same stream and then a 256 MiB slice of it is read back,
+    so L2 holds none of the config's data and none of the flush's dirty lines
+    (whose write-back would otherwise land in the timed region: +2 us on
+    C3).  All reps are enqueued back to back and synchronised once, so host
+    jitter (e.g. the clock sampler's NVML calls) never idles the GPU inside a
+    timed region."""
     import torch
 
     evs = []
@@ -252,6 +255,7 @@ def timed(stream, fn, reps, flush=None):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if flush is not None:
                 flush.zero_()
+                flush[: flush.numel() // 2].sum()
             s.record(stream)
             fn()
             e.record(stream)
@@ -447,7 +451,7 @@ def bench_c1(args, local):
 
 def bench_c3(args, local, real_out=False):
     """C3 (BASELINE configs[2]); real_out: the NEXT-3 real-to-real form of the
-    same pipeline (float32 out).  Cold L2 (512 MiB memset before each rep)."""
+    same pipeline (float32 out).  Cold L2 (see `timed`)."""
     import torch
 
     import paper_cs_0103001_b200 as b

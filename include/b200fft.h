@@ -216,7 +216,7 @@ fft_status fft_forward_paper_tree(fft_plan plan, const void* in, void* out);
 
 /* End-to-end call on HOST buffers (pageable or pinned): copies the input
  * host->device, transforms, copies the result device->host, pipelined over
- * batch chunks (B200FFT_HOST_CHUNK_MB, default 64 MiB) on two plan-owned
+ * batch chunks (B200FFT_HOST_CHUNK_MB, default 64 MiB) on three plan-owned
  * streams: chunk c's copies overlap chunk c - 1's compute, while the computes
  * run one after another (they share the plan's workspace); returns after the
  * result is in host_out.  direction: +1 forward, -1 inverse, 0 filter

@@ -147,12 +147,13 @@ struct fft_plan_s {
     size_t ws_bytes = 0;
     bool ws_owned = false;
     // host-execution staging buffers
-    void* hbuf[2] = {nullptr, nullptr};   // device output staging per stream
-    void* hbin[2] = {nullptr, nullptr};   // device input staging per stream
+    static constexpr int kHS = 3;          // host-execution streams (chunks round robin)
+    void* hbuf[kHS] = {};                  // device output staging per stream
+    void* hbin[kHS] = {};                  // device input staging per stream
     size_t hbuf_bytes = 0;
-    cudaStream_t hstream[2] = {nullptr, nullptr};
+    cudaStream_t hstream[kHS] = {};
     cudaEvent_t hev = nullptr;
-    cudaEvent_t hcomp[2] = {nullptr, nullptr};  // end of a chunk's compute (fft_execute_host)
+    cudaEvent_t hcomp[kHS] = {};  // end of a chunk's compute (fft_execute_host)
     int last_launches = 0;
     // distributed (slab decomposition of rank-2 plans)
     int nranks = 1, my_rank = 0;
@@ -1868,42 +1869,43 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
     const size_t chunk_bytes = (size_t)(per * unit) * eb;
     cudaError_t e;
     if (p->hbuf_bytes < chunk_bytes) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < fft_plan_s::kHS; ++i) {
             if (p->hbuf[i]) cudaFree(p->hbuf[i]);
             if (p->hbin[i]) cudaFree(p->hbin[i]);
             p->hbuf[i] = p->hbin[i] = nullptr;
         }
         p->hbuf_bytes = 0;
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < fft_plan_s::kHS; ++i) {
             e = cudaMalloc(&p->hbuf[i], chunk_bytes);
             if (e == cudaSuccess) e = cudaMalloc(&p->hbin[i], chunk_bytes);
             if (e != cudaSuccess) return fail(FFT_E_ALLOC, "host-execution staging buffers");
         }
         p->hbuf_bytes = chunk_bytes;
     }
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < fft_plan_s::kHS; ++i)
         if (!p->hstream[i]) {
             e = cudaStreamCreateWithFlags(&p->hstream[i], cudaStreamNonBlocking);
             if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
         }
     if (!p->hev) {
         e = cudaEventCreateWithFlags(&p->hev, cudaEventDisableTiming);
-        for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&p->hcomp[i], cudaEventDisableTiming);
+        for (int i = 0; i < fft_plan_s::kHS && e == cudaSuccess; ++i)
+            e = cudaEventCreateWithFlags(&p->hcomp[i], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
     }
     // order after the work already queued on the plan stream
     e = cudaEventRecord(p->hev, p->stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->hstream[0], p->hev, 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->hstream[1], p->hev, 0);
+    for (int i = 0; i < fft_plan_s::kHS && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->hstream[i], p->hev, 0);
     if (e != cudaSuccess) return cuda_fail(e, "stream ordering");
     const int64_t saved_batch = p->batch;
     int launches = 0;
     fft_status s = FFT_OK;
     for (int64_t u0 = 0, c = 0; u0 < units && s == FFT_OK; u0 += per, ++c) {
         const int64_t nu = (units - u0) < per ? (units - u0) : per;
-        cudaStream_t st = p->hstream[c & 1];
-        void* d = p->hbuf[c & 1];
-        void* din = p->hbin[c & 1];
+        const int hs = (int)(c % fft_plan_s::kHS);
+        cudaStream_t st = p->hstream[hs];
+        void* d = p->hbuf[hs];
+        void* din = p->hbin[hs];
         e = cudaMemcpyAsync(din, (const char*)host_in + (size_t)(u0 * unit) * in_eb, (size_t)(nu * unit) * in_eb,
                             cudaMemcpyHostToDevice, st);
         if (e != cudaSuccess) {
@@ -1912,10 +1914,11 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
         }
         // the chunks' computes share the plan's workspace (the C2 ring and
         // counters, the 2D intermediate grid, the pass ping-pong buffer):
-        // chunk c's compute starts after chunk c - 1's, on the other stream;
-        // only the copies overlap the compute
+        // chunk c's compute starts after chunk c - 1's; with three streams the
+        // H2D copy of chunk c + 1 and the D2H copy of chunk c - 1 both run
+        // under chunk c's compute (PCIe in both directions at once)
         if (c > 0) {
-            e = cudaStreamWaitEvent(st, p->hcomp[(c - 1) & 1], 0);
+            e = cudaStreamWaitEvent(st, p->hcomp[(c - 1) % fft_plan_s::kHS], 0);
             if (e != cudaSuccess) {
                 s = cuda_fail(e, "chunk ordering");
                 break;
@@ -1929,7 +1932,7 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
         launches += p->last_launches;
         p->batch = saved_batch;
         if (s != FFT_OK) break;
-        e = cudaEventRecord(p->hcomp[c & 1], st);
+        e = cudaEventRecord(p->hcomp[hs], st);
         if (e != cudaSuccess) {
             s = cuda_fail(e, "chunk ordering");
             break;
@@ -1939,11 +1942,13 @@ fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void
         if (e != cudaSuccess) s = cuda_fail(e, "D2H copy");
     }
     p->last_launches = launches;
-    cudaError_t e0 = cudaStreamSynchronize(p->hstream[0]);
-    cudaError_t e1 = cudaStreamSynchronize(p->hstream[1]);
+    cudaError_t es = cudaSuccess;
+    for (int i = 0; i < fft_plan_s::kHS; ++i) {
+        cudaError_t ei = cudaStreamSynchronize(p->hstream[i]);
+        if (es == cudaSuccess) es = ei;
+    }
     if (s != FFT_OK) return s;
-    if (e0 != cudaSuccess) return cuda_fail(e0, "host execution");
-    if (e1 != cudaSuccess) return cuda_fail(e1, "host execution");
+    if (es != cudaSuccess) return cuda_fail(es, "host execution");
     return FFT_OK;
 }
 
@@ -2075,14 +2080,14 @@ fft_status fft_plan_destroy(fft_plan p) {
     if (p->gu) cudaFree(p->gu);
     if (p->gv) cudaFree(p->gv);
     if (p->ws_owned && p->ws) cudaFree(p->ws);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < fft_plan_s::kHS; ++i) {
         if (p->hbuf[i]) cudaFree(p->hbuf[i]);
         if (p->hbin[i]) cudaFree(p->hbin[i]);
         if (p->hstream[i]) cudaStreamDestroy(p->hstream[i]);
     }
     if (p->hev) cudaEventDestroy(p->hev);
     for (cudaEvent_t ev : p->pev) cudaEventDestroy(ev);
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < fft_plan_s::kHS; ++i)
         if (p->hcomp[i]) cudaEventDestroy(p->hcomp[i]);
 #ifdef B200FFT_WITH_NCCL
     p2p_release(p);
