@@ -28,6 +28,8 @@
 #include <nccl.h>  // the torch wheel's NCCL 2.28 (not /usr/include's 2.27)
 #endif
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys / ncu --nvtx
+
 #include "../../include/b200fft.h"
 #include "fft_engine.cuh"
 #include "launch.h"
@@ -40,6 +42,12 @@ using namespace b200fft;
 namespace {
 
 thread_local std::string g_last_error;
+
+// an NVTX range around each public entry point (a no-op without a tool)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 fft_status fail(fft_status s, const std::string& msg) {
     g_last_error = msg;
@@ -1715,9 +1723,13 @@ static fft_status exec_body(fft_plan p, const void* in, void* out, bool inv) {
     return s == FFT_OK ? dist_check(p) : s;
 }
 
-fft_status fft_forward(fft_plan p, const void* in, void* out) { return exec(p, in, out, false); }
+fft_status fft_forward(fft_plan p, const void* in, void* out) {
+    NvtxRange r("b200fft.forward");
+    return exec(p, in, out, false);
+}
 
 fft_status fft_forward_paper_tree(fft_plan p, const void* in, void* out) {
+    NvtxRange nvtx("b200fft.forward_paper_tree");
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (p->rank != 1 || p->batch != 1) return fail(FFT_E_INVALID_ARG, "the paper's schedule needs a single 1D transform");
     if (!in) return fail(FFT_E_INVALID_ARG, "null input");
@@ -1731,7 +1743,10 @@ fft_status fft_forward_paper_tree(fft_plan p, const void* in, void* out) {
     fft_status s = run_paper_tree(p, in, master ? out : nullptr, p->stream);
     return s == FFT_OK ? dist_check(p) : s;
 }
-fft_status fft_inverse(fft_plan p, const void* in, void* out) { return exec(p, in, out, true); }
+fft_status fft_inverse(fft_plan p, const void* in, void* out) {
+    NvtxRange r("b200fft.inverse");
+    return exec(p, in, out, true);
+}
 
 static fft_status check_real(fft_plan p, const void* in, void* out, bool c2r) {
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
@@ -1747,6 +1762,7 @@ static fft_status check_real(fft_plan p, const void* in, void* out, bool c2r) {
 }
 
 fft_status fft_forward_r2c(fft_plan p, const void* in, void* out) {
+    NvtxRange nvtx("b200fft.forward_r2c");
     fft_status s = check_real(p, in, out, false);
     if (s != FFT_OK) return s;
     if (p->elems() == 0) return FFT_OK;
@@ -1757,6 +1773,7 @@ fft_status fft_forward_r2c(fft_plan p, const void* in, void* out) {
 }
 
 fft_status fft_inverse_c2r(fft_plan p, const void* in, void* out) {
+    NvtxRange nvtx("b200fft.inverse_c2r");
     fft_status s = check_real(p, in, out, true);
     if (s != FFT_OK) return s;
     if (p->elems() == 0) return FFT_OK;
@@ -1767,6 +1784,7 @@ fft_status fft_inverse_c2r(fft_plan p, const void* in, void* out) {
 }
 
 fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filter filter, double param) {
+    NvtxRange nvtx("b200fft.filter_pipeline");
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (p->rank != 2) return fail(FFT_E_INVALID_ARG, "fft2d_filter_pipeline needs a rank-2 plan");
     const bool real_in = (p->flags & FFT_IN_REAL_F32) != 0;
@@ -1792,6 +1810,7 @@ fft_status fft2d_filter_pipeline(fft_plan p, const void* in, void* out, fft_filt
 
 fft_status fft2d_image_filter_u8(fft_plan p, const uint8_t* in, int64_t h, int64_t w, uint8_t* out,
                                  fft_filter filter, double param, int max_val, float* spectrum) {
+    NvtxRange nvtx("b200fft.image_filter_u8");
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (p->rank != 2 || p->prec != FFT_C64) return fail(FFT_E_INVALID_ARG, "image filter needs a rank-2 complex64 plan");
     if (p->dist()) return fail(FFT_E_UNSUPPORTED, "image filter on a distributed plan");
@@ -1840,6 +1859,7 @@ fft_status fft2d_image_filter_u8(fft_plan p, const uint8_t* in, int64_t h, int64
 
 fft_status fft_execute_host(fft_plan p, int direction, const void* host_in, void* host_out, fft_filter filter,
                             double param) {
+    NvtxRange nvtx("b200fft.execute_host");
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (!host_in || !host_out) return fail(FFT_E_INVALID_ARG, "null host pointer");
     if (direction == 0 && p->rank != 2) return fail(FFT_E_INVALID_ARG, "pipeline needs a rank-2 plan");
