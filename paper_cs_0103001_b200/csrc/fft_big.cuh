@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(320, 3)
     k_big(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_ring,
           float2* __restrict__ ring, float2* __restrict__ out, float scale, const float2* __restrict__ tw256,
           const float2* __restrict__ tw128, const float2* __restrict__ twl, const float2* __restrict__ whi,
-          const float2* __restrict__ wlo, BigCtl ctl) {
+          const float2* __restrict__ wlo, BigCtl ctl, int xo) {
     using G = BigCfg;
     constexpr int NS = G::NS, NSIG = G::NSIG;
     constexpr int64_t L = G::L, GROUPS = 2048;  // 32768 lines / 16
@@ -218,10 +218,19 @@ __global__ void __launch_bounds__(320, 3)
                 float2 wm = big_w(whi, wlo, n1 * (kc + 256 * lt));
                 const float2 ws = big_w(whi, wlo, n1 * 2048);
                 float2* o = out + (kc + 256 * lt) * L + n1;
+                if (xo & 2) {
 #pragma unroll
-                for (int m = 0; m < 16; ++m) {
-                    st_pol(o + (int64_t)m * 2048 * L, cmul_dir<INV>(v[FB::pos_out(m)], wm), keep);
-                    wm = cmul(wm, ws);
+                    for (int m = 0; m < 16; ++m) {
+                        o[(int64_t)m * 2048 * L] = cmul_dir<INV>(v[FB::pos_out(m)], wm);
+                        wm = cmul(wm, ws);
+                    }
+                } else {
+                    const uint64_t yp = (xo & 1) ? stream : keep;
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) {
+                        st_pol(o + (int64_t)m * 2048 * L, cmul_dir<INV>(v[FB::pos_out(m)], wm), yp);
+                        wm = cmul(wm, ws);
+                    }
                 }
             } else {
                 // [2 kc][16 r][128 a]: lines contiguous.  Step 0 (radix 16,

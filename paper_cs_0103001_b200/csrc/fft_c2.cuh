@@ -357,20 +357,24 @@ __device__ __forceinline__ void st_pol(float2* p, float2 v, uint64_t pol) {
 template <bool INV>
 __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, uint32_t empty, int part, float2* y0,
                                           float scale, const float2* __restrict__ tw4,
-                                          const float2* __restrict__ tw256) {
+                                          const float2* __restrict__ tw256, int xo) {
     float2 v[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
-    dft<16, INV>(v);
-    grp_sync(bar);
+    if (!(xo & 8)) dft<16, INV>(v);
+    if (!(xo & 64)) {
+        grp_sync(bar);
 #pragma unroll
-    for (int q = 0; q < 16; ++q) st[(16 * hi + q) * 16 + lo] = v[q];
-    grp_sync(bar);
+        for (int q = 0; q < 16; ++q) st[(16 * hi + q) * 16 + lo] = v[q];
+        grp_sync(bar);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
+        for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
+    }
     bk_arrive(empty);
-    st_step1_twiddle<INV>(v, hi, tw256);
-    dft<16, INV>(v);
+    if (!(xo & 8)) {
+        st_step1_twiddle<INV>(v, hi, tw256);
+        dft<16, INV>(v);
+    }
     // Y[k2][n1] = v[q] * W_N^{n1 k2} * scale, k2 = hi + 16 q
     const int n1 = part * 16 + lo;
     float2 wm = cscale(__ldg(tw4 + (int64_t)hi * 256 + n1), scale);
@@ -380,31 +384,51 @@ __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, u
     const uint64_t keep = tmaops::policy_evict_last();
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-        st_pol(y + q * 16 * 256, cmul_dir<INV>(v[q], wm), keep);
+        if (!(xo & 2) || v[q].x == 1.2345e-38f) st_pol(y + q * 16 * 256, cmul_dir<INV>(v[q], wm), keep);
         if (q < 15) wm = cmul(wm, ws);
     }
 }
 
 template <bool INV>
 __device__ __forceinline__ void st_task_b(float2* st, int lo, int hi, int bar, uint32_t empty, float2* x0,
-                                          const float2* __restrict__ tw256) {
+                                          const float2* __restrict__ tw256, int xo) {
     float2 v[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = st[hi * 256 + lo + 16 * r];
-    dft<16, INV>(v);
-    grp_sync(bar);
+    if (!(xo & 8)) dft<16, INV>(v);
+    if (!(xo & 64)) {
+        grp_sync(bar);
 #pragma unroll
-    for (int q = 0; q < 16; ++q) st[(16 * lo + q) * 16 + (hi ^ lo)] = v[q];
-    grp_sync(bar);
+        for (int q = 0; q < 16; ++q) st[(16 * lo + q) * 16 + (hi ^ lo)] = v[q];
+        grp_sync(bar);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + (lo ^ r)];
+        for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + (lo ^ r)];
+    }
     bk_arrive(empty);
-    st_step1_twiddle<INV>(v, hi, tw256);
-    dft<16, INV>(v);
+    if (!(xo & 8)) {
+        st_step1_twiddle<INV>(v, hi, tw256);
+        dft<16, INV>(v);
+    }
     float2* x = x0 + lo + (int64_t)hi * 256;
-    const uint64_t stream = tmaops::policy_evict_first();
+    // X is stored without a cache hint: evict-first stores measured 0.7-0.9%
+    // slower (profiles/README.md, round 2 C2 experiments); xo bits 256 / 1024
+    // select the .cs / evict-first / evict-last forms for timing comparisons
+    const uint64_t stream = (xo & 1024) ? tmaops::policy_evict_last() : tmaops::policy_evict_first();
+    if (xo & 2048) {  // timing experiment: each task writes one contiguous 32 KiB block (wrong order)
+        float2* xc = x0 - (x0 - (float2*)nullptr) % 65536 + ((x0 - (float2*)nullptr) % 256) / 16 * 4096 + hi * 16 + lo;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) st_pol(x + q * 16 * 256, v[q], stream);
+        for (int q = 0; q < 16; ++q) st_pol(xc + q * 256, v[q], stream);
+    } else if (xo & 256) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) __stcs(x + q * 16 * 256, v[q]);
+    } else if (xo & (2 | 1024 | 128)) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if (!(xo & 2) || v[q].x == 1.2345e-38f) st_pol(x + q * 16 * 256, v[q], stream);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) x[q * 16 * 256] = v[q];
+    }
 }
 
 template <bool INV, int NS, int MINB>
@@ -439,16 +463,25 @@ __global__ void __launch_bounds__(320, MINB)
         const int lane = tid & 31;
         if (lane != 0) return;
         if (tid < 288) {  // ---- producer ----
-            const uint64_t pol_stream = tmaops::policy_evict_first();
+            const uint64_t pol_stream = (opts & 512) ? tmaops::policy_evict_last() : tmaops::policy_evict_first();
             const uint64_t pol_keep = tmaops::policy_evict_last();
             int na = 0;  // A tasks issued by this CTA
             // (taking the next position before the stage is free, relaxed
             // flag polling and L2 prefetches of later A boxes measured +4%,
             // +-0 and +1.5%: profiles/README.md)
+            int64_t ipair = 0;
             for (int64_t k = 0;; ++k) {
                 const int s = (int)(k % NS);
                 if (k >= NS) bk_wait(empty0 + 8 * s, (uint32_t)(((k / NS) - 1) & 1));
-                const int64_t i = (int64_t)atomicAdd(ctl.next, 1ull);
+                int64_t i;
+                if (opts & 16) {
+                    i = blockIdx.x + k * gridDim.x;
+                } else if (opts & 32) {
+                    if ((k & 1) == 0) ipair = (int64_t)atomicAdd(ctl.next, 2ull);
+                    i = ipair + (k & 1);
+                } else {
+                    i = (int64_t)atomicAdd(ctl.next, 1ull);
+                }
                 task[s] = i;
                 const uint32_t st = s_base + (uint32_t)(s * G::STAGE), bar = full0 + 8 * s;
                 if (i >= ntasks) {  // no more work: the compute warps exit on this stage
@@ -459,18 +492,25 @@ __global__ void __launch_bounds__(320, MINB)
                 int64_t b;
                 int part;
                 ab_decode(i, batch, Dp, isb, b, part);
-                if (!isb) {
+                if (opts & 1) {  // timing experiment: no loads, no dependency waits
+                    if (!isb) {
+                        while (*sigdone < na - NSIG + 1) __nanosleep(20);
+                        ++na;
+                    }
+                    bk_arrive(bar);
+                } else if (!isb) {
                     // a free signal slot for this A task (the signaller is at most
                     // NSIG A tasks behind the compute warps)
                     while (*sigdone < na - NSIG + 1) __nanosleep(20);
                     ++na;
                     // the ring slot's previous transform: all its B parts have read it
-                    if (b >= ctl.ring)
+                    if (b >= ctl.ring && !(opts & 4))
                         while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
                 } else {
-                    while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
+                    if (!(opts & 4))
+                        while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, pol_keep);
@@ -505,7 +545,7 @@ __global__ void __launch_bounds__(320, MINB)
         int part;
         ab_decode(i, batch, Dp, isb, b, part);
         if (!isb) {
-            st_task_a<INV>(st, lo, hi, 1, empty0 + 8 * s, part, ring + (b % ctl.ring) * 65536, scale, tw4, tw256);
+            st_task_a<INV>(st, lo, hi, 1, empty0 + 8 * s, part, ring + (b % ctl.ring) * 65536, scale, tw4, tw256, opts);
             if (tid == 0) sigb[ja % NSIG] = b;
             bk_arrive(sig0 + 8 * (ja % NSIG));  // release: this thread's Y stores
             ++ja;
@@ -513,7 +553,7 @@ __global__ void __launch_bounds__(320, MINB)
             // the stage's Y rows landed (the TMA read is complete): the ring
             // slot's rows are free for the next transform
             if (tid == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;\n" ::"l"(ctl.done_b + b) : "memory");
-            st_task_b<INV>(st, lo, hi, 1, empty0 + 8 * s, out + b * 65536 + part * 16, tw256);
+            st_task_b<INV>(st, lo, hi, 1, empty0 + 8 * s, out + b * 65536 + part * 16, tw256, opts);
         }
     }
     // done: tell the signaller (once its slot is free)
@@ -524,6 +564,5 @@ __global__ void __launch_bounds__(320, MINB)
     grp_sync(1);
     bk_arrive(sig0 + 8 * (ja % NSIG));
 }
-
 
 }  // namespace b200fft

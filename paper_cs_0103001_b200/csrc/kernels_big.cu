@@ -78,7 +78,14 @@ cudaError_t big_pass(const void* in, void* out, double scale, const void* tw, co
     const float2* a_twl = reinterpret_cast<const float2*>(twl);
     const float2* a_hi = reinterpret_cast<const float2*>(whi);
     const float2* a_lo = reinterpret_cast<const float2*>(wlo);
-    void* args[] = {&mi, &mr, &a_ring, &a_out, &a_scale, &a_tw256, &a_tw128, &a_twl, &a_hi, &a_lo, &c};
+    // B200FFT_BIG_XO (tuning): pass 1's Y stores 0 = evict-last, 1 = evict-first,
+    // 2 = without a cache hint (default: C5 19.97 / 19.69 / 19.69 ms fwd + inv)
+    static const int xo = [] {
+        const char* v = getenv("B200FFT_BIG_XO");
+        return v ? atoi(v) : 2;
+    }();
+    int a_xo = xo;
+    void* args[] = {&mi, &mr, &a_ring, &a_out, &a_scale, &a_tw256, &a_tw128, &a_twl, &a_hi, &a_lo, &c, &a_xo};
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;

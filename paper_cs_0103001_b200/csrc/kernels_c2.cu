@@ -158,10 +158,22 @@ int64_t ab_launch_grid(int64_t grid, int64_t batch, int64_t D, int NS) {
 // k_ab_ws's tuning bits (B200FFT_AB_OPTS; default = the measured best, 144):
 // bits 4..6 = L2 tensor prefetch of the A tile d tasks ahead (d = 1: -1.3%);
 // bit 7 = A twiddles by a 15-step product from two table entries instead of
-// 16 loads (-4.5%).  k_ab_st takes none.
+// 16 loads (-4.5%).  k_ab_st takes only experiment bits (B200FFT_AB_XOPTS,
+// honoured only with B200FFT_ALLOW_WRONG=1; profiles/README.md "C2 bound"):
+// wrong results: 1 = no loads / dependency waits, 2 = no stores, 4 = no
+// dependency waits, 8 = no FFT arithmetic, 64 = no step-0 -> 1 exchange,
+// 2048 = each B task stores one contiguous 32 KiB block; correct results:
+// 16 = static round-robin positions, 32 = two positions per atomic, 128 /
+// 256 / 1024 = X stores evict-first / .cs / evict-last (default: no hint),
+// 512 = A loads evict-last.
 int ab_opts(int kind) {
-    const char* v = getenv("B200FFT_AB_OPTS");
-    return kind == C2_WS ? (v ? atoi(v) : (128 | 16)) : 0;
+    if (kind == C2_WS) {
+        const char* v = getenv("B200FFT_AB_OPTS");
+        return v ? atoi(v) : (128 | 16);
+    }
+    const char* w = getenv("B200FFT_ALLOW_WRONG");
+    const char* x = getenv("B200FFT_AB_XOPTS");
+    return (w && w[0] == '1' && x) ? atoi(x) : 0;
 }
 
 template <bool INV>

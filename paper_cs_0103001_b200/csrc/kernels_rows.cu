@@ -100,6 +100,13 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     cpx<T>* a_out = reinterpret_cast<cpx<T>*>(out);
     const cpx<T>* a_tw = reinterpret_cast<const cpx<T>*>(tw) + tw_base(R, ml_of(E));
     const T* a_filt = reinterpret_cast<const T*>(rowfilt);
+    // timing experiments (wrong results): B200FFT_ROWS_XO with B200FFT_ALLOW_WRONG=1;
+    // 1 = no FFT arithmetic / exchanges, 2 = no stores
+    static const int xo = [] {
+        const char* w = getenv("B200FFT_ALLOW_WRONG");
+        const char* v = getenv("B200FFT_ROWS_XO");
+        return (w && w[0] == '1' && v) ? atoi(v) : 0;
+    }();
     if (pdl && pdl_enabled()) {  // may start on the SMs the previous kernel's CTAs leave (it waits for its results)
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
@@ -111,9 +118,9 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
         cfg.stream = st;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, kern, in, a_out, batch, (T)scale, a_tw, a_filt);
+        return cudaLaunchKernelEx(&cfg, kern, in, a_out, batch, (T)scale, a_tw, a_filt, xo);
     }
-    kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(in, a_out, batch, (T)scale, a_tw, a_filt);
+    kern<<<grid, W * (R / E), G::SMEM_BYTES, st>>>(in, a_out, batch, (T)scale, a_tw, a_filt, xo);
     return cudaGetLastError();
 }
 
