@@ -52,6 +52,34 @@ struct RowsTmaCfg {
     static constexpr uint32_t ROW_IN_BYTES = (uint32_t)(R * (REAL_IN ? sizeof(float) : sizeof(cpx<T>)));
 };
 
+// One pass of tiles: the stage ring (STAGES stages of W lines at smem_raw,
+// mbarriers at bar0) over tiles blockIdx.x, + gridDim.x, ...  The first
+// STAGES tiles are issued by rows_tma_issue_first (thread 0) beforehand.
+template <typename T, int R, int E, int W, bool REAL_IN, int STAGES>
+__device__ __forceinline__ void rows_tma_issue(const void* in_, int64_t batch, unsigned char* smem_raw, uint32_t bar0,
+                                               int64_t tile, int s) {
+    using C = cpx<T>;
+    using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
+    const char* in = reinterpret_cast<const char*>(in_);
+    const int64_t r0 = tile * W;
+    const int64_t nr = (batch - r0) < W ? (batch - r0) : W;
+    const uint32_t bar = bar0 + 8 * s;
+    mbar_expect_tx(bar, (uint32_t)(nr * G::ROW_IN_BYTES));
+    const uint32_t dst = smem_addr_u32(smem_raw + s * G::STAGE_BYTES);
+    for (int64_t i = 0; i < nr; ++i)
+        bulk_g2s(dst + (uint32_t)(i * G::LS * sizeof(C)), in + (r0 + i) * G::ROW_IN_BYTES, G::ROW_IN_BYTES, bar);
+}
+
+template <typename T, int R, int E, int W, bool REAL_IN, int STAGES>
+__device__ __forceinline__ void rows_tma_issue_first(const void* in_, int64_t batch, unsigned char* smem_raw,
+                                                     uint32_t bar0) {
+    const int64_t ntiles = (batch + W - 1) / W;
+    for (int s = 0; s < STAGES; ++s) {
+        const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+        if (tile < ntiles) rows_tma_issue<T, R, E, W, REAL_IN, STAGES>(in_, batch, smem_raw, bar0, tile, s);
+    }
+}
+
 // TRANS: store the tile transposed, out[v][row] (leading dimension = batch),
 // through the stage buffer so that the W rows of a tile form W-element runs
 // -- the separable pipeline's passes then always read contiguous rows.
@@ -65,11 +93,11 @@ struct RowsTmaCfg {
 // each real row to complex.  PAIR = 2: the same, stored as the transposed
 // COMPLEX grid (a', 0), (b', 0) -- the last pass of a real-input pipeline
 // with complex output, whose exact result is real.
-template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false, bool TRANS = false,
-          int PAIR = 0, int MINB = 1>
-__global__ void __launch_bounds__(W*(R / E), MINB)
-    k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
-               const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt, int xo = 0) {
+// xo: timing experiments only (wrong results): 1 = no FFT arithmetic, 2 = no stores.
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT, bool TRANS, int PAIR>
+__device__ __forceinline__ void rows_tma_loop(const void* in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
+                                              const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt, int xo,
+                                              unsigned char* smem_raw, uint32_t bar0) {
     using C = cpx<T>;
 #ifndef B200FFT_ROWS_TWREC
 #define B200FFT_ROWS_TWREC 1
@@ -79,38 +107,9 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
     constexpr bool TWR = B200FFT_ROWS_TWREC != 0;
     using F = LineFFT<T, R, E, INV, 0, !TWR, TWR>;
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
-    static_assert(R >= 256 && (R * sizeof(cpx<T>)) % 16 == 0, "bulk copies need >= 16 B rows");
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const uint32_t bar0 = smem_addr_u32(smem_raw + STAGES * G::STAGE_BYTES);
     const int tid = threadIdx.x;
     const int t = tid / F::TPL, lt = tid % F::TPL;
     const int64_t ntiles = (batch + W - 1) / W;
-    const char* in = reinterpret_cast<const char*>(in_);
-    // programmatic dependent launch: when this launch overlaps the tail of
-    // the previous kernel (the second pass of a pipeline), wait for that
-    // kernel's results before the first load; let the next one launch early
-    // (both no-ops for an ordinary launch)
-    B200FFT_PDL_PROLOGUE();
-
-    auto issue = [&](int64_t tile, int s) {
-        const int64_t r0 = tile * W;
-        const int64_t nr = (batch - r0) < W ? (batch - r0) : W;
-        const uint32_t bar = bar0 + 8 * s;
-        mbar_expect_tx(bar, (uint32_t)(nr * G::ROW_IN_BYTES));
-        const uint32_t dst = smem_addr_u32(smem_raw + s * G::STAGE_BYTES);
-        for (int64_t i = 0; i < nr; ++i)
-            bulk_g2s(dst + (uint32_t)(i * G::LS * sizeof(C)), in + (r0 + i) * G::ROW_IN_BYTES, G::ROW_IN_BYTES, bar);
-    };
-
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        for (int s = 0; s < STAGES; ++s) {
-            const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
-            if (tile < ntiles) issue(tile, s);
-        }
-    }
-    __syncthreads();
 
     for (int64_t k = 0;; ++k) {
         const int64_t tile = blockIdx.x + k * gridDim.x;
@@ -133,7 +132,7 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
         }
         const int bar = (F::TPL % 32 == 0 && W <= 15) ? 1 + t : 0;
         T sc = scale;
-        if (!(xo & 1)) {  // (xo: timing experiments only, wrong results)
+        if (!(xo & 1)) {
             F::run(v, line, lt, tw, bar);
             row_filter_pass<T, R, E, FILT, 0, !TWR, TWR>(v, line, lt, tw, rowfilt, sc, bar);
         }
@@ -171,9 +170,84 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             const int64_t nt = blockIdx.x + (k + STAGES) * gridDim.x;
-            if (nt < ntiles) issue(nt, s);
+            if (nt < ntiles) rows_tma_issue<T, R, E, W, REAL_IN, STAGES>(in_, batch, smem_raw, bar0, nt, s);
         }
     }
+}
+
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT = false, bool TRANS = false,
+          int PAIR = 0, int MINB = 1>
+__global__ void __launch_bounds__(W*(R / E), MINB)
+    k_rows_tma(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
+               const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt, int xo = 0) {
+    using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
+    static_assert(R >= 256 && (R * sizeof(cpx<T>)) % 16 == 0, "bulk copies need >= 16 B rows");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t bar0 = smem_addr_u32(smem_raw + STAGES * G::STAGE_BYTES);
+    // programmatic dependent launch: when this launch overlaps the tail of
+    // the previous kernel (the second pass of a pipeline), wait for that
+    // kernel's results before the first load; let the next one launch early
+    // (both no-ops for an ordinary launch)
+    B200FFT_PDL_PROLOGUE();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        rows_tma_issue_first<T, R, E, W, REAL_IN, STAGES>(in_, batch, smem_raw, bar0);
+    }
+    __syncthreads();
+    rows_tma_loop<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS, PAIR>(in_, out, batch, scale, tw, rowfilt, xo,
+                                                                         smem_raw, bar0);
+}
+
+// ---------------------------------------------------------------------------
+// k_rows_tma2: BOTH passes of the separable real-pair pipeline (C3's shape,
+// square R x R grids, R <= 2048) in ONE cooperative launch: pass 1 = the
+// row filter pass over the input's real-row pairs, stored transposed into
+// the intermediate `mid` (PAIR 1: float pairs); a grid-wide barrier; pass 2
+// = the row filter pass over the transposed grid's row pairs, stored
+// transposed into `out` (PAIR2 = 2: complex (a, 0), (b, 0); 1: real pairs).
+// One launch instead of two saves the second launch's ramp and tail (the
+// C3 breakdown: ~15 us of the 40 were launch + first-load latency).
+// Grid barrier: every CTA's pass-1 stores are released at gpu scope by
+// thread 0 (bar.sync + fence.acq_rel.gpu: cumulative) and counted in *gbar;
+// thread 0 of every CTA waits for the launch's target count (acquire), then
+// a proxy fence orders the generic-proxy stores before the TMA (async
+// proxy) reads of pass 2.  *gbar only grows: the host passes target =
+// (launch number) x gridDim.  All CTAs are co-resident (cooperative launch).
+// ---------------------------------------------------------------------------
+template <int R, int E, int W, int STAGES, int PAIR2>
+__global__ void __launch_bounds__(W*(R / E), 1)
+    k_rows_tma2(const void* __restrict__ in_, float2* __restrict__ mid, void* __restrict__ out_, int64_t lines,
+                const float2* __restrict__ tw, float scale1, const float* __restrict__ filt1, float scale2,
+                const float* __restrict__ filt2, unsigned long long* gbar, unsigned long long target, int xo) {
+    using G = RowsTmaCfg<float, R, W, false, STAGES>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t bar0 = smem_addr_u32(smem_raw + STAGES * G::STAGE_BYTES);
+    const uint32_t bar1 = bar0 + 8 * STAGES;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2 * STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        rows_tma_issue_first<float, R, E, W, false, STAGES>(in_, lines, smem_raw, bar0);
+    }
+    __syncthreads();
+    rows_tma_loop<float, R, E, W, false, false, STAGES, true, true, 1>(in_, mid, lines, scale1, tw, filt1, xo,
+                                                                      smem_raw, bar0);
+    // ---- grid barrier (the loop ended with a __syncthreads) ----
+    if (threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;\n" ::"l"(gbar) : "memory");
+        unsigned long long v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(gbar) : "memory");
+            if (v >= target) break;
+            __nanosleep(64);
+        }
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        rows_tma_issue_first<float, R, E, W, false, STAGES>(mid, lines, smem_raw, bar1);
+    }
+    __syncthreads();
+    rows_tma_loop<float, R, E, W, false, false, STAGES, true, true, PAIR2>(
+        mid, reinterpret_cast<float2*>(out_), lines, scale2, tw, filt2, xo, smem_raw, bar1);
 }
 
 }  // namespace b200fft

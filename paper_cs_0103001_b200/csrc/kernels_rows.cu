@@ -86,7 +86,7 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
                           : (int)((STAGE_KB * 1024) / (R * sizeof(cpx<T>)));
     // OCC CTAs per SM (registers capped): one stage each, or (OCC = 3, the
     // C2 lesson) two smaller stages each
-    constexpr int STAGES = OCC == 3 ? 2 : (OCC > 1 ? 1 : 3);
+    constexpr int STAGES = OCC == 3 ? 2 : (OCC > 1 && STAGE_KB >= 64 ? 1 : 3);
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
     auto kern = k_rows_tma<T, R, E, W, INV, REAL_IN, STAGES, FILT, TRANS, PAIR, OCC>;
     int grid_max = 0;
@@ -162,6 +162,75 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
     }
 }
 
+
+// both passes of the square real-pair pipeline in one cooperative launch
+// (fft_tma.cuh k_rows_tma2); 3 stages of ~64 KiB, 512 threads, one CTA per SM
+template <int R, int PAIR2>
+cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const void* filt1, double scale2,
+                    const void* filt2, const void* tw, unsigned long long* gbar, unsigned long long* gen,
+                    cudaStream_t st) {
+    constexpr int E = 16, STAGES = 3;
+    constexpr int W = (int)((64 * 1024) / (R * sizeof(float2)));
+    using G = RowsTmaCfg<float, R, W, false, STAGES>;
+    auto kern = k_rows_tma2<R, E, W, STAGES, PAIR2>;
+    const size_t smem = G::SMEM_BYTES + 8 * STAGES;  // a second set of stage barriers
+    int grid_max = 0;
+    cudaError_t e = kernel_setup((const void*)kern, W * (R / E), smem, &grid_max);
+    if (e != cudaSuccess) return e;
+    const int64_t lines = R / 2;  // row pairs per pass
+    const int64_t tiles = (lines + W - 1) / W;
+    const int grid = (int)(tiles < grid_max ? tiles : grid_max);
+    const unsigned long long target = (++*gen) * (unsigned long long)grid;
+    static const int xo = [] {
+        const char* w = getenv("B200FFT_ALLOW_WRONG");
+        const char* v = getenv("B200FFT_ROWS_XO");
+        return (w && w[0] == '1' && v) ? atoi(v) : 0;
+    }();
+    const void* a_in = in;
+    float2* a_mid = reinterpret_cast<float2*>(mid);
+    void* a_out = out;
+    int64_t a_lines = lines;
+    const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(R, ml_of(E));
+    float a_s1 = (float)scale1, a_s2 = (float)scale2;
+    const float* a_f1 = reinterpret_cast<const float*>(filt1);
+    const float* a_f2 = reinterpret_cast<const float*>(filt2);
+    unsigned long long a_target = target;
+    int a_xo = xo;
+    void* args[] = {&a_in, &a_mid, &a_out, &a_lines, &a_tw, &a_s1, &a_f1, &a_s2, &a_f2, &gbar, &a_target, &a_xo};
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(W * (R / E));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, (const void*)kern, args);
+}
+
+}  // namespace
+
+bool rows_filter2_supported(int prec, int64_t N, int64_t M) {
+    const char* e = getenv("B200FFT_PIPE_FUSED2");  // "0": the two-launch form (read per call: tests cover both)
+    return !(e && e[0] == '0') && N == M && rows_filter_transposed_supported(prec, N) && N >= 512;
+}
+
+cudaError_t launch_rows_filter2(int64_t R, const void* in, void* mid, void* out, double scale1, const void* filt1,
+                                double scale2, const void* filt2, const void* tw, int pair2, unsigned long long* gbar,
+                                unsigned long long* gen, cudaStream_t st) {
+    switch (R) {
+    if (pair2 != 2) return cudaErrorInvalidValue;  // complex output only (the C3 form)
+#define B200_R2_CASE(r) \
+    case r: return rows2_t<r, 2>(in, mid, out, scale1, filt1, scale2, filt2, tw, gbar, gen, st);
+        B200_R2_CASE(512) B200_R2_CASE(1024) B200_R2_CASE(2048)
+#undef B200_R2_CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+namespace {
 }  // namespace
 
 bool rows_filter_transposed_supported(int prec, int64_t R) {

@@ -80,6 +80,19 @@ cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* i
                                           double scale, const void* tw, const void* rowfilt, cudaStream_t st,
                                           int pair = 0, bool pdl = false);
 
+// Both passes of the real-pair pipeline of a square R x R grid (512 <= R
+// <= 2048, complex64) in one cooperative launch (k_rows_tma2): in (R real
+// rows) -> pass 1 (row pairs, fwd * filt1 * scale1 * inv) -> mid (the
+// transposed real grid, R x R floats) -> grid barrier -> pass 2 (filt2,
+// scale2) -> out (pair2 = 2: the complex grid, imaginary parts 0; the only
+// form built).
+// gbar: a device counter that only grows (zeroed once); *gen: the host's
+// launch count for it (incremented here).
+bool rows_filter2_supported(int prec, int64_t N, int64_t M);
+cudaError_t launch_rows_filter2(int64_t R, const void* in, void* mid, void* out, double scale1, const void* filt1,
+                                double scale2, const void* filt2, const void* tw, int pair2, unsigned long long* gbar,
+                                unsigned long long* gen, cudaStream_t st);
+
 // Kernel family B: column transforms of nimg grids [R][S]; mode 0 fwd, 1 inv,
 // 2 fwd -> filter*scale -> inv.
 cudaError_t launch_cols(int prec, int mode, int64_t R, const void* in, void* out, int64_t S,

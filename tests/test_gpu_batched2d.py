@@ -135,3 +135,32 @@ def test_real_to_real_other_filters_use_the_half_spectrum(b):
     ref, _ = oracle.filter_pipeline_real(img, oracle.ideal_filter(256, 256, 10.0, literal=False))
     assert oracle.rel_l2(o.cpu().numpy(), ref) <= 1e-5
     p.destroy()
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("real_out", [False, True])
+@pytest.mark.parametrize("N,batch", [(512, 2), (1024, 3), (2048, 2)])
+def test_fused_two_pass_pipeline(b, N, batch, real_out, fused, monkeypatch):
+    """The square real-pair pipeline with both passes in one cooperative
+    launch (k_rows_tma2, a grid barrier between the passes) against the
+    two-launch form and the oracle; the plan is called twice so the barrier
+    counter's later generations are exercised too."""
+    monkeypatch.setenv("B200FFT_PIPE_FUSED2", fused)
+    imgs = np.stack([fixtures.sky_image(N, N, seed=900 + i, nsrc=50) for i in range(batch)])
+    flags = b.IN_REAL_F32 | (b.OUT_REAL_F32 if real_out else 0)
+    p = b.Plan((N, N), batch=batch, flags=flags)
+    x = torch.from_numpy(imgs).cuda()
+    o = torch.empty((batch, N, N), dtype=torch.float32 if real_out else torch.complex64, device="cuda")
+    for _ in range(2):
+        o.zero_()
+        p.filter_pipeline(x, o, b.FILTER_GAUSS, 0.1)
+        torch.cuda.synchronize()
+        assert p.last_launch_count() == (batch if fused == "1" and not real_out else 2 * batch)
+        ref = np.stack([oracle.gauss_pipeline(imgs[i].astype(np.complex128), 0.1) for i in range(batch)])
+        out = o.cpu().numpy()
+        if real_out:
+            assert oracle.rel_l2(out, ref.real) <= 1e-5
+        else:
+            assert oracle.rel_l2(out, ref) <= 1e-5
+            assert np.all(out.imag == 0)
+    p.destroy()

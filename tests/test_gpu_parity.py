@@ -348,7 +348,8 @@ def test_real_input_complex_output_gauss(fft, N, M, batch, realpair, monkeypatch
     o = torch.empty((batch, N, M), dtype=torch.complex64, device="cuda")
     p.filter_pipeline(x, o, b.FILTER_GAUSS, 0.1)
     torch.cuda.synchronize()
-    assert p.last_launch_count() == 2 * batch
+    fused = realpair == "1" and N == M and N >= 512  # both passes in one launch (k_rows_tma2)
+    assert p.last_launch_count() == (batch if fused else 2 * batch)
     p.destroy()
     out = o.cpu().numpy()
     ref = np.stack([oracle.gauss_pipeline(imgs[i].astype(np.complex128), 0.1) for i in range(batch)])
