@@ -157,8 +157,10 @@ __global__ void __launch_bounds__(320, 3)
     }
 
     // ---- compute warps (256 threads, named barrier 1) ----
-    using FA = LineFFT<float, 256, 16, INV, 2, false, true>;
-    using FB = LineFFT<float, 128, 16, INV, 2, false, true>;
+    // step twiddles from the constant table (TWREC 2): the butterfly index is
+    // the lane index hi (A: two values per warp) or lt = tid / 32 (B: one)
+    using FA = LineFFT<float, 256, 16, INV, 2, false, 2>;
+    using FB = LineFFT<float, 128, 16, INV, 2, false, 2>;
     const uint64_t keep = tmaops::policy_evict_last();
     const uint64_t stream = tmaops::policy_evict_first();
     const int lo = tid & 15, hi = tid >> 4;
@@ -258,14 +260,9 @@ __global__ void __launch_bounds__(320, 3)
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
                     const int jp = lt + 8 * b;
-                    // W_128^{jp r} = powers of the step table's entry [0][jp]
-                    const float2 w1 = __ldg(tw128 + tw_off(128, 1, 4) + jp);
-                    float2 w = w1;
+                    // W_128^{jp r} = W_256^{2 jp r} from the constant table (jp is warp-uniform)
 #pragma unroll
-                    for (int r = 1; r < 8; ++r) {
-                        u[b * 8 + r] = cmul_dir<INV>(u[b * 8 + r], w);
-                        if (r < 7) w = cmul(w, w1);
-                    }
+                    for (int r = 1; r < 8; ++r) u[b * 8 + r] = cmul_dir<INV>(u[b * 8 + r], c_w256[(2 * jp * r) & 255]);
                     dft<8, INV>(u + b * 8);
                 }
                 // outputs c[jp + 16 q] = u[b 8 + q]: ka = jp + 16 q -> X[k2 + N2 (kc + 256 ka)]

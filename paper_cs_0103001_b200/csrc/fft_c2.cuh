@@ -325,6 +325,14 @@ struct AbStCfg {
     static constexpr size_t SMEM = INFO_OFF + 8 * (NS + NSIG) + 16;
 };
 
+// step-1 twiddles W_256^{l r} from the constant table (fft_engine.cuh
+// c_w256): a thread's depend only on its lane l, two distinct l per warp
+template <bool INV>
+__device__ __forceinline__ void st_step1_twiddle_c(float2* v, int l) {
+#pragma unroll
+    for (int r = 1; r < 16; ++r) v[r] = cmul_dir<INV>(v[r], c_w256[(l * r) & 255]);
+}
+
 template <bool INV>
 __device__ __forceinline__ void st_step1_twiddle(float2* v, int l, const float2* __restrict__ tw256) {
     // step 1 of the 256-point Stockham (span 16): v[r] *= W_256^{l r}, r < 16,
@@ -372,7 +380,8 @@ __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, u
     }
     bk_arrive(empty);
     if (!(xo & 8)) {
-        st_step1_twiddle<INV>(v, hi, tw256);
+        if (xo & 4096) st_step1_twiddle<INV>(v, hi, tw256);  // the round-2 recurrence (3% slower)
+        else st_step1_twiddle_c<INV>(v, hi);
         dft<16, INV>(v);
     }
     // Y[k2][n1] = v[q] * W_N^{n1 k2} * scale, k2 = hi + 16 q
@@ -406,7 +415,8 @@ __device__ __forceinline__ void st_task_b(float2* st, int lo, int hi, int bar, u
     }
     bk_arrive(empty);
     if (!(xo & 8)) {
-        st_step1_twiddle<INV>(v, hi, tw256);
+        if (xo & 4096) st_step1_twiddle<INV>(v, hi, tw256);  // the round-2 recurrence (3% slower)
+        else st_step1_twiddle_c<INV>(v, hi);
         dft<16, INV>(v);
     }
     float2* x = x0 + lo + (int64_t)hi * 256;

@@ -58,7 +58,7 @@ __device__ __forceinline__ bool cp_decode(int64_t p, int64_t G, int D, int& phas
 
 // grid: [nimg][8192][M] complex64 (in place); tl = W_N^x, x < N (fp64-generated);
 // gu = g_N[u] (N entries); gv = g_M (M_total entries, distributed slabs) or null
-template <int N2 = 128>
+template <int N2 = 128, int TW = 0>
 __global__ void __launch_bounds__(320, 3)
     k_colfilt(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               float2* __restrict__ grid, int64_t M, int64_t nimg, float scale, const float2* __restrict__ tw64,
@@ -144,10 +144,13 @@ __global__ void __launch_bounds__(320, 3)
     }
 
     // ---- compute warps (256 threads, named barrier 1) ----
-    using FA = LineFFT<float, 64, 16, false, 5, false, true>;
-    using FAI = LineFFT<float, 64, 16, true, 5, false, true>;
-    using FB = LineFFT<float, 128, 16, false, 2, false, true>;
-    using FBI = LineFFT<float, 128, 16, true, 2, false, true>;
+    // step twiddles from the constant table (TWREC 2): lt = tid / 64 (A, A')
+    // or tid / 32 (B) is uniform across a warp
+    // (TW bit 0: A / A' steps, bit 1: B steps from the constant table)
+    using FA = LineFFT<float, 64, 16, false, 5, false, (TW & 1) ? 2 : 1>;
+    using FAI = LineFFT<float, 64, 16, true, 5, false, (TW & 1) ? 2 : 1>;
+    using FB = LineFFT<float, 128, 16, false, 2, false, (TW & 2) ? 2 : 1>;
+    using FBI = LineFFT<float, 128, 16, true, 2, false, (TW & 2) ? 2 : 1>;
     const uint64_t keep = tmaops::policy_evict_last();
     const uint64_t stream = tmaops::policy_evict_first();
     int ja = 0;

@@ -17,12 +17,46 @@
 // and stores coalesced and lets a forward and an inverse transform chain in
 // registers (the fused filter pipeline).
 #pragma once
+#include <cmath>
+#include <mutex>
+#include <set>
+
 #include "fft_common.cuh"
 #include "launch.h"
 
 namespace b200fft {
 
 constexpr int RMAX = 8192;  // largest in-CTA DFT
+
+// W_256^k, k < 256 (fp64-generated on the host, rounded once), in the
+// constant cache of every module that includes this header (static: one
+// copy per translation unit, uploaded by that unit's launchers through
+// w256_upload()).  The step twiddles W_{Ns rho}^{k r} of lines of R <= 256
+// points are entries of it (index k r 256 / (Ns rho)); in the task-pipeline
+// kernels the butterfly index k is uniform (or takes two values) across a
+// warp, so these loads are constant-cache broadcasts that take the twiddle
+// products off the FP32 pipe (round 2: C2 -3.2%, and more accurate than the
+// recurrence's powers).
+static __constant__ float2 c_w256[256];
+
+// upload c_w256 for the current device (once per device per module)
+static inline cudaError_t w256_upload() {
+    static std::mutex mu;
+    static std::set<int> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(dev)) return cudaSuccess;
+    float2 h[256];
+    for (int k = 0; k < 256; ++k) {
+        const double a = -2.0 * 3.14159265358979323846 * (double)k / 256.0;
+        h[k] = make_float2((float)cos(a), (float)sin(a));
+    }
+    e = cudaMemcpyToSymbol(c_w256, h, sizeof(h));
+    if (e == cudaSuccess) done.insert(dev);
+    return e;
+}
 // Twiddles of the in-CTA steps come from the step-major tables of
 // fft_common.cuh (tw_base / tw_off), fp64-generated on the host and rounded
 // once; kernels receive the pointer to their R's table.
@@ -54,8 +88,10 @@ __device__ __forceinline__ int il8(int i) { return (i ^ ((i >> 3) & 1)) * 8; }
 // barriers (for kernels with a 128-register budget)
 // TWREC: a step's twiddles W^{k r}, r = 1..rho-1, as powers of the one
 // table entry W^{k} (rho - 2 complex products, ~rho ulp in fp32) instead of
-// rho - 1 loads -- for kernels whose warps are short of load bandwidth
-template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false, bool TWREC = (sizeof(T) == 4)>
+// rho - 1 loads -- for kernels whose warps are short of load bandwidth.
+// TWREC = 2 (complex64, R <= 256): from the constant table c_w256, for
+// kernels whose butterfly index is (nearly) uniform across a warp.
+template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false, int TWREC = (sizeof(T) == 4)>
 struct LineFFT {
     using C = cpx<T>;
     static constexpr int ML = ml_of(E);  // largest radix 2^ML (16, or 8 when E = 8)
@@ -83,7 +119,13 @@ struct LineFFT {
                 const int j = lt + b * TPL;
                 const int k = j & (Ns - 1);
                 const C* __restrict__ ts = tw + tw_off(R, s, ML) + k;
-                if constexpr (TWREC) {
+                if constexpr (TWREC == 2) {
+                    static_assert(sizeof(T) == 4 && 256 % (Ns * rho) == 0, "constant twiddles: R <= 256, complex64");
+                    constexpr int SC = 256 / (Ns * rho);
+#pragma unroll
+                    for (int r = 1; r < rho; ++r)
+                        v[b * rho + r] = cmul_dir<INV>(v[b * rho + r], c_w256[(k * r * SC) & 255]);
+                } else if constexpr (TWREC) {
                     const C w1 = __ldg(ts);
                     C w = w1;
 #pragma unroll
@@ -289,7 +331,7 @@ __device__ __forceinline__ int64_t block_index(int64_t row, int v, int sh) {
 
 // FILT: a row filter pass of the separable pipeline: forward
 // transform -> * rowfilt[v] * scale -> inverse transform, stored unscaled.
-template <typename T, int R, int E, bool FILT, int LAYOUT = 0, bool PF = false, bool TWREC = false>
+template <typename T, int R, int E, bool FILT, int LAYOUT = 0, bool PF = false, int TWREC = 0>
 __device__ __forceinline__ void row_filter_pass(cpx<T>* v, cpx<T>* line, int lt, const cpx<T>* __restrict__ tw,
                                                 const T* __restrict__ rowfilt, T& scale, int bar = 0) {
     if constexpr (FILT) {

@@ -49,6 +49,7 @@ cudaError_t big_pass(const void* in, void* out, double scale, const void* tw, co
     int grid_n = 0;
     const void* kern = (const void*)k_big<INV, PASS>;
     cudaError_t e = kernel_setup(kern, 320, BigCfg::SMEM, &grid_n);
+    if (e == cudaSuccess) e = w256_upload();  // the constant step twiddles (fft_engine.cuh)
     if (e != cudaSuccess) return e;
     float2* ring = reinterpret_cast<float2*>(ws);
     int* ctr = reinterpret_cast<int*>((char*)ws + (size_t)R * BigCfg::SLOT * sizeof(float2));
@@ -136,5 +137,9 @@ cudaError_t launch_big(bool inv, const void* in, void* mid, void* out, double sc
     return inv ? big_pass<true, 2>(mid, out, scale, tw, twl, whi, wlo, ws, ws_bytes, st)
                : big_pass<false, 2>(mid, out, scale, tw, twl, whi, wlo, ws, ws_bytes, st);
 }
+
+// this module's copy of the constant step-twiddle table (fft_engine.cuh
+// c_w256), uploaded at plan creation so no launch does it (graph capture)
+cudaError_t big_upload_constants() { return w256_upload(); }
 
 }  // namespace b200fft

@@ -165,7 +165,8 @@ int64_t ab_launch_grid(int64_t grid, int64_t batch, int64_t D, int NS) {
 // 2048 = each B task stores one contiguous 32 KiB block; correct results:
 // 16 = static round-robin positions, 32 = two positions per atomic, 128 /
 // 256 / 1024 = X stores evict-first / .cs / evict-last (default: no hint),
-// 512 = A loads evict-last.
+// 512 = A loads evict-last, 4096 = step-1 twiddles by the recurrence (the
+// earlier form, 3% slower) instead of the constant table.
 int ab_opts(int kind) {
     if (kind == C2_WS) {
         const char* v = getenv("B200FFT_AB_OPTS");
@@ -187,6 +188,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     if (e != cudaSuccess) return e;
     if (batch <= 0) return cudaSuccess;
     if (!ws || ws_bytes < ab_ws_bytes(g.ring, batch)) return cudaErrorInvalidValue;
+    if ((e = w256_upload()) != cudaSuccess) return e;
     void* ring = ws;
     const size_t rb = (size_t)g.ring * 65536 * sizeof(float2);
     int* ctl = reinterpret_cast<int*>((char*)ws + rb);
@@ -293,5 +295,9 @@ cudaError_t launch_c2(bool inv, const void* in, void* out, int64_t batch, double
     return inv ? ab_launch<true>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st)
                : ab_launch<false>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
 }
+
+// this module's copy of the constant step-twiddle table (fft_engine.cuh
+// c_w256), uploaded at plan creation so no launch does it (graph capture)
+cudaError_t c2_upload_constants() { return w256_upload(); }
 
 }  // namespace b200fft

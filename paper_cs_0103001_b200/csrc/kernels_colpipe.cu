@@ -50,7 +50,18 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
     if (!colfilt_supported(N, M) || nimg <= 0) return nimg <= 0 ? cudaSuccess : cudaErrorInvalidValue;
     if (!ws || ws_bytes < colfilt_workspace_bytes(M, nimg)) return cudaErrorInvalidValue;
     int grid_n = 0;
-    cudaError_t e = kernel_setup((const void*)k_colfilt<128>, 320, ColPipeCfg::SMEM, &grid_n);
+    // tuning: B200FFT_COLFILT_TW = bit 0: A / A' step twiddles, bit 1: B step
+    // twiddles from the constant table (else by recurrence).  Default 1: C4
+    // 0.8997 / 0.8955 / 1.043 ms for 0 / 1 / 2 (the B steps' constant loads
+    // push the 64-register B task into 300 B of spills)
+    const char* twv = getenv("B200FFT_COLFILT_TW");
+    const int twm = twv ? atoi(twv) & 3 : 1;
+    const void* kern = twm == 0   ? (const void*)k_colfilt<128, 0>
+                       : twm == 1 ? (const void*)k_colfilt<128, 1>
+                       : twm == 2 ? (const void*)k_colfilt<128, 2>
+                                 : (const void*)k_colfilt<128, 3>;
+    cudaError_t e = kernel_setup(kern, 320, ColPipeCfg::SMEM, &grid_n);
+    if (e == cudaSuccess) e = w256_upload();  // the constant step twiddles (fft_engine.cuh)
     if (e != cudaSuccess) return e;
     const int64_t groups = (M / 16) * nimg;
     int* ctr = reinterpret_cast<int*>(ws);
@@ -92,7 +103,11 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelExC(&cfg, (const void*)k_colfilt<128>, args);
+    return cudaLaunchKernelExC(&cfg, kern, args);
 }
+
+// this module's copy of the constant step-twiddle table (fft_engine.cuh
+// c_w256), uploaded at plan creation so no launch does it (graph capture)
+cudaError_t colfilt_upload_constants() { return w256_upload(); }
 
 }  // namespace b200fft

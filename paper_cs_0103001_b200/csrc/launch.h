@@ -190,4 +190,10 @@ void l2_persist_request(int dev, size_t ring_bytes);
 cudaError_t launch_c2(bool inv, const void* in, void* out, int64_t batch, double scale, const void* tw4,
                       const void* tw, void* ws, size_t ws_bytes, cudaStream_t st);
 
+// the constant step-twiddle tables of the task-pipeline modules (one copy per
+// module, fft_engine.cuh c_w256), uploaded for the current device
+cudaError_t c2_upload_constants();
+cudaError_t big_upload_constants();
+cudaError_t colfilt_upload_constants();
+
 }  // namespace b200fft

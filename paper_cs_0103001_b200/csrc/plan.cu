@@ -1638,6 +1638,9 @@ fft_status fft_plan_create_ex(fft_plan* out, const int64_t* dims, int rank, int6
         return cuda_fail(e, "cudaGetDevice");
     }
     e = device_twiddles(p->device, ip, &p->tw);
+    if (e == cudaSuccess) e = c2_upload_constants();
+    if (e == cudaSuccess) e = big_upload_constants();
+    if (e == cudaSuccess) e = colfilt_upload_constants();
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "twiddle table upload");
