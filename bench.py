@@ -100,10 +100,18 @@ class ClockSampler:
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
+    # NVML reports a clock change ~100 ms after it happens (measured: C2's
+    # kernels slow down under sw_power_cap ~40 ms into a back-to-back run,
+    # NVML shows it ~100 ms later), so sampling continues for TAIL seconds
+    # after the region: the reasons are those seen in the region and the tail;
+    # the median clock is over the region's samples only.
+    TAIL = 0.15
+
     def __init__(self, index: int, period: float = 0.002):
         self.index = index
         self.period = period
         self.samples = []
+        self.tail = []
         self.stop = threading.Event()
         self.mx = None
         self.ok = False
@@ -123,34 +131,41 @@ class ClockSampler:
 
     def _poll(self):
         nv = self.nv
+        t_stop = None
         while True:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((sm, rs))
+                (self.tail if t_stop is not None else self.samples).append((sm, rs))
             except Exception:
                 pass
             self.started.set()
-            if self.stop.is_set() and len(self.samples) >= 5:
+            if self.stop.is_set() and t_stop is None and len(self.samples) >= 5:
+                t_stop = time.perf_counter()
+            if t_stop is not None and time.perf_counter() - t_stop >= self.TAIL:
                 break
             time.sleep(self.period)
 
     def __exit__(self, *a):
         self.stop.set()
         if self.ok:
-            self.t.join(timeout=2)
+            self.t.join(timeout=2 + self.TAIL)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": ["unavailable"], "samples": 0}
         reasons = set()
-        for _, rs in self.samples:
+        for _, rs in self.samples + self.tail:
             for nm, bit in self.REASONS.items():
                 if rs & bit:
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.mx,
-                "reasons": sorted(reasons), "samples": len(self.samples),
-                "source": f"NVML, {self.period * 1e3:.0f} ms poll"}
+        out = {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.mx,
+               "reasons": sorted(reasons), "samples": len(self.samples),
+               "source": f"NVML, {self.period * 1e3:.0f} ms poll, reasons include a "
+                         f"{self.TAIL * 1e3:.0f} ms tail (NVML lags ~100 ms)"}
+        if self.tail:
+            out["sm_mhz_tail_min"] = min(s for s, _ in self.tail)
+        return out
 
 
 # ------------------------------------------------------------- distributed

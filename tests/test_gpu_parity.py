@@ -467,3 +467,41 @@ def test_c2_two_plans_two_streams(fft):
     assert oracle.rel_l2(y2.cpu().numpy(), oracle.fft_batch(x, inverse=True)) <= 1e-5
     p1.destroy()
     p2.destroy()
+
+
+@pytest.mark.parametrize("bits", [16, 32, 128, 256, 512, 1024, 4096])
+def test_c2_tuning_variants(fft, bits, monkeypatch):
+    """k_ab_st's tuning bits that keep the results (kernels_c2.cu ab_opts:
+    static / paired task positions, X store and A load cache policies, the
+    recurrence instead of the constant-table step twiddles) against the
+    oracle, so every selectable variant of the product kernel is covered."""
+    import paper_cs_0103001_b200 as b
+
+    monkeypatch.setenv("B200FFT_ALLOW_WRONG", "1")
+    monkeypatch.setenv("B200FFT_AB_XOPTS", str(bits))
+    n, batch = 65536, 40
+    x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=960 + bits % 97).reshape(batch, n)
+    p = b.Plan((n,), batch=batch)
+    xd = torch.from_numpy(x).cuda()
+    yd, zd = torch.empty_like(xd), torch.empty_like(xd)
+    p.forward(xd, yd)
+    p.inverse(yd, zd)
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy()
+    assert oracle.rel_l2(y, oracle.fft_batch(x)) <= 1e-5
+    assert oracle.rel_l2(zd.cpu().numpy(), oracle.fft_batch(y, inverse=True)) <= 1e-5
+    p.destroy()
+
+
+@pytest.mark.parametrize("tw", ["0", "1", "2", "3"])
+def test_colfilt_twiddle_variants(fft, tw, monkeypatch):
+    """k_colfilt with each step-twiddle source (B200FFT_COLFILT_TW: A / A'
+    and B steps from the constant table or by recurrence) on an 8192 x 256
+    Gaussian pipeline against the oracle."""
+    import paper_cs_0103001_b200 as b
+
+    monkeypatch.setenv("B200FFT_COLFILT_TW", tw)
+    N, M = 8192, 256
+    f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=970 + int(tw)).reshape(N, M)
+    out = run_pipeline(b, f, b.FILTER_GAUSS, 0.1)
+    assert oracle.rel_l2(out, oracle.gauss_pipeline(f, 0.1)) <= 1e-5
