@@ -56,6 +56,18 @@ __device__ __forceinline__ bool cp_decode(int64_t p, int64_t G, int D, int& phas
     return g >= 0 && g < G;
 }
 
+// group g -> (image, first column): shift / mask for a power-of-two number
+// of column groups per image, else (cg_sh < 0) a 32-bit division
+__device__ __forceinline__ void cp_group(int64_t g, int64_t CG, int cg_sh, int& img, int& c0) {
+    if (cg_sh >= 0) {
+        img = (int)(g >> cg_sh);
+        c0 = (int)(g & (CG - 1)) * 16;
+    } else {
+        img = (int)((uint32_t)g / (uint32_t)CG);
+        c0 = (int)((uint32_t)g - (uint32_t)img * (uint32_t)CG) * 16;
+    }
+}
+
 // grid: [nimg][8192][M] complex64 (in place); tl = W_N^x, x < N (fp64-generated);
 // gu = g_N[u] (N entries); gv = g_M (M_total entries, distributed slabs) or null
 template <int N2 = 128, int TW = 0>
@@ -75,7 +87,7 @@ __global__ void __launch_bounds__(320, 3)
     volatile int64_t* sigb = task + NS;
     volatile int* sigdone = reinterpret_cast<volatile int*>(sigb + NSIG);
     const int tid = threadIdx.x;
-    const int64_t CG = M / 16;  // column groups per image (a power of two, 2^cg_sh)
+    const int64_t CG = M / 16;  // column groups per image (2^cg_sh, or cg_sh = -1)
     const int64_t groups = CG * nimg;
     const int64_t npos = (groups + 2 * (int64_t)ctl.D) * 96;
 
@@ -111,8 +123,8 @@ __global__ void __launch_bounds__(320, 3)
                     break;
                 }
                 task[s] = i;
-                const int img = (int)(g >> cg_sh);
-                const int c0 = (int)(g & (CG - 1)) * 16;
+                int img, c0;
+                cp_group(g, CG, cg_sh, img, c0);
                 if (phase != 2) {
                     while (*sigdone < na - NSIG + 1) __nanosleep(20);
                     ++na;
@@ -163,8 +175,9 @@ __global__ void __launch_bounds__(320, 3)
         int phase, part;
         int64_t g;
         cp_decode(i, groups, ctl.D, phase, g, part);
-        const int64_t img = g >> cg_sh;
-        const int64_t c0 = (g & (CG - 1)) * 16;
+        int img_i, c0_i;
+        cp_group(g, CG, cg_sh, img_i, c0_i);
+        const int64_t img = img_i, c0 = c0_i;
         float2 v[16];
         if (phase != 1) {
             // line (n2l, col) = tid % 64, 4 lanes of 16 elements (n1 or k1)

@@ -17,11 +17,11 @@
 
 namespace b200fft {
 
-// out[row][k] = scale * X[k], k = 0 .. R (row stride R + 1), in: rows of 2R reals
+// out[row][k] = scale * X[k], k = 0 .. R (row stride ld >= R + 1), in: rows of 2R reals
 template <typename T, int R, int E, int W>
 __global__ void __launch_bounds__(W*(R / E)) k_rows_r2c(const T* __restrict__ in, cpx<T>* __restrict__ out,
                                                         int64_t batch, T scale, const cpx<T>* __restrict__ tw,
-                                                        const cpx<T>* __restrict__ rtw) {
+                                                        const cpx<T>* __restrict__ rtw, int64_t ld) {
     using C = cpx<T>;
     using F = LineFFT<T, R, E, false>;
     B200FFT_PDL_PROLOGUE();
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows_r2c(const T* __restrict__ in
     for (int m = 0; m < E; ++m) line[F::bpos(lt, m)] = v[F::pos_out(m)];
     __syncthreads();
     if (!valid) return;
-    C* o = out + row * (R + 1);
+    C* o = out + row * ld;
     const T h = (T)0.5;
 #pragma unroll
     for (int m = 0; m < E; ++m) {
@@ -58,11 +58,11 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows_r2c(const T* __restrict__ in
     }
 }
 
-// out[row][j] = scale * f[j], j < 2R (real), in: rows of R + 1 bins X[0 .. R]
+// out[row][j] = scale * f[j], j < 2R (real), in: rows of R + 1 bins X[0 .. R] (row stride ld)
 template <typename T, int R, int E, int W>
 __global__ void __launch_bounds__(W*(R / E)) k_rows_c2r(const cpx<T>* __restrict__ in, T* __restrict__ out,
                                                         int64_t batch, T scale, const cpx<T>* __restrict__ tw,
-                                                        const cpx<T>* __restrict__ rtw) {
+                                                        const cpx<T>* __restrict__ rtw, int64_t ld) {
     using C = cpx<T>;
     using FI = LineFFT<T, R, E, true>;
     B200FFT_PDL_PROLOGUE();
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(W*(R / E)) k_rows_c2r(const cpx<T>* __restrict
     const int64_t row = (int64_t)blockIdx.x * W + t;
     const bool valid = row < batch;
     C* line = reinterpret_cast<C*>(smem_raw) + t * FI::LS;
-    const C* x = in + (valid ? row : 0) * (R + 1);
+    const C* x = in + (valid ? row : 0) * ld;
     // the row X[0 .. R] into the line buffer (X[R] in the spare last slot)
 #pragma unroll
     for (int m = 0; m < E; ++m) line[FI::bpos(lt, m)] = valid ? x[lt + FI::TPL * m] : mk((T)0, (T)0);

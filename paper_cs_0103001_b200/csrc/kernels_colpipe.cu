@@ -47,7 +47,8 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
                            const void* gu, const void* gv, int64_t col_off, void* ws, size_t ws_bytes,
                            cudaStream_t st) {
     constexpr int64_t N = 8192;
-    if (!colfilt_supported(N, M) || nimg <= 0) return nimg <= 0 ? cudaSuccess : cudaErrorInvalidValue;
+    if (nimg <= 0) return cudaSuccess;
+    if (M < 16 || M % 16 || (M / 16) * nimg >= ((int64_t)1 << 30)) return cudaErrorInvalidValue;
     if (!ws || ws_bytes < colfilt_workspace_bytes(M, nimg)) return cudaErrorInvalidValue;
     int grid_n = 0;
     // tuning: B200FFT_COLFILT_TW = bit 0: A / A' step twiddles, bit 1: B step
@@ -88,8 +89,11 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
     const float* a_gu = reinterpret_cast<const float*>(gu);
     const float* a_gv = reinterpret_cast<const float*>(gv);
     int64_t a_off = col_off;
+    // column groups per image: a power of two (mask / shift indexing) or, for
+    // other widths, cg_sh = -1 (32-bit division)
     int cg_sh = 0;
     while (((int64_t)1 << cg_sh) < M / 16) ++cg_sh;
+    if (((int64_t)1 << cg_sh) != M / 16) cg_sh = -1;
     void* args[] = {&ma, &mb, &a_grid, &a_M, &a_nimg, &a_scale, &a_tw64, &a_tw128, &a_tl, &a_gu, &a_gv, &a_off,
                     &cg_sh, &c};
     cudaLaunchConfig_t cfg = {};

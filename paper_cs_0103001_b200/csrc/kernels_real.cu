@@ -10,7 +10,8 @@ namespace {
 // R = M / 2 complex points per row; E values per thread, W rows per CTA
 template <typename T, int R, bool C2R>
 cudaError_t real_rows_t(const void* in, void* out, int64_t batch, double scale, const void* tw, const void* rtw,
-                        cudaStream_t st) {
+                        cudaStream_t st, int64_t ld) {
+    if (ld <= 0) ld = R + 1;
     constexpr int E = R < 16 ? R : 16;
     constexpr int TPL = R / E;
     constexpr int W = TPL >= 256 ? 1 : 256 / TPL;
@@ -26,18 +27,18 @@ cudaError_t real_rows_t(const void* in, void* out, int64_t batch, double scale, 
     if constexpr (C2R)
         return launch_pdl(k_rows_c2r<T, R, E, W>, grid, dim3(W * TPL), smem, st,
                           reinterpret_cast<const cpx<T>*>(in), reinterpret_cast<T*>(out), batch, (T)scale, a_tw,
-                          a_rtw);
+                          a_rtw, ld);
     else
         return launch_pdl(k_rows_r2c<T, R, E, W>, grid, dim3(W * TPL), smem, st, reinterpret_cast<const T*>(in),
-                          reinterpret_cast<cpx<T>*>(out), batch, (T)scale, a_tw, a_rtw);
+                          reinterpret_cast<cpx<T>*>(out), batch, (T)scale, a_tw, a_rtw, ld);
 }
 
 template <typename T, bool C2R>
 cudaError_t real_rows_r(int64_t M, const void* in, void* out, int64_t batch, double scale, const void* tw,
-                        const void* rtw, cudaStream_t st) {
+                        const void* rtw, cudaStream_t st, int64_t ld) {
     switch (M / 2) {
 #define B200_REAL_CASE(r) \
-    case r: return real_rows_t<T, r, C2R>(in, out, batch, scale, tw, rtw, st);
+    case r: return real_rows_t<T, r, C2R>(in, out, batch, scale, tw, rtw, st, ld);
         B200_REAL_CASE(1) B200_REAL_CASE(2) B200_REAL_CASE(4) B200_REAL_CASE(8) B200_REAL_CASE(16)
         B200_REAL_CASE(32) B200_REAL_CASE(64) B200_REAL_CASE(128) B200_REAL_CASE(256) B200_REAL_CASE(512)
         B200_REAL_CASE(1024) B200_REAL_CASE(2048) B200_REAL_CASE(4096)
@@ -49,15 +50,15 @@ cudaError_t real_rows_r(int64_t M, const void* in, void* out, int64_t batch, dou
 }  // namespace
 
 cudaError_t launch_rows_r2c(int prec, int64_t M, const void* in, void* out, int64_t batch, double scale,
-                            const void* tw, const void* rtw, cudaStream_t st) {
-    return prec == 0 ? real_rows_r<float, false>(M, in, out, batch, scale, tw, rtw, st)
-                     : real_rows_r<double, false>(M, in, out, batch, scale, tw, rtw, st);
+                            const void* tw, const void* rtw, cudaStream_t st, int64_t ld) {
+    return prec == 0 ? real_rows_r<float, false>(M, in, out, batch, scale, tw, rtw, st, ld)
+                     : real_rows_r<double, false>(M, in, out, batch, scale, tw, rtw, st, ld);
 }
 
 cudaError_t launch_rows_c2r(int prec, int64_t M, const void* in, void* out, int64_t batch, double scale,
-                            const void* tw, const void* rtw, cudaStream_t st) {
-    return prec == 0 ? real_rows_r<float, true>(M, in, out, batch, scale, tw, rtw, st)
-                     : real_rows_r<double, true>(M, in, out, batch, scale, tw, rtw, st);
+                            const void* tw, const void* rtw, cudaStream_t st, int64_t ld) {
+    return prec == 0 ? real_rows_r<float, true>(M, in, out, batch, scale, tw, rtw, st, ld)
+                     : real_rows_r<double, true>(M, in, out, batch, scale, tw, rtw, st, ld);
 }
 
 }  // namespace b200fft

@@ -144,15 +144,19 @@ cudaError_t launch_tree_combine(int prec, const void* e, const void* o, void* y,
 // batch rows of M reals (float for prec 0, double for 1) <-> rows of M/2 + 1
 // complex bins (Hermitian half spectrum), out = scale * (forward sum e^-,
 // or for C2R the unscaled inverse sum e^+).  rtw: W_M^k, k < M/2.  2 <= M <= 8192.
+// ld: row stride of the half spectrum in bins (<= 0: M/2 + 1, the API layout;
+// the internal pipeline pads it to a multiple of 16 for k_colfilt).
 cudaError_t launch_rows_r2c(int prec, int64_t M, const void* in, void* out, int64_t batch, double scale,
-                            const void* tw, const void* rtw, cudaStream_t st);
+                            const void* tw, const void* rtw, cudaStream_t st, int64_t ld = -1);
 cudaError_t launch_rows_c2r(int prec, int64_t M, const void* in, void* out, int64_t batch, double scale,
-                            const void* tw, const void* rtw, cudaStream_t st);
+                            const void* tw, const void* rtw, cudaStream_t st, int64_t ld = -1);
 
 // One-pass column filter of the 8192-row Gaussian pipeline (kernels_colpipe.cu,
 // fft_colpipe.cuh): in place on [nimg][8192][M] complex64 (M % 16 == 0),
 // column operator IDFT_N(g_N(u) * scale * [g_M(v + col_off)] * DFT_N); tl =
 // W_N^x (x < N), gu = g_N (N floats), gv = g_M or null; ws: counters.
+// colfilt_supported: the pipelines' power-of-two widths; any M % 16 == 0
+// (e.g. a padded half spectrum) is accepted by launch_colfilt.
 bool colfilt_supported(int64_t N, int64_t M);
 size_t colfilt_workspace_bytes(int64_t M, int64_t nimg);
 cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, const void* tw, const void* tl,

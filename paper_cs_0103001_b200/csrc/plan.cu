@@ -559,6 +559,9 @@ fft_status run_c2r(fft_plan_s* p, const void* in, void* out, cudaStream_t st) {
 // is real with H(u, v) = H(-u, -v) (the Gaussian and both readings of Eq.
 // filtro): R2C rows -> columns fwd (1/N) x H x inv -> C2R rows (1/M); half
 // the bytes and flops of the complex pipeline.
+cudaError_t colfilt(fft_plan_s* p, void* grid, int64_t SM, int64_t nimg, double scale, const void* gv,
+                    int64_t col_off, cudaStream_t st);
+
 fft_status run_pipeline_half(fft_plan_s* p, const void* in, void* out, const FilterArgs& f, cudaStream_t st) {
     const int64_t N = p->n0, M = p->n1;
     cudaError_t e = ensure_rtw(p, M);
@@ -566,6 +569,23 @@ fft_status run_pipeline_half(fft_plan_s* p, const void* in, void* out, const Fil
     fft_status s = ensure_workspace(p);
     if (s != FFT_OK) return s;
     const size_t grid_r = (size_t)N * M * sizeof(float);
+    // the Gaussian on 8192 rows: the half spectrum with rows padded to
+    // M/2 + 16 bins (a multiple of 16; the pad bins are never read back) so
+    // the one-pass column filter k_colfilt takes all its columns, applying
+    // g_N(u) g_M(v) / (N M) (its g_M-per-column mode); 0.50 -> ~0.25 ms for
+    // the 8192^2 column pass against k_cols' 8192-long column tiles
+    if (f.kind == FFT_FILTER_GAUSS && p->prec == 0 && N == 8192 && M >= 32 && colfilt_supported(N, M)) {
+        const int64_t ld = M / 2 + 16;
+        for (int64_t g = 0; g < p->batch; ++g) {
+            e = launch_rows_r2c(p->prec, M, (const char*)in + g * grid_r, p->ws, N, 1.0, p->tw, p->rtw, st, ld);
+            if (e == cudaSuccess) e = colfilt(p, p->ws, ld, 1, 1.0 / ((double)N * (double)M), p->gv, 0, st);
+            if (e == cudaSuccess)
+                e = launch_rows_c2r(p->prec, M, p->ws, (char*)out + g * grid_r, N, 1.0, p->tw, p->rtw, st, ld);
+            if (e != cudaSuccess) return cuda_fail(e, "half-spectrum pipeline (k_colfilt) launch");
+        }
+        p->last_launches = (int)(3 * p->batch);
+        return FFT_OK;
+    }
     for (int64_t g = 0; g < p->batch; ++g) {
         e = launch_rows_r2c(p->prec, M, (const char*)in + g * grid_r, p->ws, N, 1.0, p->tw, p->rtw, st);
         if (e == cudaSuccess)

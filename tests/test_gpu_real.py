@@ -165,3 +165,25 @@ def test_real_entry_point_errors(b):
     with pytest.raises(b.FFTError) as ei:
         q.forward_r2c(x, x)  # in place
     assert ei.value.status == 2
+
+
+@pytest.mark.parametrize("cols1", ["1", "0"])
+@pytest.mark.parametrize("M,batch", [(256, 2), (2048, 1), (32, 1)])
+def test_half_spectrum_pipeline_8192_rows_colfilt(b, M, batch, cols1, monkeypatch):
+    """8192-row real-to-real Gaussian pipelines: the half spectrum padded to
+    M/2 + 16 bins per row and filtered by the one-pass k_colfilt (g_N(u) g_M(v)
+    / (N M)), or (B200FFT_PIPE_COLS1=0) unpadded through k_cols, both against
+    the oracle."""
+    monkeypatch.setenv("B200FFT_PIPE_COLS1", cols1)
+    N = 8192
+    imgs = np.stack([fixtures.sky_image(N, M, seed=1960 + i, nsrc=200) for i in range(batch)])
+    p = b.Plan((N, M), batch=batch, flags=b.IN_REAL_F32 | b.OUT_REAL_F32)
+    x = torch.from_numpy(imgs).cuda()
+    o = torch.empty_like(x)
+    p.filter_pipeline(x, o, b.FILTER_GAUSS, 0.1)
+    torch.cuda.synchronize()
+    assert p.last_launch_count() == 3 * batch
+    H = oracle.gauss_filter(N, M, 0.1)
+    ref = np.stack([oracle.filter_pipeline_real(imgs[i], H)[0] for i in range(batch)])
+    assert oracle.rel_l2(o.cpu().numpy(), ref) <= 1e-5
+    p.destroy()
