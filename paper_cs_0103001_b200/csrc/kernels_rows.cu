@@ -180,7 +180,10 @@ cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const v
     const int64_t lines = R / 2;  // row pairs per pass
     const int64_t tiles = (lines + W - 1) / W;
     const int grid = (int)(tiles < grid_max ? tiles : grid_max);
-    const unsigned long long target = (++*gen) * (unsigned long long)grid;
+    // the counter grows by `grid` per completed launch: this launch's target;
+    // *gen advances only when the launch was accepted (a rejected launch
+    // must not leave later targets beyond what the counter can reach)
+    const unsigned long long target = (*gen + 1) * (unsigned long long)grid;
     static const int xo = [] {
         const char* w = getenv("B200FFT_ALLOW_WRONG");
         const char* v = getenv("B200FFT_ROWS_XO");
@@ -207,7 +210,9 @@ cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const v
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelExC(&cfg, (const void*)kern, args);
+    e = cudaLaunchKernelExC(&cfg, (const void*)kern, args);
+    if (e == cudaSuccess) ++*gen;
+    return e;
 }
 
 }  // namespace
