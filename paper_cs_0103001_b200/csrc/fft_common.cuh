@@ -123,11 +123,38 @@ __host__ __device__ constexpr double cos16(int e) {
     }
 }
 __host__ __device__ constexpr double sin16(int e) { return cos16(e - 4); }  // sin x = cos(x - pi/2)
+// cos of 2 pi e / 32: even e from cos16, odd e from the first-octant values
+// (exact decimal expansions, 20 digits) by the quadrant symmetries
+__host__ __device__ constexpr double cos32(int e) {
+    e &= 31;
+    if (!(e & 1)) return cos16(e / 2);
+    // cos(2 pi e / 32) for e = 1, 3, 5, 7 (and 9..15 = -cos of 16 - e)
+    const int q = e < 16 ? e : 32 - e;  // cos is even: fold to e <= 16
+    switch (q) {
+        case 1: return 0.98078528040323044913;
+        case 3: return 0.83146961230254523708;
+        case 5: return 0.55557023301960222474;
+        case 7: return 0.19509032201612826785;
+        case 9: return -0.19509032201612826785;
+        case 11: return -0.55557023301960222474;
+        case 13: return -0.83146961230254523708;
+        default: return -0.98078528040323044913;  // 15
+    }
+}
+__host__ __device__ constexpr double sin32(int e) { return cos32(e - 8); }
 
 // a * W_N^e with W_N = exp(-2 pi i / N) (forward) or exp(+2 pi i / N) (INV),
-// N in {1, 2, 4, 8, 16}; e is a compile-time constant after unrolling.
+// N in {1, 2, 4, 8, 16, 32}; e is a compile-time constant after unrolling.
 template <int N, bool INV, typename C>
 __device__ __forceinline__ C mulw(C a, int e) {
+    if constexpr (N == 32) {
+        const int e32 = e & 31;
+        if (!(e32 & 1)) return mulw<16, INV>(a, e32 / 2);
+        using T = decltype(a.x);
+        const T c = (T)cos32(e32);
+        const T s = INV ? (T)sin32(e32) : (T)(-sin32(e32));
+        return cmul(a, mk(c, s));
+    }
     const int e16 = (e * (16 / N)) & 15;
     using T = decltype(a.x);
     if (e16 == 0) return a;
@@ -140,7 +167,7 @@ __device__ __forceinline__ C mulw(C a, int e) {
 }
 
 // In-place DFT of N values v[0..N-1] (natural order in and out), N in
-// {1,2,4,8,16}.  Two-factor decomposition N = A * B:
+// {1,2,4,8,16,32}.  Two-factor decomposition N = A * B:
 //   Y[n1][k2] = sum_{n2<B} v[n1 + A n2] W_B^{n2 k2}
 //   Y[n1][k2] *= W_N^{n1 k2}
 //   V[k2 + B k1] = sum_{n1<A} Y[n1][k2] W_A^{n1 k1}
@@ -208,14 +235,19 @@ __host__ __device__ constexpr int tw_off(int R, int s, int ML = 4) {
 }
 __host__ __device__ constexpr int tw_size(int R, int ML = 4) { return tw_off(R, n_steps(R, ML), ML); }
 // all R = 2, 4, ..., 8192 tables concatenated (the ML = 4 set first, then
-// the ML = 3 set): base offset of R's table
+// the ML = 3 set, then the ML = 5 set of the radix-32 kernels): base offset
+// of R's table
 __host__ __device__ constexpr int tw_base_ml(int R, int ML) {
     return R <= 2 ? 0 : tw_base_ml(R / 2, ML) + tw_size(R / 2, ML);
 }
 __host__ __device__ constexpr int tw_base(int R, int ML = 4) {
-    return ML == 4 ? tw_base_ml(R, 4) : tw_base_ml(16384, 4) + tw_base_ml(R, ML);
+    return ML == 4   ? tw_base_ml(R, 4)
+           : ML == 3 ? tw_base_ml(16384, 4) + tw_base_ml(R, 3)
+                     : tw_base_ml(16384, 4) + tw_base_ml(16384, 3) + tw_base_ml(R, 5);  // ML = 5
 }
-__host__ __device__ constexpr int tw_total() { return tw_base_ml(16384, 4) + tw_base_ml(16384, 3); }
+__host__ __device__ constexpr int tw_total() {
+    return tw_base_ml(16384, 4) + tw_base_ml(16384, 3) + tw_base_ml(16384, 5);
+}
 // largest radix of a kernel holding E values per thread
 __host__ __device__ constexpr int ml_of(int E) { return E >= 16 ? 4 : (E >= 8 ? 3 : 4); }
 

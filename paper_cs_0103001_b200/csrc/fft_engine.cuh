@@ -91,10 +91,12 @@ __device__ __forceinline__ int il8(int i) { return (i ^ ((i >> 3) & 1)) * 8; }
 // rho - 1 loads -- for kernels whose warps are short of load bandwidth.
 // TWREC = 2 (complex64, R <= 256): from the constant table c_w256, for
 // kernels whose butterfly index is (nearly) uniform across a warp.
-template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false, int TWREC = (sizeof(T) == 4)>
+// MLX: the largest radix 2^MLX (0: ml_of(E); 5: radix-32 steps for E >= 32)
+template <typename T, int R, int E, bool INV, int LAYOUT = 0, bool PF = false, int TWREC = (sizeof(T) == 4),
+          int MLX = 0>
 struct LineFFT {
     using C = cpx<T>;
-    static constexpr int ML = ml_of(E);  // largest radix 2^ML (16, or 8 when E = 8)
+    static constexpr int ML = MLX ? MLX : ml_of(E);  // largest radix 2^ML (16, or 8 when E = 8; 32 with MLX 5)
     static constexpr int TPL = R / E;
     static constexpr int S = n_steps(R, ML);
     static constexpr int LS = pad16c(R) + 1;  // odd line stride in smem (slots)
@@ -204,6 +206,7 @@ struct LineFFT {
             } else if constexpr (LAYOUT == 4) {
 #pragma unroll
                 for (int q = 0; q < rho; ++q) line[il8(base + q * Ns)] = v[b * rho + q];
+
             } else if constexpr (Ns % 16 == 0) {
                 const int pb = pad16(base);
 #pragma unroll
@@ -241,6 +244,7 @@ struct LineFFT {
             } else if constexpr (LAYOUT == 4) {
 #pragma unroll
                 for (int r = 0; r < rho; ++r) v[b * rho + r] = line[il8(j + r * st)];
+
             } else if constexpr (st % 16 == 0) {
                 const int pj = pad16(j);
 #pragma unroll
@@ -331,12 +335,12 @@ __device__ __forceinline__ int64_t block_index(int64_t row, int v, int sh) {
 
 // FILT: a row filter pass of the separable pipeline: forward
 // transform -> * rowfilt[v] * scale -> inverse transform, stored unscaled.
-template <typename T, int R, int E, bool FILT, int LAYOUT = 0, bool PF = false, int TWREC = 0>
+template <typename T, int R, int E, bool FILT, int LAYOUT = 0, bool PF = false, int TWREC = 0, int MLX = 0>
 __device__ __forceinline__ void row_filter_pass(cpx<T>* v, cpx<T>* line, int lt, const cpx<T>* __restrict__ tw,
                                                 const T* __restrict__ rowfilt, T& scale, int bar = 0) {
     if constexpr (FILT) {
-        using F = LineFFT<T, R, E, false, LAYOUT, PF, TWREC>;
-        using FI = LineFFT<T, R, E, true, LAYOUT, PF, TWREC>;
+        using F = LineFFT<T, R, E, false, LAYOUT, PF, TWREC, MLX>;
+        using FI = LineFFT<T, R, E, true, LAYOUT, PF, TWREC, MLX>;
         cpx<T> w[E];
 #pragma unroll
         for (int m = 0; m < E; ++m)

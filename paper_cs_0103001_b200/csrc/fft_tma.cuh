@@ -200,6 +200,66 @@ __global__ void __launch_bounds__(W*(R / E), MINB)
 }
 
 // ---------------------------------------------------------------------------
+// k_rows_tma_g: long natural rows (one row per stage) processed by NG
+// independent thread groups of R/E threads each, E values per thread (the
+// 8192-point rows of C4: E = 32, two groups of 256 threads, radix-32 steps
+// (MLX 5: 8192 = 32 x 32 x 8, two exchanges per transform instead of the
+// three of radix 16): the row filter pass 430 -> 355 us, C4 0.897 -> 0.832
+// ms; the same groups with radix-16 steps measured no gain, a 33-slot
+// padding that removes the first write's 2-way bank conflicts measured
+// equal (it spills)).  Group g takes the CTA's tiles k = g, g + NG,
+// ... from the shared ring of STAGES stages; its steps synchronise on its own
+// named barrier (1 + g), so one group's exchanges and barriers overlap the
+// other's arithmetic, and each thread has twice the independent work of the
+// one-group E = 16 form.  The group that finishes a stage refills it with
+// the tile STAGES positions later (which another group may consume: the
+// per-stage mbarrier phase orders them).  Natural stores (no TRANS / PAIR).
+// ---------------------------------------------------------------------------
+template <typename T, int R, int E, int NG, bool INV, int STAGES, bool FILT, int MLX = 0>
+__global__ void __launch_bounds__(NG*(R / E), 1)
+    k_rows_tma_g(const void* __restrict__ in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
+                 const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt) {
+    using C = cpx<T>;
+    using F = LineFFT<T, R, E, INV, 0, false, true, MLX>;
+    using G = RowsTmaCfg<T, R, 1, false, STAGES>;
+    static_assert(F::TPL % 32 == 0 && NG <= 15, "whole warps per group, named barriers 1..NG");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t bar0 = smem_addr_u32(smem_raw + STAGES * G::STAGE_BYTES);
+    B200FFT_PDL_PROLOGUE();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        rows_tma_issue_first<T, R, E, 1, false, STAGES>(in_, batch, smem_raw, bar0);
+    }
+    __syncthreads();
+    const int g = threadIdx.x / F::TPL, lt = threadIdx.x % F::TPL;
+    const int bar = 1 + g;
+    for (int64_t k = g;; k += NG) {
+        const int64_t row = blockIdx.x + k * gridDim.x;
+        if (row >= batch) break;
+        const int s = (int)(k % STAGES);
+        mbar_wait(bar0 + 8 * s, (uint32_t)((k / STAGES) & 1));
+        C* line = reinterpret_cast<C*>(smem_raw + s * G::STAGE_BYTES);
+        C v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[F::pos_in(m)] = line[lt + F::TPL * m];
+        F::run(v, line, lt, tw, bar);
+        T sc = scale;
+        row_filter_pass<T, R, E, FILT, 0, false, true, MLX>(v, line, lt, tw, rowfilt, sc, bar);
+        C* o = out + row * R + lt;
+#pragma unroll
+        for (int m = 0; m < E; ++m) o[F::TPL * m] = cscale(v[F::pos_out(m)], sc);
+        F::lsync(bar);  // the group is done with stage s
+        if (lt == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const int64_t nk = k + STAGES;
+            if (blockIdx.x + nk * gridDim.x < batch)
+                rows_tma_issue<T, R, E, 1, false, STAGES>(in_, batch, smem_raw, bar0, blockIdx.x + nk * gridDim.x, s);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_rows_tma2: BOTH passes of the separable real-pair pipeline (C3's shape,
 // square R x R grids, R <= 2048) in ONE cooperative launch: pass 1 = the
 // row filter pass over the input's real-row pairs, stored transposed into

@@ -124,9 +124,37 @@ cudaError_t rows_tma_t(const void* in, void* out, int64_t batch, double scale, c
     return cudaGetLastError();
 }
 
+// 8192-point complex64 rows: two independent 256-thread groups, E = 32,
+// radix-32 steps (fft_tma.cuh k_rows_tma_g); B200FFT_ROWS_G2=0 selects the
+// one-group radix-16 k_rows_tma (the earlier form)
+template <bool INV, bool FILT>
+cudaError_t rows_g2_8192(const void* in, void* out, int64_t batch, double scale, const void* tw, const void* rowfilt,
+                         cudaStream_t st) {
+    constexpr int R = 8192, E = 32, NG = 2, STAGES = 3, ML = 5;
+    using G = RowsTmaCfg<float, R, 1, false, STAGES>;
+    auto kern = k_rows_tma_g<float, R, E, NG, INV, STAGES, FILT, ML>;
+    int grid_max = 0;
+    cudaError_t e = kernel_setup((const void*)kern, NG * (R / E), G::SMEM_BYTES, &grid_max);
+    if (e != cudaSuccess) return e;
+    if (batch <= 0) return cudaSuccess;
+    const int grid = (int)(batch < grid_max ? batch : grid_max);
+    kern<<<grid, NG * (R / E), G::SMEM_BYTES, st>>>(in, reinterpret_cast<float2*>(out), batch, (float)scale,
+                                                     reinterpret_cast<const float2*>(tw) + tw_base(R, ML),
+                                                     reinterpret_cast<const float*>(rowfilt));
+    return cudaGetLastError();
+}
+
+bool rows_g2() {
+    const char* v = getenv("B200FFT_ROWS_G2");
+    return !(v && v[0] == '0');
+}
+
 template <bool INV, bool REAL_IN, bool FILT>
 cudaError_t rows_tma_r(int64_t R, const void* in, void* out, int64_t batch, double scale, const void* tw,
                        const void* rowfilt, cudaStream_t st) {
+    if constexpr (!REAL_IN) {
+        if (R == 8192 && rows_g2()) return rows_g2_8192<INV, FILT>(in, out, batch, scale, tw, rowfilt, st);
+    }
     switch (R) {
         case 256: return rows_tma_t<float, 256, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);
         case 512: return rows_tma_t<float, 512, INV, REAL_IN, FILT>(in, out, batch, scale, tw, rowfilt, st);

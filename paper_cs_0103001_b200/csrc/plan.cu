@@ -93,7 +93,7 @@ void fill_step_tables(std::vector<double>& v) {
     static_assert(2 * RMAX == 16384, "tw_base's concatenation bound");
     const int total = tw_total();
     v.assign(2 * (size_t)total, 0.0);
-    for (int ml = 4; ml >= 3; --ml)
+    for (int ml = 5; ml >= 3; --ml)
     for (int R = 2; R <= RMAX; R *= 2) {
         for (int s = 1; s < n_steps(R, ml); ++s) {
             const int rho = radix_at(R, s, ml), Ns = span_at(R, s, ml);

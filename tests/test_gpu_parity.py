@@ -505,3 +505,30 @@ def test_colfilt_twiddle_variants(fft, tw, monkeypatch):
     f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=970 + int(tw)).reshape(N, M)
     out = run_pipeline(b, f, b.FILTER_GAUSS, 0.1)
     assert oracle.rel_l2(out, oracle.gauss_pipeline(f, 0.1)) <= 1e-5
+
+
+@pytest.mark.parametrize("g2", ["1", "0"])
+def test_8192_point_rows_both_kernels(fft, g2, monkeypatch):
+    """8192-point complex64 rows: the two-group radix-32 k_rows_tma_g (the
+    default) and the one-group radix-16 k_rows_tma (B200FFT_ROWS_G2=0), as 2D
+    forward / inverse rows on a 64 x 8192 grid and as the row filter pass of
+    the 4096 x 8192 Gaussian pipeline, against the oracle."""
+    import paper_cs_0103001_b200 as b
+
+    monkeypatch.setenv("B200FFT_ROWS_G2", g2)
+    N, M = 64, 8192
+    f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=980).reshape(N, M)
+    p = b.Plan((N, M), batch=1)
+    fd = torch.from_numpy(f).cuda()
+    F, g = torch.empty_like(fd), torch.empty_like(fd)
+    p.forward(fd, F)
+    p.inverse(F, g)
+    torch.cuda.synchronize()
+    p.destroy()
+    assert oracle.rel_l2(F.cpu().numpy(), oracle.fft2d(f)) <= 1e-5
+    assert oracle.rel_l2(g.cpu().numpy(), oracle.ifft2d(F.cpu().numpy())) <= 1e-5
+    # the row filter pass (fwd * g * inv) of the long-column Gaussian path
+    N = 4096
+    f = fixtures.complex_input(N * M, fixtures.UNIFORM, seed=981).reshape(N, M)
+    out = run_pipeline(b, f, b.FILTER_GAUSS, 0.1)
+    assert oracle.rel_l2(out, oracle.gauss_pipeline(f, 0.1)) <= 1e-5
