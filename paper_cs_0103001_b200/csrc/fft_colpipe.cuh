@@ -48,8 +48,9 @@ struct ColPipeCfg {
 // position -> (phase 0 = A, 1 = B, 2 = A', group, part); false for the
 // empty slots of the ramp-up / ramp-down blocks
 __device__ __forceinline__ bool cp_decode(int64_t p, int64_t G, int D, int& phase, int64_t& g, int& part) {
-    const int64_t j = p / 96;
-    const int r = (int)(p % 96);
+    // positions < 2^31 (launch_colfilt bounds the group count): 32-bit division
+    const int64_t j = (int64_t)((uint32_t)p / 96u);
+    const int r = (int)((uint32_t)p - (uint32_t)j * 96u);
     phase = r / 32;
     part = r % 32;
     g = j - (int64_t)phase * D;
@@ -57,9 +58,11 @@ __device__ __forceinline__ bool cp_decode(int64_t p, int64_t G, int D, int& phas
 }
 
 // group g -> (image, first column): shift / mask for a power-of-two number
-// of column groups per image, else (cg_sh < 0) a 32-bit division
+// of column groups per image (P2), else a 32-bit division (a separate
+// instantiation: the division's registers pushed the B task into spills)
+template <bool P2>
 __device__ __forceinline__ void cp_group(int64_t g, int64_t CG, int cg_sh, int& img, int& c0) {
-    if (cg_sh >= 0) {
+    if constexpr (P2) {
         img = (int)(g >> cg_sh);
         c0 = (int)(g & (CG - 1)) * 16;
     } else {
@@ -70,7 +73,7 @@ __device__ __forceinline__ void cp_group(int64_t g, int64_t CG, int cg_sh, int& 
 
 // grid: [nimg][8192][M] complex64 (in place); tl = W_N^x, x < N (fp64-generated);
 // gu = g_N[u] (N entries); gv = g_M (M_total entries, distributed slabs) or null
-template <int N2 = 128, int TW = 0>
+template <int N2 = 128, int TW = 0, bool P2 = true>
 __global__ void __launch_bounds__(320, 3)
     k_colfilt(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               float2* __restrict__ grid, int64_t M, int64_t nimg, float scale, const float2* __restrict__ tw64,
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(320, 3)
                 }
                 task[s] = i;
                 int img, c0;
-                cp_group(g, CG, cg_sh, img, c0);
+                cp_group<P2>(g, CG, cg_sh, img, c0);
                 if (phase != 2) {
                     while (*sigdone < na - NSIG + 1) __nanosleep(20);
                     ++na;
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(320, 3)
         int64_t g;
         cp_decode(i, groups, ctl.D, phase, g, part);
         int img_i, c0_i;
-        cp_group(g, CG, cg_sh, img_i, c0_i);
+        cp_group<P2>(g, CG, cg_sh, img_i, c0_i);
         const int64_t img = img_i, c0 = c0_i;
         float2 v[16];
         if (phase != 1) {

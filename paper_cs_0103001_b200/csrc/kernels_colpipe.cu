@@ -51,16 +51,16 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
     if (M < 16 || M % 16 || (M / 16) * nimg >= ((int64_t)1 << 30)) return cudaErrorInvalidValue;
     if (!ws || ws_bytes < colfilt_workspace_bytes(M, nimg)) return cudaErrorInvalidValue;
     int grid_n = 0;
-    // tuning: B200FFT_COLFILT_TW = bit 0: A / A' step twiddles, bit 1: B step
-    // twiddles from the constant table (else by recurrence).  Default 1: C4
-    // 0.8997 / 0.8955 / 1.043 ms for 0 / 1 / 2 (the B steps' constant loads
-    // push the 64-register B task into 300 B of spills)
+    // tuning: B200FFT_COLFILT_TW = 1 (default): the A / A' step twiddles from
+    // the constant table, 0: by recurrence (C4 0.8955 / 0.8997 ms; with the B
+    // steps' from the table too, 1.043 ms: the B task then spills 300 B)
     const char* twv = getenv("B200FFT_COLFILT_TW");
-    const int twm = twv ? atoi(twv) & 3 : 1;
-    const void* kern = twm == 0   ? (const void*)k_colfilt<128, 0>
-                       : twm == 1 ? (const void*)k_colfilt<128, 1>
-                       : twm == 2 ? (const void*)k_colfilt<128, 2>
-                                 : (const void*)k_colfilt<128, 3>;
+    const int twm = twv ? atoi(twv) & 1 : 1;
+    int cg_sh = 0;
+    while (((int64_t)1 << cg_sh) < M / 16) ++cg_sh;
+    const bool p2 = ((int64_t)1 << cg_sh) == M / 16;
+    const void* kern = p2 ? (twm ? (const void*)k_colfilt<128, 1, true> : (const void*)k_colfilt<128, 0, true>)
+                          : (twm ? (const void*)k_colfilt<128, 1, false> : (const void*)k_colfilt<128, 0, false>);
     cudaError_t e = kernel_setup(kern, 320, ColPipeCfg::SMEM, &grid_n);
     if (e == cudaSuccess) e = w256_upload();  // the constant step twiddles (fft_engine.cuh)
     if (e != cudaSuccess) return e;
@@ -89,11 +89,8 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
     const float* a_gu = reinterpret_cast<const float*>(gu);
     const float* a_gv = reinterpret_cast<const float*>(gv);
     int64_t a_off = col_off;
-    // column groups per image: a power of two (mask / shift indexing) or, for
-    // other widths, cg_sh = -1 (32-bit division)
-    int cg_sh = 0;
-    while (((int64_t)1 << cg_sh) < M / 16) ++cg_sh;
-    if (((int64_t)1 << cg_sh) != M / 16) cg_sh = -1;
+    // column groups per image: a power of two (mask / shift indexing, p2) or
+    // not (32-bit division)
     void* args[] = {&ma, &mb, &a_grid, &a_M, &a_nimg, &a_scale, &a_tw64, &a_tw128, &a_tl, &a_gu, &a_gv, &a_off,
                     &cg_sh, &c};
     cudaLaunchConfig_t cfg = {};

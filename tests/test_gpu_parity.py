@@ -493,10 +493,10 @@ def test_c2_tuning_variants(fft, bits, monkeypatch):
     p.destroy()
 
 
-@pytest.mark.parametrize("tw", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("tw", ["0", "1"])
 def test_colfilt_twiddle_variants(fft, tw, monkeypatch):
     """k_colfilt with each step-twiddle source (B200FFT_COLFILT_TW: A / A'
-    and B steps from the constant table or by recurrence) on an 8192 x 256
+    steps from the constant table or by recurrence) on an 8192 x 256
     Gaussian pipeline against the oracle."""
     import paper_cs_0103001_b200 as b
 
