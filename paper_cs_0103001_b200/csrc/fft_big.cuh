@@ -68,9 +68,13 @@ __device__ __forceinline__ float2 big_w(const float2* __restrict__ hi, const flo
     return cmul(__ldg(hi + (x >> 15)), __ldg(lo + (x & 32767)));
 }
 
-// XOR layout of pass 2's B exchange (32 lines of 128 points): conflict-free
-// for the lane-fastest writes (4 lines x 8 lanes) and line-fastest reads
-__device__ __forceinline__ int big_bx(int x, int line) { return x * 32 + (line ^ (((x >> 4) & 3) << 2)); }
+// XOR layout of pass 2's B exchange (32 lines of 128 points): element x of
+// line L at x * 32 + (L ^ 2 ((x / 16) mod 8)).  The writes (a half-warp = 2
+// lines x 8 lanes j, element 16 j + q) hit 16 distinct 8-B bank pairs (l ^ 2 j
+// for l < 2, j < 8), the line-fastest reads (x fixed) a permutation of each
+// half's 16 lines.  (The earlier L ^ 4 ((x / 16) mod 4) repeated every 4 j:
+// 2-way conflicts on every write -- ncu: 209 M excess wavefronts per pass.)
+__device__ __forceinline__ int big_bx(int x, int line) { return x * 32 + (line ^ (((x >> 4) & 7) << 1)); }
 
 template <bool INV, int PASS>
 __global__ void __launch_bounds__(320, 3)
