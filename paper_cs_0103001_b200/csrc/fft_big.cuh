@@ -272,11 +272,24 @@ __global__ void __launch_bounds__(320, 3)
                 // outputs c[jp + 16 q] = u[b 8 + q]: ka = jp + 16 q -> X[k2 + N2 (kc + 256 ka)]
                 const int64_t k2 = 16 * g + t;
                 float2* o = out + k2 + L * kc;
+                if (xo & 4) {  // timing experiment (wrong order): one contiguous 32 KiB block per task
+                    float2* oc = out + (g * 128 + part) * 4096 + line;
 #pragma unroll
-                for (int b = 0; b < 2; ++b)
+                    for (int b = 0; b < 2; ++b)
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        st_pol(o + (int64_t)(lt + 8 * b + 16 * q) * 256 * L, u[b * 8 + q], stream);
+                        for (int q = 0; q < 8; ++q) oc[(lt + 8 * b + 16 * q) * 32] = u[b * 8 + q];
+                } else if (xo & 8) {  // X without a cache hint
+#pragma unroll
+                    for (int b = 0; b < 2; ++b)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) o[(int64_t)(lt + 8 * b + 16 * q) * 256 * L] = u[b * 8 + q];
+                } else {
+#pragma unroll
+                    for (int b = 0; b < 2; ++b)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            st_pol(o + (int64_t)(lt + 8 * b + 16 * q) * 256 * L, u[b * 8 + q], stream);
+                }
             }
         }
     }
