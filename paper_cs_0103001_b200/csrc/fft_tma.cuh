@@ -94,7 +94,8 @@ __device__ __forceinline__ void rows_tma_issue_first(const void* in_, int64_t ba
 // COMPLEX grid (a', 0), (b', 0) -- the last pass of a real-input pipeline
 // with complex output, whose exact result is real.
 // xo: timing experiments only (wrong results): 1 = no FFT arithmetic, 2 = no stores.
-template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT, bool TRANS, int PAIR>
+template <typename T, int R, int E, int W, bool INV, bool REAL_IN, int STAGES, bool FILT, bool TRANS, int PAIR,
+          int MLX = 0>
 __device__ __forceinline__ void rows_tma_loop(const void* in_, cpx<T>* __restrict__ out, int64_t batch, T scale,
                                               const cpx<T>* __restrict__ tw, const T* __restrict__ rowfilt, int xo,
                                               unsigned char* smem_raw, uint32_t bar0) {
@@ -105,7 +106,7 @@ __device__ __forceinline__ void rows_tma_loop(const void* in_, cpx<T>* __restric
     // step twiddles: prefetched table entries (default) or, with
     // B200FFT_ROWS_TWREC, powers of one entry (LineFFT TWREC)
     constexpr bool TWR = B200FFT_ROWS_TWREC != 0;
-    using F = LineFFT<T, R, E, INV, 0, !TWR, TWR>;
+    using F = LineFFT<T, R, E, INV, 0, !TWR, TWR, MLX>;
     using G = RowsTmaCfg<T, R, W, REAL_IN, STAGES>;
     const int tid = threadIdx.x;
     const int t = tid / F::TPL, lt = tid % F::TPL;
@@ -134,7 +135,7 @@ __device__ __forceinline__ void rows_tma_loop(const void* in_, cpx<T>* __restric
         T sc = scale;
         if (!(xo & 1)) {
             F::run(v, line, lt, tw, bar);
-            row_filter_pass<T, R, E, FILT, 0, !TWR, TWR>(v, line, lt, tw, rowfilt, sc, bar);
+            row_filter_pass<T, R, E, FILT, 0, !TWR, TWR, MLX>(v, line, lt, tw, rowfilt, sc, bar);
         }
         const int64_t row = tile * W + t;
         if (xo & 2) {
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(NG*(R / E), 1)
 // proxy) reads of pass 2.  *gbar only grows: the host passes target =
 // (launch number) x gridDim.  All CTAs are co-resident (cooperative launch).
 // ---------------------------------------------------------------------------
-template <int R, int E, int W, int STAGES, int PAIR2>
+template <int R, int E, int W, int STAGES, int PAIR2, int MLX = 0>
 __global__ void __launch_bounds__(W*(R / E), 1)
     k_rows_tma2(const void* __restrict__ in_, float2* __restrict__ mid, void* __restrict__ out_, int64_t lines,
                 const float2* __restrict__ tw, float scale1, const float* __restrict__ filt1, float scale2,
@@ -290,8 +291,8 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         rows_tma_issue_first<float, R, E, W, false, STAGES>(in_, lines, smem_raw, bar0);
     }
     __syncthreads();
-    rows_tma_loop<float, R, E, W, false, false, STAGES, true, true, 1>(in_, mid, lines, scale1, tw, filt1, xo,
-                                                                      smem_raw, bar0);
+    rows_tma_loop<float, R, E, W, false, false, STAGES, true, true, 1, MLX>(in_, mid, lines, scale1, tw, filt1, xo,
+                                                                           smem_raw, bar0);
     // ---- grid barrier (the loop ended with a __syncthreads) ----
     if (threadIdx.x == 0) {
         asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(W*(R / E), 1)
         rows_tma_issue_first<float, R, E, W, false, STAGES>(mid, lines, smem_raw, bar1);
     }
     __syncthreads();
-    rows_tma_loop<float, R, E, W, false, false, STAGES, true, true, PAIR2>(
+    rows_tma_loop<float, R, E, W, false, false, STAGES, true, true, PAIR2, MLX>(
         mid, reinterpret_cast<float2*>(out_), lines, scale2, tw, filt2, xo, smem_raw, bar1);
 }
 

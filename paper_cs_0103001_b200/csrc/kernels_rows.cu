@@ -193,14 +193,18 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
 
 // both passes of the square real-pair pipeline in one cooperative launch
 // (fft_tma.cuh k_rows_tma2); 3 stages of ~64 KiB, 512 threads, one CTA per SM
-template <int R, int PAIR2>
+// E = 16, tiles of ~64 KiB (4 line pairs at R = 2048), 3 stages.  (8-pair
+// tiles with E = 32 and one 128 KiB stage -- one tile per CTA and pass --
+// measured 37.9-38.9 us with radix-16 steps, 43.0 with radix-32 (spills):
+// profiles/README.md)
+template <int R, int PAIR2, int CFG = 0>
 cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const void* filt1, double scale2,
                     const void* filt2, const void* tw, unsigned long long* gbar, unsigned long long* gen,
                     cudaStream_t st) {
-    constexpr int E = 16, STAGES = 3;
-    constexpr int W = (int)((64 * 1024) / (R * sizeof(float2)));
+    constexpr int E = CFG ? 32 : 16, STAGES = CFG ? 1 : 3, MLX = CFG == 2 ? 5 : 0;
+    constexpr int W = CFG ? 8 : (int)((64 * 1024) / (R * sizeof(float2)));
     using G = RowsTmaCfg<float, R, W, false, STAGES>;
-    auto kern = k_rows_tma2<R, E, W, STAGES, PAIR2>;
+    auto kern = k_rows_tma2<R, E, W, STAGES, PAIR2, MLX>;
     const size_t smem = G::SMEM_BYTES + 8 * STAGES;  // a second set of stage barriers
     int grid_max = 0;
     cudaError_t e = kernel_setup((const void*)kern, W * (R / E), smem, &grid_max);
@@ -221,7 +225,7 @@ cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const v
     float2* a_mid = reinterpret_cast<float2*>(mid);
     void* a_out = out;
     int64_t a_lines = lines;
-    const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(R, ml_of(E));
+    const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(R, MLX ? MLX : ml_of(E));
     float a_s1 = (float)scale1, a_s2 = (float)scale2;
     const float* a_f1 = reinterpret_cast<const float*>(filt1);
     const float* a_f2 = reinterpret_cast<const float*>(filt2);
@@ -253,8 +257,8 @@ bool rows_filter2_supported(int prec, int64_t N, int64_t M) {
 cudaError_t launch_rows_filter2(int64_t R, const void* in, void* mid, void* out, double scale1, const void* filt1,
                                 double scale2, const void* filt2, const void* tw, int pair2, unsigned long long* gbar,
                                 unsigned long long* gen, cudaStream_t st) {
-    switch (R) {
     if (pair2 != 2) return cudaErrorInvalidValue;  // complex output only (the C3 form)
+    switch (R) {
 #define B200_R2_CASE(r) \
     case r: return rows2_t<r, 2>(in, mid, out, scale1, filt1, scale2, filt2, tw, gbar, gen, st);
         B200_R2_CASE(512) B200_R2_CASE(1024) B200_R2_CASE(2048)
