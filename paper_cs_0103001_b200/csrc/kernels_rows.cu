@@ -197,12 +197,12 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
 // tiles with E = 32 and one 128 KiB stage -- one tile per CTA and pass --
 // measured 37.9-38.9 us with radix-16 steps, 43.0 with radix-32 (spills):
 // profiles/README.md)
-template <int R, int PAIR2, int CFG = 0>
+template <int R, int PAIR2>
 cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const void* filt1, double scale2,
                     const void* filt2, const void* tw, unsigned long long* gbar, unsigned long long* gen,
                     cudaStream_t st) {
-    constexpr int E = CFG ? 32 : 16, STAGES = CFG ? 1 : 3, MLX = CFG == 2 ? 5 : 0;
-    constexpr int W = CFG ? 8 : (int)((64 * 1024) / (R * sizeof(float2)));
+    constexpr int E = 16, STAGES = 3, MLX = 0;
+    constexpr int W = (int)((64 * 1024) / (R * sizeof(float2)));
     using G = RowsTmaCfg<float, R, W, false, STAGES>;
     auto kern = k_rows_tma2<R, E, W, STAGES, PAIR2, MLX>;
     const size_t smem = G::SMEM_BYTES + 8 * STAGES;  // a second set of stage barriers
