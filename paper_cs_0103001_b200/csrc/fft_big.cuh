@@ -224,7 +224,14 @@ __global__ void __launch_bounds__(320, 3)
                 float2 wm = big_w(whi, wlo, n1 * (kc + 256 * lt));
                 const float2 ws = big_w(whi, wlo, n1 * 2048);
                 float2* o = out + (kc + 256 * lt) * L + n1;
-                if (xo & 2) {
+                if (xo & 16) {  // timing experiment (wrong order): one contiguous 32 KiB block per task
+                    float2* oc = out + (g * 128 + part) * 4096 + (lt * 16) * 32 + line;
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) {
+                        oc[m * 32] = cmul_dir<INV>(v[FB::pos_out(m)], wm);
+                        wm = cmul(wm, ws);
+                    }
+                } else if (xo & 2) {
 #pragma unroll
                     for (int m = 0; m < 16; ++m) {
                         o[(int64_t)m * 2048 * L] = cmul_dir<INV>(v[FB::pos_out(m)], wm);

@@ -81,8 +81,9 @@ cudaError_t big_pass(const void* in, void* out, double scale, const void* tw, co
     const float2* a_lo = reinterpret_cast<const float2*>(wlo);
     // B200FFT_BIG_XO (tuning): pass 1's Y stores 0 = evict-last, 1 = evict-first,
     // 2 = without a cache hint (default: C5 19.97 / 19.69 / 19.69 ms fwd + inv);
-    // + 8: pass 2's X stores without a hint (else evict-first); + 4: timing
-    // experiment, pass 2's X stored as contiguous blocks (wrong order)
+    // + 8: pass 2's X stores without a hint (else evict-first); + 4 / + 16:
+    // timing experiments, pass 2's X / pass 1's Y stored as contiguous blocks
+    // (wrong order)
     static const int xo = [] {
         const char* v = getenv("B200FFT_BIG_XO");
         return v ? atoi(v) : 2;
