@@ -255,6 +255,25 @@ fft_status fft_nccl_unique_id(unsigned char id[128]); /* on one rank; broadcast 
  * (batch x N/nranks x M elements per call); rank-1 plans keep their own
  * (local) batch and run without any collective. */
 fft_status fft_plan_set_comm(fft_plan plan, const unsigned char id[128], int nranks, int my_rank);
+/* Tests on ONE GPU: the cross-process data plane of the fused schedules
+ * without NCCL (NCCL refuses two ranks on one device).  The two collectives
+ * of the fused schedules -- the IPC-handle all-gather (and the all-ranks-
+ * mapped check) and the stream-ordered barrier -- are done by the caller's
+ * host callbacks instead: allgather(ctx, mine, all, bytes) gathers `bytes`
+ * from every rank into all[nranks * bytes] (rank order), barrier(ctx) blocks
+ * until every rank has called it; both return 0 on success.  A barrier first
+ * drains the plan's stream (cudaStreamSynchronize), so no kernel ever waits
+ * on another process.  Everything else -- the slab layouts, the receive
+ * slabs mapped by cudaIpcOpenMemHandle, the kernels' stores into and loads
+ * from the other ranks' slabs, the schedule -- is the fft_plan_set_comm
+ * path's.  Collective; same argument rules as fft_plan_set_comm; the
+ * ncclSend/Recv all-to-all (B200FFT_P2P=0) and fft_forward_paper_tree are
+ * NCCL-only (FFT_E_UNSUPPORTED).  The callbacks and ctx must stay valid
+ * until fft_plan_destroy. */
+typedef int (*fft_host_allgather_fn)(void* ctx, const void* mine, void* all, size_t bytes);
+typedef int (*fft_host_barrier_fn)(void* ctx);
+fft_status fft_plan_set_host_collectives(fft_plan plan, int nranks, int my_rank, fft_host_allgather_fn allgather,
+                                        fft_host_barrier_fn barrier, void* ctx);
 /* Tests / diagnostics: run the slab-decomposed schedule of a rank-2 plan (or
  * the four-step of a rank-1, batch-1 plan) as `nranks` virtual ranks on this
  * one GPU: the fused schedule with local slabs in place of peer memory

@@ -36,7 +36,8 @@ EXPORTS = [
     "fft_plan_create", "fft_plan_create_ex", "fft_plan_set_stream", "fft_plan_workspace_bytes",
     "fft_plan_set_workspace", "fft_forward", "fft_inverse", "fft2d_filter_pipeline", "fft2d_image_filter_u8",
     "fft_forward_paper_tree",
-    "fft_execute_host", "fft_nccl_unique_id", "fft_plan_set_comm", "fft_plan_set_virtual_ranks",
+    "fft_execute_host", "fft_nccl_unique_id", "fft_plan_set_comm", "fft_plan_set_host_collectives",
+    "fft_plan_set_virtual_ranks",
     "fft_plan_destroy",
     "fft_status_string", "fft_last_error", "fft_plan_last_launch_count", "fft_build_info",
     "fft_plan_set_profiling", "fft_plan_phase_times", "fft_forward_r2c", "fft_inverse_c2r",
@@ -50,6 +51,10 @@ class FFTError(RuntimeError):
 
 
 _lib = None
+
+# fft_host_allgather_fn / fft_host_barrier_fn (include/b200fft.h)
+HOST_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t)
+HOST_BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -76,6 +81,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fft_forward_paper_tree": ([vp, vp, vp], ci),
         "fft_nccl_unique_id": ([ctypes.c_char_p], ci),
         "fft_plan_set_comm": ([vp, ctypes.c_char_p, ci, ci], ci),
+        "fft_plan_set_host_collectives": ([vp, ci, ci, HOST_ALLGATHER_FN, HOST_BARRIER_FN, vp], ci),
         "fft_plan_set_virtual_ranks": ([vp, ci], ci),
         "fft_plan_destroy": ([vp], ci),
         "fft_status_string": ([ci], ctypes.c_char_p),
@@ -202,6 +208,32 @@ class Plan:
     def set_comm(self, unique_id: bytes, nranks: int, rank: int) -> None:
         _check(load_library().fft_plan_set_comm(self._h, unique_id, int(nranks), int(rank)),
                "fft_plan_set_comm")
+
+    def set_host_collectives(self, nranks: int, rank: int, allgather, barrier) -> None:
+        """Tests on one GPU (fft_plan_set_host_collectives): the fused
+        schedules' two collectives by host callables -- ``allgather(mine:
+        bytes) -> list of nranks bytes`` (rank order) and ``barrier()`` --
+        e.g. over a gloo process group; the data plane is the NCCL path's."""
+        def _ag(ctx, mine, out, nbytes):
+            try:
+                parts = allgather(ctypes.string_at(mine, nbytes))
+                blob = b"".join(parts)
+                assert len(blob) == nranks * nbytes
+                ctypes.memmove(out, blob, len(blob))
+                return 0
+            except Exception:  # reported to the library as a failed collective
+                return 1
+
+        def _bar(ctx):
+            try:
+                barrier()
+                return 0
+            except Exception:
+                return 1
+        self._hc = (HOST_ALLGATHER_FN(_ag), HOST_BARRIER_FN(_bar))  # kept alive with the plan
+        _check(load_library().fft_plan_set_host_collectives(self._h, int(nranks), int(rank), self._hc[0],
+                                                            self._hc[1], None),
+               "fft_plan_set_host_collectives")
 
     def set_virtual_ranks(self, nranks: int) -> None:
         """Tests: emulate the slab decomposition over ``nranks`` virtual ranks on this GPU."""

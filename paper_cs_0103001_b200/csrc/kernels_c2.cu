@@ -9,6 +9,7 @@
 #include <mutex>
 
 #include "fft_c2.cuh"
+#include "fft_c2pair.cuh"
 #include "launch.h"
 
 namespace b200fft {
@@ -251,6 +252,69 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     return cudaLaunchKernelExC(&cfg, c2_kernel(kind, INV), kind == C2_WS ? args_ws : args_st);
 }
 
+// k_ab_pair (fft_c2pair.cuh): one 2-CTA cluster per transform, Y in TMEM;
+// grid = 2 x the co-resident clusters (at most one per transform)
+std::mutex g_pair_mu;
+std::map<int, int> g_pair_clusters;  // [device] -> co-resident 2-CTA clusters
+
+template <bool INV>
+cudaError_t pair_launch(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
+                        cudaStream_t st) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (batch <= 0) return cudaSuccess;
+    if ((e = w256_upload()) != cudaSuccess) return e;
+    const void* kern = (const void*)k_ab_pair<INV>;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(PairCfg::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = PairCfg::SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_pair_mu);
+        auto it = g_pair_clusters.find(dev * 2 + (INV ? 1 : 0));
+        if (it == g_pair_clusters.end()) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairCfg::SMEM);
+            if (e != cudaSuccess) return e;
+            cfg.gridDim = dim3(296, 1, 1);
+            e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+            if (e != cudaSuccess) return e;
+            if (ncl < 1) return cudaErrorInvalidConfiguration;
+            g_pair_clusters[dev * 2 + (INV ? 1 : 0)] = ncl;
+            if (getenv("B200FFT_VERBOSE")) fprintf(stderr, "c2 pair: device %d, %d clusters of 2\n", dev, ncl);
+        } else {
+            ncl = it->second;
+        }
+    }
+    const int64_t npairs = batch < ncl ? batch : ncl;
+    cfg.gridDim = dim3((unsigned)(2 * npairs), 1, 1);
+    CUtensorMap m_x;
+    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, 0)) return cudaErrorInvalidValue;
+    float a_scale = (float)scale;
+    const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
+    const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
+    int64_t a_batch = batch;
+    float2* a_out = reinterpret_cast<float2*>(out);
+    const char* w = getenv("B200FFT_ALLOW_WRONG");
+    const char* x = getenv("B200FFT_PAIR_XO");
+    int a_xo = (w && w[0] == '1' && x) ? atoi(x) : 0;
+    void* args[] = {&m_x, &a_out, &a_batch, &a_scale, &a_tw4, &a_tw, &a_xo};
+    return cudaLaunchKernelExC(&cfg, kern, args);
+}
+
+bool c2_pair_selected() {
+    const char* v = getenv("B200FFT_C2");
+    return v && !strcmp(v, "pair");
+}
+
 }  // namespace
 
 bool c2_supported(int prec, int64_t n, int* n1, int* n2) {
@@ -292,6 +356,9 @@ size_t c2_workspace_bytes(int64_t batch) {
 
 cudaError_t launch_c2(bool inv, const void* in, void* out, int64_t batch, double scale, const void* tw4,
                       const void* tw, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (c2_pair_selected())
+        return inv ? pair_launch<true>(in, out, batch, scale, tw4, tw, st)
+                   : pair_launch<false>(in, out, batch, scale, tw4, tw, st);
     return inv ? ab_launch<true>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st)
                : ab_launch<false>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
 }

@@ -166,6 +166,13 @@ struct fft_plan_s {
     // distributed (slab decomposition of rank-2 plans)
     int nranks = 1, my_rank = 0;
     void* comm = nullptr;  // ncclComm_t owned by the plan
+    // test mode (fft_plan_set_host_collectives): the IPC-handle all-gather and
+    // the barriers are host callbacks instead of NCCL (comm stays null); the
+    // data plane (IPC mappings, peer stores / loads by the kernels) is the same
+    fft_host_allgather_fn hc_allgather = nullptr;
+    fft_host_barrier_fn hc_barrier = nullptr;
+    void* hc_ctx = nullptr;
+    bool multi() const { return comm != nullptr || hc_barrier != nullptr; }
     int virt = 1;          // virtual ranks emulated on this GPU (tests), 1 = off
     // fused all-to-alls of the 2D slab schedule:
     // every rank's receive slabs (2 phases) mapped into every rank by CUDA IPC
@@ -217,13 +224,13 @@ struct fft_plan_s {
     int pn = 0;
 
     size_t elem_bytes() const { return prec == 0 ? 8 : 16; }
-    int P() const { return comm ? nranks : virt; }
+    int P() const { return multi() ? nranks : virt; }
     // slab-decomposed schedule: a communicator (any size, 1 included) or virtual ranks
-    bool dist() const { return (rank == 2 || batch == 1) && (comm != nullptr || virt > 1); }
+    bool dist() const { return (rank == 2 || batch == 1) && (multi() || virt > 1); }
     // elements addressed by one call: the local slab (NCCL) or everything (virtual)
     int64_t elems() const {
-        if (rank == 1 && batch == 1 && comm) return n0 / nranks;
-        if (rank == 2 && comm) return batch * (n0 / nranks) * n1;
+        if (rank == 1 && batch == 1 && multi()) return n0 / nranks;
+        if (rank == 2 && multi()) return batch * (n0 / nranks) * n1;
         return batch * n0 * (rank == 2 ? n1 : 1);
     }
 };
@@ -833,7 +840,8 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
 fft_status dist_exchange(fft_plan_s* p, char* send, char* recv, int64_t blk, cudaStream_t st) {
     const int P = p->P();
     const size_t eb = p->elem_bytes(), bytes = (size_t)blk * eb;
-    if (p->comm) {
+    if (p->multi()) {
+        if (!p->comm) return fail(FFT_E_UNSUPPORTED, "host collectives: the peer-memory schedule only");
 #ifdef B200FFT_WITH_NCCL
         ncclComm_t comm = (ncclComm_t)p->comm;
         const ncclDataType_t dt = p->prec == 0 ? ncclFloat : ncclDouble;
@@ -947,13 +955,19 @@ fft_status p2p_prepare(fft_plan_s* p, cudaStream_t st) {
     // the handshake buffer was allocated by fft_plan_set_comm, so no local
     // failure can make this rank skip the all-gather the others are in
     static_assert(sizeof(Rec) * (kMaxBlocks + 1) <= 4096, "handshake buffer");
-    char* d = (char*)p->ctl_buf;
     std::vector<Rec> all(P);
-    cudaError_t e = cudaMemcpyAsync(d + P * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, st);
-    ncclResult_t r = ncclAllGather(d + P * sizeof(Rec), d, sizeof(Rec), ncclChar, comm, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(all.data(), d, sizeof(Rec) * P, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    bool all_ok = e == cudaSuccess && r == ncclSuccess;
+    char* d = (char*)p->ctl_buf;
+    bool all_ok;
+    if (!comm) {  // host collectives (tests)
+        cudaError_t e = cudaStreamSynchronize(st);
+        all_ok = p->hc_allgather(p->hc_ctx, &mine, all.data(), sizeof(Rec)) == 0 && e == cudaSuccess;
+    } else {
+        cudaError_t e = cudaMemcpyAsync(d + P * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, st);
+        ncclResult_t r = ncclAllGather(d + P * sizeof(Rec), d, sizeof(Rec), ncclChar, comm, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(all.data(), d, sizeof(Rec) * P, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        all_ok = e == cudaSuccess && r == ncclSuccess;
+    }
     for (int q = 0; q < P && all_ok; ++q) all_ok = all[q].ok != 0;
     int opened = 1;
     if (all_ok) {
@@ -967,12 +981,18 @@ fft_status p2p_prepare(fft_plan_s* p, cudaStream_t st) {
             }
         }
         // every rank must have mapped every peer
-        int* f = reinterpret_cast<int*>(d);
-        e = cudaMemcpyAsync(f, &opened, sizeof(int), cudaMemcpyHostToDevice, st);
-        r = ncclAllReduce(f, f, 1, ncclInt32, ncclMin, comm, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(&opened, f, sizeof(int), cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        all_ok = e == cudaSuccess && r == ncclSuccess && opened == 1;
+        if (!comm) {
+            std::vector<int> op(P);
+            all_ok = p->hc_allgather(p->hc_ctx, &opened, op.data(), sizeof(int)) == 0;
+            for (int q = 0; q < P && all_ok; ++q) all_ok = op[q] == 1;
+        } else {
+            int* f = reinterpret_cast<int*>(d);
+            cudaError_t e = cudaMemcpyAsync(f, &opened, sizeof(int), cudaMemcpyHostToDevice, st);
+            ncclResult_t r = ncclAllReduce(f, f, 1, ncclInt32, ncclMin, comm, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&opened, f, sizeof(int), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            all_ok = e == cudaSuccess && r == ncclSuccess && opened == 1;
+        }
     }
     if (!all_ok) p2p_release(p);
     p->p2p = all_ok ? 1 : -1;
@@ -993,6 +1013,12 @@ fft_status nccl_async_check(fft_plan_s* p) {
 }
 
 fft_status dist_barrier(fft_plan_s* p, cudaStream_t st) {
+    if (!p->comm) {  // host collectives (tests): drain, then the host barrier
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "barrier");
+        if (p->hc_barrier(p->hc_ctx) != 0) return fail(FFT_E_NCCL, "host barrier failed");
+        return FFT_OK;
+    }
     ncclResult_t r = ncclAllReduce(p->bar_buf, p->bar_buf, 1, ncclFloat, ncclSum, (ncclComm_t)p->comm, st);
     if (r != ncclSuccess) return fail(FFT_E_NCCL, std::string("barrier: ") + ncclGetErrorString(r));
     return FFT_OK;
@@ -1010,10 +1036,10 @@ fft_status run_dist_2d_fused(fft_plan_s* p, const void* in, void* out, int mode,
     const size_t eb = p->elem_bytes();
     const int64_t slab = SN * M, blk = SN * SM;
     const int sh = ilog2(SM);
-    const int nloc = p->comm ? 1 : P;
-    const int r0 = p->comm ? p->my_rank : 0;
+    const int nloc = p->multi() ? 1 : P;
+    const int r0 = p->multi() ? p->my_rank : 0;
     char* vbase = nullptr;
-    if (p->comm) {
+    if (p->multi()) {
 #ifdef B200FFT_WITH_NCCL
         fft_status s = p2p_prepare(p, st);
         if (s != FFT_OK) return s;
@@ -1034,7 +1060,7 @@ fft_status run_dist_2d_fused(fft_plan_s* p, const void* in, void* out, int mode,
         const int ph = (int)(p->dist_phase++ & 1);
         // rank q's receive (column) slab of this phase
         auto rslab = [&](int q) -> char* {
-            return p->comm ? (char*)p->peer_buf[q] + (size_t)ph * slab * eb
+            return p->multi() ? (char*)p->peer_buf[q] + (size_t)ph * slab * eb
                            : vbase + ((size_t)ph * P + q) * slab * eb;
         };
         const char* gin = (const char*)in + (size_t)g * nloc * slab * in_eb;
@@ -1051,7 +1077,7 @@ fft_status run_dist_2d_fused(fft_plan_s* p, const void* in, void* out, int mode,
         }
         prof_mark(p, st, "rows+exchange(peer stores)");
 #ifdef B200FFT_WITH_NCCL
-        if (p->comm) {
+        if (p->multi()) {
             fft_status s = dist_barrier(p, st);
             if (s != FFT_OK) return s;
             prof_mark(p, st, "barrier");
@@ -1064,7 +1090,7 @@ fft_status run_dist_2d_fused(fft_plan_s* p, const void* in, void* out, int mode,
         }
         prof_mark(p, st, "columns");
 #ifdef B200FFT_WITH_NCCL
-        if (p->comm) {
+        if (p->multi()) {
             fft_status s = dist_barrier(p, st);
             if (s != FFT_OK) return s;
             prof_mark(p, st, "barrier");
@@ -1103,8 +1129,8 @@ fft_status run_dist_2d(fft_plan_s* p, const void* in, void* out, int mode, fft_f
     const int64_t slab = SN * M;      // elements per rank per grid
     const int64_t blk = SN * SM;      // elements per (rank, peer) block
     const int sh = ilog2(SM);
-    const int nloc = p->comm ? 1 : P;  // slabs handled by this process
-    const int r0 = p->comm ? p->my_rank : 0;
+    const int nloc = p->multi() ? 1 : P;  // slabs handled by this process
+    const int r0 = p->multi() ? p->my_rank : 0;
     const bool real_in = mode == 2 && (p->flags & FFT_IN_REAL_F32);
     const size_t in_eb = real_in ? 4 : eb;
     FilterArgs f{};
@@ -1248,7 +1274,7 @@ cudaError_t unpack_blocks(char* dst, const char* src, int64_t R, int64_t Cb, int
 fft_status tree_prepare(fft_plan_s* p) {
     const int P = p->P();
     const int64_t n = p->n0, L = n / P;
-    const int nloc = p->comm ? 1 : P;
+    const int nloc = p->multi() ? 1 : P;
     if (!p->tree_sub || p->tree_sub->n0 != L || p->tree_sub->batch != nloc) {
         if (p->tree_sub) fft_plan_destroy(p->tree_sub);
         p->tree_sub = nullptr;
@@ -1279,7 +1305,7 @@ fft_status tree_prepare(fft_plan_s* p) {
     // communicator needs its largest vector twice plus the received half
     const size_t eb = p->elem_bytes();
     size_t need;
-    if (!p->comm) {
+    if (!p->multi()) {
         need = 2 * (size_t)n * eb;
     } else {
         int64_t mx = L;
@@ -1309,7 +1335,7 @@ fft_status run_paper_tree(fft_plan_s* p, const void* in, void* out, cudaStream_t
     char* B = A + (size_t)n * eb;  // virtual ranks; a communicator rank re-slices below
     int launches = 0;
     p->tree_sub->stream = st;
-    if (!p->comm) {
+    if (!p->multi()) {
         // 1. every branch: P slabs of n/P, one batched forward (1/(n/P))
         s = run_1d(p->tree_sub, in, A, false, st);
         if (s != FFT_OK) return s;
@@ -1332,6 +1358,7 @@ fft_status run_paper_tree(fft_plan_s* p, const void* in, void* out, cudaStream_t
         return FFT_OK;
     }
 #ifdef B200FFT_WITH_NCCL
+    if (!p->comm) return fail(FFT_E_UNSUPPORTED, "host collectives: no tree schedule");
     const int q = p->my_rank;
     int64_t mx = M;
     for (int S = P; S > 1; S /= 2)
@@ -1396,7 +1423,7 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
     fft_status s = fs_prepare(p);
     if (s != FFT_OK) return s;
     char* vbase = nullptr;
-    if (p->comm) {
+    if (p->multi()) {
 #ifdef B200FFT_WITH_NCCL
         s = p2p_prepare(p, st);
         if (s != FFT_OK) return s;
@@ -1414,13 +1441,13 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
     const int64_t N1 = p->fs1, N2 = p->fs2, S1 = N1 / P, S2 = N2 / P;
     const int64_t loc = p->n0 / P;
     const size_t eb = p->elem_bytes();
-    const int nloc = p->comm ? 1 : P;
-    const int r0 = p->comm ? p->my_rank : 0;
+    const int nloc = p->multi() ? 1 : P;
+    const int r0 = p->multi() ? p->my_rank : 0;
     auto buf = [&](int ph, int q) -> char* {
-        return p->comm ? (char*)p->peer_buf[q] + (size_t)ph * loc * eb : vbase + ((size_t)ph * P + q) * loc * eb;
+        return p->multi() ? (char*)p->peer_buf[q] + (size_t)ph * loc * eb : vbase + ((size_t)ph * P + q) * loc * eb;
     };
     auto local = [&](const void* base, int q) -> void* {  // rank q's slab of a caller buffer
-        return p->comm ? (q == p->my_rank ? const_cast<void*>(base) : nullptr)
+        return p->multi() ? (q == p->my_rank ? const_cast<void*>(base) : nullptr)
                        : (char*)const_cast<void*>(base) + (size_t)q * loc * eb;
     };
     BlockPtrs bin{}, ba{}, bb{}, bout{};
@@ -1439,7 +1466,7 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
     ++launches;
     prof_mark(p, st, "exchange 1 (transpose, peer stores)");
 #ifdef B200FFT_WITH_NCCL
-    if (p->comm) {
+    if (p->multi()) {
         if ((s = dist_barrier(p, st)) != FFT_OK) return s;
         prof_mark(p, st, "barrier");
     }
@@ -1461,7 +1488,7 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
     ++launches;
     prof_mark(p, st, "exchange 2 (transpose, peer stores)");
 #ifdef B200FFT_WITH_NCCL
-    if (p->comm) {
+    if (p->multi()) {
         if ((s = dist_barrier(p, st)) != FFT_OK) return s;
         prof_mark(p, st, "barrier");
     }
@@ -1482,7 +1509,7 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
 #ifdef B200FFT_WITH_NCCL
         // every rank's (B) FFTs ran in place in its phase-B slab: they must
         // all be complete before this rank pulls from the peers' slabs
-        if (p->comm) {
+        if (p->multi()) {
             if ((s = dist_barrier(p, st)) != FFT_OK) return s;
             prof_mark(p, st, "barrier");
         }
@@ -1510,8 +1537,8 @@ fft_status run_dist_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaS
     const int64_t N1 = p->fs1, N2 = p->fs2, S1 = N1 / P, S2 = N2 / P;
     const int64_t loc = p->n0 / P;  // elements per rank
     const size_t eb = p->elem_bytes();
-    const int nloc = p->comm ? 1 : P;
-    const int r0 = p->comm ? p->my_rank : 0;
+    const int nloc = p->multi() ? 1 : P;
+    const int r0 = p->multi() ? p->my_rank : 0;
     char* w0 = (char*)p->ws;
     char* w1 = w0 + (size_t)nloc * loc * eb;
     cudaError_t e;
@@ -1785,8 +1812,9 @@ fft_status fft_forward_paper_tree(fft_plan p, const void* in, void* out) {
     if (!in) return fail(FFT_E_INVALID_ARG, "null input");
     const int P = p->P();
     if (P < 1 || (P & (P - 1))) return fail(FFT_E_INVALID_SIZE, "the paper's schedule needs 2^l ranks");
+    if (p->multi() && !p->comm) return fail(FFT_E_UNSUPPORTED, "host collectives: no tree schedule");
     if (p->n0 % P) return fail(FFT_E_INVALID_SIZE, "n must be a multiple of the rank count");
-    const bool master = !p->comm || p->my_rank == 0;
+    const bool master = !p->multi() || p->my_rank == 0;
     if (master && !out) return fail(FFT_E_INVALID_ARG, "rank 0 needs an n-element output");
     if (!aligned(in, p->elem_bytes()) || (out && !aligned(out, p->elem_bytes())))
         return fail(FFT_E_INVALID_ARG, "data pointer not aligned to the element size");
@@ -2039,7 +2067,7 @@ fft_status fft_nccl_unique_id(unsigned char id[128]) {
 fft_status fft_plan_set_comm(fft_plan p, const unsigned char id[128], int nranks, int my_rank) {
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (nranks < 1 || my_rank < 0 || my_rank >= nranks) return fail(FFT_E_INVALID_ARG, "bad rank / nranks");
-    if (p->comm) return fail(FFT_E_STATE, "plan already has a communicator");
+    if (p->multi()) return fail(FFT_E_STATE, "plan already has a communicator");
     if (p->virt > 1) return fail(FFT_E_STATE, "plan emulates virtual ranks");
     if (p->rank == 2 && (p->n0 % nranks || p->n1 % nranks))
         return fail(FFT_E_INVALID_SIZE, "2D sides must be divisible by the rank count");
@@ -2077,11 +2105,36 @@ fft_status fft_plan_set_comm(fft_plan p, const unsigned char id[128], int nranks
 #endif
 }
 
+fft_status fft_plan_set_host_collectives(fft_plan p, int nranks, int my_rank, fft_host_allgather_fn allgather,
+                                        fft_host_barrier_fn barrier, void* ctx) {
+    if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
+    if (!allgather || !barrier) return fail(FFT_E_INVALID_ARG, "null collective callback");
+    if (nranks < 1 || my_rank < 0 || my_rank >= nranks) return fail(FFT_E_INVALID_ARG, "bad rank / nranks");
+    if (p->multi()) return fail(FFT_E_STATE, "plan already has a communicator");
+    if (p->virt > 1) return fail(FFT_E_STATE, "plan emulates virtual ranks");
+    if (p->rank == 1 && p->batch != 1) return fail(FFT_E_INVALID_ARG, "batch-sharded plans need no collectives");
+    if (p->rank == 2 && (p->n0 % nranks || p->n1 % nranks))
+        return fail(FFT_E_INVALID_SIZE, "2D sides must be divisible by the rank count");
+    if (p->rank == 1 && ((int64_t)nranks * nranks > p->n0 || p->n0 % nranks))
+        return fail(FFT_E_INVALID_SIZE, "1D four-step needs n >= nranks^2");
+    p->hc_allgather = allgather;
+    p->hc_barrier = barrier;
+    p->hc_ctx = ctx;
+    p->nranks = nranks;
+    p->my_rank = my_rank;
+    if (p->ws_owned && p->ws) {  // slab-sized workspace from now on
+        cudaFree(p->ws);
+        p->ws = nullptr;
+        p->ws_bytes = 0;
+    }
+    return FFT_OK;
+}
+
 fft_status fft_plan_set_virtual_ranks(fft_plan p, int nranks) {
     if (!p) return fail(FFT_E_INVALID_ARG, "null plan");
     if (p->rank != 2 && p->batch != 1)
         return fail(FFT_E_INVALID_ARG, "virtual ranks apply to rank-2 plans and single 1D transforms");
-    if (p->comm) return fail(FFT_E_STATE, "plan has a communicator");
+    if (p->multi()) return fail(FFT_E_STATE, "plan has a communicator");
     if (nranks < 1 || p->n0 % nranks || (p->rank == 2 && p->n1 % nranks))
         return fail(FFT_E_INVALID_SIZE, "sizes must be divisible by the rank count");
     p->virt = nranks;

@@ -419,7 +419,7 @@ def test_c5_config_single_gpu_sampled(fft):
 
 
 @pytest.mark.parametrize("batch", [1, 2, 5, 20, 27, 28, 37, 300])
-@pytest.mark.parametrize("kernel", ["ws", "st"])
+@pytest.mark.parametrize("kernel", ["ws", "st", "pair"])
 def test_c2_kernel_batches_and_inplace(fft, batch, kernel, monkeypatch):
     """The 65536-point one-HBM-pass task pipelines (fft_c2.cuh: k_ab_ws and
     k_ab_st in both stage configurations) at batch
