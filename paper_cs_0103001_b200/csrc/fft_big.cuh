@@ -64,9 +64,7 @@ __device__ __forceinline__ bool big_decode(int64_t p, int64_t G, int D, bool& is
 }
 
 // W_n^x for x < 2^30 from two fp64-generated tables: hi[x >> 15] lo[x & 32767]
-__device__ __forceinline__ float2 big_w(const float2* __restrict__ hi, const float2* __restrict__ lo, int64_t x) {
-    return cmul(__ldg(hi + (x >> 15)), __ldg(lo + (x & 32767)));
-}
+// (pass 1's B tasks; the product is formed after the FFT, the loads before)
 
 // XOR layout of pass 2's B exchange (32 lines of 128 points): element x of
 // line L at x * 32 + (L ^ 2 ((x / 16) mod 8)).  The writes (a half-warp = 2
@@ -185,14 +183,15 @@ __global__ void __launch_bounds__(320, 3)
             // line t = lo (pass 1: column n1 = 16 g + t; pass 2: a = 16 ab + t),
             // elements c = hi + 16 r of the [256 c][16] box
             const int a = PASS == 1 ? part : 16 * (part & 7) + lo;
+            // W_L^{a kc}, kc = hi + 16 m: W_L^{a hi} (W_L^{16 a})^m; pass 2 forward also the 1/n
+            // (loaded before the FFT: their latency hides behind it)
+            float2 wm = __ldg(twl + a * hi);
+            const float2 ws = __ldg(twl + 16 * a);
             float2* ln = st + lo;
 #pragma unroll
             for (int m = 0; m < 16; ++m) v[FA::pos_in(m)] = ln[FA::bpos(hi, m)];
             FA::run(v, ln, hi, tw256, -256);
             bk_arrive(empty0 + 8 * s);
-            // W_L^{a kc}, kc = hi + 16 m: W_L^{a hi} (W_L^{16 a})^m; pass 2 forward also the 1/n
-            float2 wm = __ldg(twl + a * hi);
-            const float2 ws = __ldg(twl + 16 * a);
             if (PASS == 2) wm = cscale(wm, scale);
             // pass 1: ring[kc][a][16 n1]; pass 2: ring[kc][r][128 a]
             float2* y = PASS == 1 ? slot + (int64_t)hi * 2048 + a * 16 + lo
@@ -212,17 +211,21 @@ __global__ void __launch_bounds__(320, 3)
             const int kcl = line >> 4, t = line & 15;
             const int64_t kc = 2 * part + kcl;
             if (PASS == 1) {
+                // Y[k2][n1] x W_n^{n1 k2}, k2 = kc + 256 ka, ka = lt + 8 m:
+                // W_n^{n1 (kc + 256 lt)} (W_n^{2048 n1})^m -- the four table
+                // entries loaded before the FFT (latency hidden behind it)
+                const int64_t n1 = 16 * g + t;
+                const int64_t x0 = n1 * (kc + 256 * lt), x1 = n1 * 2048;
+                const float2 h0 = __ldg(whi + (x0 >> 15)), l0 = __ldg(wlo + (x0 & 32767));
+                const float2 h1 = __ldg(whi + (x1 >> 15)), l1 = __ldg(wlo + (x1 & 32767));
                 // [2 kc][128 a][16 n1]: element a of line (kcl, n1) at kcl 2048 + a 16 + n1
                 float2* ln = st + kcl * 2048 + t;
 #pragma unroll
                 for (int m = 0; m < 16; ++m) v[FB::pos_in(m)] = ln[FB::bpos(lt, m)];
                 FB::run(v, ln, lt, tw128, -256);
                 bk_arrive(empty0 + 8 * s);
-                // Y[k2][n1] x W_n^{n1 k2}, k2 = kc + 256 ka, ka = lt + 8 m:
-                // W_n^{n1 (kc + 256 lt)} (W_n^{2048 n1})^m
-                const int64_t n1 = 16 * g + t;
-                float2 wm = big_w(whi, wlo, n1 * (kc + 256 * lt));
-                const float2 ws = big_w(whi, wlo, n1 * 2048);
+                float2 wm = cmul(h0, l0);
+                const float2 ws = cmul(h1, l1);
                 float2* o = out + (kc + 256 * lt) * L + n1;
                 if (xo & 16) {  // timing experiment (wrong order): one contiguous 32 KiB block per task
                     float2* oc = out + (g * 128 + part) * 4096 + (lt * 16) * 32 + line;

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(PairCfg::THREADS, 1)
     k_ab_pair(const __grid_constant__ CUtensorMap map_x, float2* __restrict__ out, int64_t batch, float scale,
               const float2* __restrict__ tw4, const float2* __restrict__ tw256, int xo) {
     // xo: timing-experiment bits (wrong results; B200FFT_PAIR_XO with
-    // B200FFT_ALLOW_WRONG=1): 1 no DSMEM stores, 2 no X stores, 4 no TMA
+    // B200FFT_ALLOW_WRONG=1): 2 no X stores, 4 no TMA
     // loads, 8 no FFT arithmetic, 16 no TMEM traffic, 64 no in-stage exchanges
     using G = PairCfg;
     constexpr int NSA = G::NSA, NB = G::NB;
@@ -242,9 +242,9 @@ __global__ void __launch_bounds__(PairCfg::THREADS, 1)
                     for (int i = 0; i < 4; ++i) {
                         const int idx = hi * 256 + 16 * (8 * (int)c + g + 2 * i) + lo;  // [row hi][n1]
                         gbuf[s * 4096 + idx] = vo[i];
-                        if (!(xo & 1)) pr_st_async(rbuf + 8 * idx, vp[i], rbar);
+                        pr_st_async(rbuf + 8 * idx, vp[i], rbar);
                     }
-                    if (tid == 0 && !(xo & 1)) bk_arrive_expect(gfull0 + 8 * s, 16384u);
+                    if (tid == 0) bk_arrive_expect(gfull0 + 8 * s, 16384u);
                     else bk_arrive(gfull0 + 8 * s);
                 }
                 const int j = jj + g;
