@@ -469,7 +469,7 @@ def test_c2_two_plans_two_streams(fft):
     p2.destroy()
 
 
-@pytest.mark.parametrize("bits", [16, 32, 128, 256, 512, 1024, 4096])
+@pytest.mark.parametrize("bits", [16, 32, 128, 256, 512, 1024, 4096, 16384])
 def test_c2_tuning_variants(fft, bits, monkeypatch):
     """k_ab_st's tuning bits that keep the results (kernels_c2.cu ab_opts:
     static / paired task positions, X store and A load cache policies, the
