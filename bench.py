@@ -434,6 +434,18 @@ def bench_c2(args, ws, rank, local):
 
 
 # ---------------------------------------------------------- extra configs
+def graph_of(stream, fn):
+    """fn() (library calls on `stream`) captured once into a CUDA graph."""
+    import torch
+
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    torch.cuda.synchronize()
+    return g
+
+
 def bench_c1(args, local):
     """C1 (BASELINE configs[0]): N = 1024 complex128 forward + inverse;
     latency-bound (32 KiB), reported in microseconds."""
@@ -454,14 +466,23 @@ def bench_c1(args, local):
 
     for _ in range(5):
         step()
+    # the same two library calls captured once into a CUDA graph (the plan
+    # launches on its own stream, which is the capture stream): replays pay
+    # one graph launch instead of two kernel launches
+    graph = graph_of(stream, step)
     with ClockSampler(local) as clk:
         ts = timed(stream, step, 400)
+        gts = timed(stream, graph.replay, 400)
+    zd.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
     err = float(torch.linalg.vector_norm(zd - xd) / torch.linalg.vector_norm(xd))
     plan.destroy()
     return {"workload": "C1: BASELINE configs[0], N=1024 complex128 forward+inverse (latency, warm L2)",
             "us_median": round(statistics.median(ts) * 1e3, 2), "us_min": round(min(ts) * 1e3, 2),
+            "graph_us_median": round(statistics.median(gts) * 1e3, 2), "graph_us_min": round(min(gts) * 1e3, 2),
             "roofline": {"bound": "latency", "note": "32 KiB per transform: launch latency, not bandwidth"},
-            "launches": 2, "roundtrip_rel_l2": err, "clocks": clk.summary()}
+            "launches": 2, "roundtrip_rel_l2": err, "roundtrip_from": "graph replay", "clocks": clk.summary()}
 
 
 def bench_c3(args, local, real_out=False):
@@ -526,13 +547,22 @@ def bench_next1(args, local):
 
     for _ in range(3):
         step()
+    torch.cuda.synchronize()
+    ref = out.clone()
+    graph = graph_of(stream, step)
     with ClockSampler(local) as clk:
         ts = timed(stream, step, 200, flush)
+        gts = timed(stream, graph.replay, 200, flush)
+    out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    graph_same = bool(torch.equal(out, ref))
     med = statistics.median(ts)
     n = 512 * 512
     plan.destroy()
     return {"workload": "NEXT-1: 506x460 uint8 image -> pad 512^2 -> FFT2 -> Eq. filtro b=340 -> IFFT2 -> uint8 "
                         "(+ spectrum), cold L2", "us_median": round(med * 1e3, 2), "us_min": round(min(ts) * 1e3, 2),
+            "graph_us_median": round(statistics.median(gts) * 1e3, 2), "graph_output_identical": graph_same,
             "GFLOP/s": round(2 * 5 * n * math.log2(n) / (med / 1e3) / 1e9, 1), "launches": 3,
             "roofline": {"bound": "latency", "note": "2 MiB complex grid: three launches of ~10 us"},
             "clocks": clk.summary()}

@@ -199,8 +199,7 @@ cudaError_t rows_filter_trans_r(int64_t R, const void* in, void* out, int64_t ba
 // profiles/README.md)
 template <int R, int PAIR2>
 cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const void* filt1, double scale2,
-                    const void* filt2, const void* tw, unsigned long long* gbar, unsigned long long* gen,
-                    cudaStream_t st) {
+                    const void* filt2, const void* tw, unsigned long long* gbar, cudaStream_t st) {
     constexpr int E = 16, STAGES = 3, MLX = 0;
     constexpr int W = (int)((64 * 1024) / (R * sizeof(float2)));
     using G = RowsTmaCfg<float, R, W, false, STAGES>;
@@ -212,10 +211,6 @@ cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const v
     const int64_t lines = R / 2;  // row pairs per pass
     const int64_t tiles = (lines + W - 1) / W;
     const int grid = (int)(tiles < grid_max ? tiles : grid_max);
-    // the counter grows by `grid` per completed launch: this launch's target;
-    // *gen advances only when the launch was accepted (a rejected launch
-    // must not leave later targets beyond what the counter can reach)
-    const unsigned long long target = (*gen + 1) * (unsigned long long)grid;
     static const int xo = [] {
         const char* w = getenv("B200FFT_ALLOW_WRONG");
         const char* v = getenv("B200FFT_ROWS_XO");
@@ -229,9 +224,8 @@ cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const v
     float a_s1 = (float)scale1, a_s2 = (float)scale2;
     const float* a_f1 = reinterpret_cast<const float*>(filt1);
     const float* a_f2 = reinterpret_cast<const float*>(filt2);
-    unsigned long long a_target = target;
     int a_xo = xo;
-    void* args[] = {&a_in, &a_mid, &a_out, &a_lines, &a_tw, &a_s1, &a_f1, &a_s2, &a_f2, &gbar, &a_target, &a_xo};
+    void* args[] = {&a_in, &a_mid, &a_out, &a_lines, &a_tw, &a_s1, &a_f1, &a_s2, &a_f2, &gbar, &a_xo};
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
@@ -242,9 +236,7 @@ cudaError_t rows2_t(const void* in, void* mid, void* out, double scale1, const v
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelExC(&cfg, (const void*)kern, args);
-    if (e == cudaSuccess) ++*gen;
-    return e;
+    return cudaLaunchKernelExC(&cfg, (const void*)kern, args);
 }
 
 }  // namespace
@@ -256,11 +248,11 @@ bool rows_filter2_supported(int prec, int64_t N, int64_t M) {
 
 cudaError_t launch_rows_filter2(int64_t R, const void* in, void* mid, void* out, double scale1, const void* filt1,
                                 double scale2, const void* filt2, const void* tw, int pair2, unsigned long long* gbar,
-                                unsigned long long* gen, cudaStream_t st) {
+                                cudaStream_t st) {
     if (pair2 != 2) return cudaErrorInvalidValue;  // complex output only (the C3 form)
     switch (R) {
 #define B200_R2_CASE(r) \
-    case r: return rows2_t<r, 2>(in, mid, out, scale1, filt1, scale2, filt2, tw, gbar, gen, st);
+    case r: return rows2_t<r, 2>(in, mid, out, scale1, filt1, scale2, filt2, tw, gbar, st);
         B200_R2_CASE(512) B200_R2_CASE(1024) B200_R2_CASE(2048)
 #undef B200_R2_CASE
         default: return cudaErrorInvalidValue;

@@ -91,7 +91,7 @@ cudaError_t launch_rows_filter_transposed(bool real_in, int64_t R, const void* i
 bool rows_filter2_supported(int prec, int64_t N, int64_t M);
 cudaError_t launch_rows_filter2(int64_t R, const void* in, void* mid, void* out, double scale1, const void* filt1,
                                 double scale2, const void* filt2, const void* tw, int pair2, unsigned long long* gbar,
-                                unsigned long long* gen, cudaStream_t st);
+                                cudaStream_t st);
 
 // Kernel family B: column transforms of nimg grids [R][S]; mode 0 fwd, 1 inv,
 // 2 fwd -> filter*scale -> inv.

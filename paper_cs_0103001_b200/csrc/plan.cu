@@ -195,10 +195,10 @@ struct fft_plan_s {
     void* big_twl = nullptr;
     void* big_hi = nullptr;
     void* big_lo = nullptr;
-    // grid-barrier counter of the fused two-pass pipeline (k_rows_tma2): it
-    // only grows; gbar_gen = launches so far (plan-owned, zeroed once)
+    // grid-barrier state of the fused two-pass pipeline (k_rows_tma2): the
+    // arrival count and the generation (plan-owned, zeroed once; the barrier
+    // resets the count itself, so graph replays need no host-side state)
     unsigned long long* gbar = nullptr;
-    unsigned long long gbar_gen = 0;
     // k_colfilt's task counters (plan-owned, grown on demand)
     void* cws = nullptr;
     size_t cws_bytes = 0;
@@ -624,12 +624,11 @@ cudaError_t colfilt(fft_plan_s* p, void* grid, int64_t SM, int64_t nimg, double 
     return launch_colfilt(grid, SM, nimg, scale, p->tw, p->twl, p->gu, gv, col_off, p->cws, p->cws_bytes, st);
 }
 
-// the fused pipeline's grid-barrier counter (zeroed once; it only grows)
+// the fused pipeline's grid-barrier state (zeroed once; self-resetting)
 cudaError_t ensure_gbar(fft_plan_s* p, cudaStream_t st) {
     if (p->gbar) return cudaSuccess;
     cudaError_t e = cudaMalloc(&p->gbar, 256);
     if (e == cudaSuccess) e = cudaMemsetAsync(p->gbar, 0, 256, st);
-    p->gbar_gen = 0;
     return e;
 }
 
@@ -700,8 +699,7 @@ fft_status run_pipeline(fft_plan_s* p, const void* in, void* out, fft_filter fil
             if ((e = ensure_gbar(p, st)) != cudaSuccess) return cuda_fail(e, "grid barrier counter");
             for (int64_t g = 0; g < p->batch; ++g) {
                 e = launch_rows_filter2(M, (const char*)in + g * in_grid, p->ws, (char*)out + g * grid,
-                                        1.0 / (double)M, p->gv, 1.0 / (double)N, p->gu, p->tw, 2, p->gbar,
-                                        &p->gbar_gen, st);
+                                        1.0 / (double)M, p->gv, 1.0 / (double)N, p->gu, p->tw, 2, p->gbar, st);
                 if (e != cudaSuccess) return cuda_fail(e, "k_rows_tma2 (real pairs, complex out) launch");
             }
             p->last_launches = (int)p->batch;
