@@ -198,10 +198,18 @@ def torchrun(n, argv, timeout=None):
     return subprocess.CompletedProcess(cmd, proc.returncode, out, err)
 
 
+# Dry run of the N > 1 code paths on ONE GPU (B200FFT_BENCH_SHARE_GPU=1):
+# every rank on cuda:0, gloo instead of NCCL, and the sharded configs'
+# collectives by host callbacks (fft_plan_set_host_collectives).  Checks the
+# orchestration only -- ranks share one GPU, so its times mean nothing and
+# its lines say so ("dry_run").
+SHARE_GPU = os.environ.get("B200FFT_BENCH_SHARE_GPU") == "1"
+
+
 def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SHARE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch
         import torch.distributed as dist
@@ -209,7 +217,7 @@ def dist_init():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group("nccl" if torch.cuda.is_available() and not SHARE_GPU else "gloo")
     return ws, rank, local
 
 
@@ -233,7 +241,7 @@ def allreduce(ws, v: float, op="max") -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() and not SHARE_GPU else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -708,7 +716,14 @@ def bench_sharded_cfg(args, ws, rank, local, cfg):
         n_exch = 6
         workload = (f"C5: N=2^30 complex64 forward(1/N)+inverse, four-step 32768 x 32768 over {ws} ranks, "
                     "3 exchanges per direction (natural order)")
-    if ws > 1:
+    if ws > 1 and SHARE_GPU:
+        def allgather(mine):
+            parts = [None] * ws
+            dist.all_gather_object(parts, mine)
+            return parts
+
+        plan.set_host_collectives(ws, rank, allgather, dist.barrier)
+    elif ws > 1:
         uid = [b.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         plan.set_comm(uid[0], ws, rank)
@@ -779,6 +794,9 @@ def bench_sharded_cfg(args, ws, rank, local, cfg):
                            "step_GBps": round(nvl / (ms / 1e3) / 1e9, 1),
                            "note": "exchange_ms = device time of the phases that move data between GPUs "
                                    "(peer stores / loads fused into the row or transpose kernels)"}
+    if ws > 1 and SHARE_GPU:
+        res["dry_run"] = "ranks shared one GPU (B200FFT_BENCH_SHARE_GPU): times are not measurements"
+    elif ws > 1:
         # NCCL all-to-all of one exchange's bytes (reference)
         t = torch.empty(2 * loc, dtype=torch.float32, device=dev)
         o = torch.empty_like(t)
@@ -978,6 +996,8 @@ def main():
                                 "C5": _extra("C5", bench_c5_single, args, local)}
             else:
                 res["extra"] = {"sharded": sharded_extras(args, ws)}
+        if SHARE_GPU and ws > 1:
+            res["dry_run"] = "ranks shared one GPU (B200FFT_BENCH_SHARE_GPU): times are not measurements"
         print(json.dumps(res), flush=True)
 
 
