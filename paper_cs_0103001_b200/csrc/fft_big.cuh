@@ -66,13 +66,9 @@ __device__ __forceinline__ bool big_decode(int64_t p, int64_t G, int D, bool& is
 // W_n^x for x < 2^30 from two fp64-generated tables: hi[x >> 15] lo[x & 32767]
 // (pass 1's B tasks; the product is formed after the FFT, the loads before)
 
-// XOR layout of pass 2's B exchange (32 lines of 128 points): element x of
-// line L at x * 32 + (L ^ 2 ((x / 16) mod 8)).  The writes (a half-warp = 2
-// lines x 8 lanes j, element 16 j + q) hit 16 distinct 8-B bank pairs (l ^ 2 j
-// for l < 2, j < 8), the line-fastest reads (x fixed) a permutation of each
-// half's 16 lines.  (The earlier L ^ 4 ((x / 16) mod 4) repeated every 4 j:
-// 2-way conflicts on every write -- ncu: 209 M excess wavefronts per pass.)
-__device__ __forceinline__ int big_bx(int x, int line) { return x * 32 + (line ^ (((x >> 4) & 7) << 1)); }
+// pass 2's B exchange uses big_bx (fft_c2.cuh): element x of line L at
+// x * 32 + (L ^ 2 ((x / 16) mod 8)) -- the line XOR 4 ((x / 16) mod 4) had
+// 2-way conflicts on every write (ncu: 209 M excess wavefronts per pass).
 
 template <bool INV, int PASS>
 __global__ void __launch_bounds__(320, 3)

@@ -101,25 +101,32 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 }  // namespace tmaops
 
-// position i of the global task order -> (is B, transform b, part p)
+// position i of the global task order -> (is B, transform b, part p), T A
+// tasks and T B tasks per transform (T = 16 for N = 65536, 8 for 32768)
+template <int T = 16>
 __device__ __forceinline__ void ab_decode(int64_t i, int64_t batch, int64_t Dp, bool& isb, int64_t& b, int& part) {
-    const int64_t n1t = 16 * Dp, n2t = 32 * (batch - Dp);
+    const int64_t n1t = T * Dp, n2t = 2 * T * (batch - Dp);
     if (i < n1t) {
         isb = false;
-        b = i / 16;
-        part = (int)(i % 16);
+        b = i / T;
+        part = (int)(i % T);
     } else if (i < n1t + n2t) {
-        const int64_t j = i - n1t, r = j % 32;
-        isb = r >= 16;
-        b = Dp + j / 32 - (isb ? Dp : 0);
-        part = (int)(r % 16);
+        const int64_t j = i - n1t, r = j % (2 * T);
+        isb = r >= T;
+        b = Dp + j / (2 * T) - (isb ? Dp : 0);
+        part = (int)(r % T);
     } else {
         const int64_t j = i - n1t - n2t;
         isb = true;
-        b = batch - Dp + j / 16;
-        part = (int)(j % 16);
+        b = batch - Dp + j / T;
+        part = (int)(j % T);
     }
 }
+
+// XOR layout of a 32-line x 128-point exchange (element x of line L at
+// x * 32 + (L ^ 2 ((x / 16) mod 8))): conflict-free for the 8-lanes-per-line
+// writes and the line-fastest reads (k_big pass 2, st_task_b128)
+__device__ __forceinline__ int big_bx(int x, int line) { return x * 32 + (line ^ (((x >> 4) & 7) << 1)); }
 
 // ---------------------------------------------------------------------------
 // k_ab_ws: warp-specialised TMA form.  8 compute warps + 1 producer warp per
@@ -362,15 +369,15 @@ __device__ __forceinline__ void st_pol(float2* p, float2 v, uint64_t pol) {
                  : "memory");
 }
 
-template <bool INV>
+template <bool INV, int N1 = 256>
 __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, uint32_t empty, int part, float2* y0,
                                           float scale, const float2* __restrict__ tw4,
                                           const float2* __restrict__ tw256, int xo) {
     // the four-step twiddle's two table entries, loaded before the FFT so
     // their latency hides behind it (after the exchange: 1.3% slower, round 2)
     const int n1 = part * 16 + lo;
-    const float2 wm0 = __ldg(tw4 + (int64_t)hi * 256 + n1);
-    const float2 ws = __ldg(tw4 + (int64_t)16 * 256 + n1);
+    const float2 wm0 = __ldg(tw4 + (int64_t)hi * N1 + n1);
+    const float2 ws = __ldg(tw4 + (int64_t)16 * N1 + n1);
     float2 v[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = st[(hi + 16 * r) * 16 + lo];
@@ -391,7 +398,7 @@ __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, u
     }
     // Y[k2][n1] = v[q] * W_N^{n1 k2} * scale, k2 = hi + 16 q
     float2 wm = cscale(wm0, scale);
-    float2* y = y0 + (int64_t)hi * 256 + n1;
+    float2* y = y0 + (int64_t)hi * N1 + n1;
     const uint64_t keep = tmaops::policy_evict_last();
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
@@ -399,8 +406,8 @@ __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, u
         // access-policy window): evict-last stores measured 1.3% slower
         // (xo 16384 selects them, for comparisons)
         if (xo & 16384) {
-            if (!(xo & 2) || v[q].x == 1.2345e-38f) st_pol(y + q * 16 * 256, cmul_dir<INV>(v[q], wm), keep);
-        } else if (!(xo & 2) || v[q].x == 1.2345e-38f) y[q * 16 * 256] = cmul_dir<INV>(v[q], wm);
+            if (!(xo & 2) || v[q].x == 1.2345e-38f) st_pol(y + q * 16 * N1, cmul_dir<INV>(v[q], wm), keep);
+        } else if (!(xo & 2) || v[q].x == 1.2345e-38f) y[q * 16 * N1] = cmul_dir<INV>(v[q], wm);
         if (q < 15) wm = cmul(wm, ws);
     }
 }
@@ -448,12 +455,54 @@ __device__ __forceinline__ void st_task_b(float2* st, int lo, int hi, int bar, u
     }
 }
 
-template <bool INV, int NS, int MINB>
+// B task body for N = 32768 (N1 = 128): the stage holds 32 Y rows k2 =
+// 32 p + line of 128 points (as landed); 128-point DFTs over n1 = j + 8 r:
+// step 0 radix 16 over r (8 lanes j per line), the XOR-layout exchange,
+// step 1 radix 8 over j with W_128^{q j} (q = lt + 8 b, line-fastest):
+// X[k2 + 256 k1], k1 = q + 16 m -- a warp stores 32 consecutive k2 (256 B).
+template <bool INV>
+__device__ __forceinline__ void st_task_b128(float2* st, int tid, int bar, uint32_t empty, float2* x0) {
+    const int L0 = tid >> 3, j = tid & 7;
+    float2 v[16];
+    const float2* src = st + L0 * 128;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = src[j + 8 * r];
+    dft<16, INV>(v);
+    grp_sync(bar);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) st[big_bx(16 * j + q, L0)] = v[q];
+    grp_sync(bar);
+    const int line = tid & 31, lt = tid >> 5;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+        const int q = lt + 8 * b;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[b * 8 + r] = st[big_bx(q + 16 * r, line)];
+    }
+    bk_arrive(empty);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+        const int q = lt + 8 * b;
+#pragma unroll
+        for (int r = 1; r < 8; ++r) v[b * 8 + r] = cmul_dir<INV>(v[b * 8 + r], c_w256[(2 * q * r) & 255]);
+        dft<8, INV>(v + b * 8);
+    }
+    float2* x = x0 + line;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) x[(int64_t)256 * (lt + 8 * b + 16 * m)] = v[b * 8 + m];
+}
+
+// L = 65536 (C2: N1 = N2 = 256, 16 A + 16 B tasks per transform) or 32768
+// (N1 = 128, N2 = 256: 8 A tasks of 16 columns, 8 B tasks of 32 Y rows)
+template <bool INV, int NS, int MINB, int L = 65536>
 __global__ void __launch_bounds__(320, MINB)
     k_ab_st(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yld,
             float2* __restrict__ ring, float2* __restrict__ out, int64_t batch, float scale,
             const float2* __restrict__ tw4, const float2* __restrict__ tw256, AbCtl ctl, int opts) {
     using G = AbStCfg<NS>;
+    constexpr int N1 = L / 256, T = N1 / 16, ROWS = 4096 / N1;  // B task: ROWS Y rows of N1
     constexpr int NSIG = G::NSIG;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(smem_raw);
@@ -463,7 +512,7 @@ __global__ void __launch_bounds__(320, MINB)
     volatile int* sigdone = reinterpret_cast<volatile int*>(sigb + NSIG);
     const int tid = threadIdx.x;
     const int64_t Dp = batch < ctl.D ? batch : ctl.D;
-    const int64_t ntasks = 32 * batch;
+    const int64_t ntasks = 2 * T * batch;
 
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -508,7 +557,7 @@ __global__ void __launch_bounds__(320, MINB)
                 bool isb;
                 int64_t b;
                 int part;
-                ab_decode(i, batch, Dp, isb, b, part);
+                ab_decode<T>(i, batch, Dp, isb, b, part);
                 if (opts & 1) {  // timing experiment: no loads, no dependency waits
                     if (!isb) {
                         while (*sigdone < na - NSIG + 1) __nanosleep(20);
@@ -522,15 +571,15 @@ __global__ void __launch_bounds__(320, MINB)
                     ++na;
                     // the ring slot's previous transform: all its B parts have read it
                     if (b >= ctl.ring && !(opts & 4))
-                        while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < 16) __nanosleep(32);
+                        while (bk_ld_acquire(ctl.done_b + (b - ctl.ring)) < T) __nanosleep(32);
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
                     tmaops::load3(st, &map_x, part * 16, 0, (int)b, bar, pol_stream);
                 } else {
                     if (!(opts & 4))
-                        while (bk_ld_acquire(ctl.done_a + b) < 16) __nanosleep(32);
+                        while (bk_ld_acquire(ctl.done_a + b) < T) __nanosleep(32);
                     asm volatile("fence.proxy.async.global;\n" ::: "memory");
                     bk_arrive_expect(bar, (uint32_t)G::STAGE);
-                    tmaops::load3(st, &map_yld, 0, part * 16, (int)(b % ctl.ring), bar, (opts & 32768) ? pol_stream : pol_keep);
+                    tmaops::load3(st, &map_yld, 0, part * ROWS, (int)(b % ctl.ring), bar, pol_keep);
                 }
             }
         } else {  // ---- signaller ----
@@ -560,9 +609,10 @@ __global__ void __launch_bounds__(320, MINB)
         bool isb;
         int64_t b;
         int part;
-        ab_decode(i, batch, Dp, isb, b, part);
+        ab_decode<T>(i, batch, Dp, isb, b, part);
         if (!isb) {
-            st_task_a<INV>(st, lo, hi, 1, empty0 + 8 * s, part, ring + (b % ctl.ring) * 65536, scale, tw4, tw256, opts);
+            st_task_a<INV, N1>(st, lo, hi, 1, empty0 + 8 * s, part, ring + (b % ctl.ring) * L, scale, tw4, tw256,
+                                  opts);
             if (tid == 0) sigb[ja % NSIG] = b;
             bk_arrive(sig0 + 8 * (ja % NSIG));  // release: this thread's Y stores
             ++ja;
@@ -570,7 +620,10 @@ __global__ void __launch_bounds__(320, MINB)
             // the stage's Y rows landed (the TMA read is complete): the ring
             // slot's rows are free for the next transform
             if (tid == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;\n" ::"l"(ctl.done_b + b) : "memory");
-            st_task_b<INV>(st, lo, hi, 1, empty0 + 8 * s, out + b * 65536 + part * 16, tw256, opts);
+            if constexpr (L == 65536)
+                st_task_b<INV>(st, lo, hi, 1, empty0 + 8 * s, out + b * 65536 + part * 16, tw256, opts);
+            else
+                st_task_b128<INV>(st, tid, 1, empty0 + 8 * s, out + b * L + part * ROWS);
         }
     }
     // done: tell the signaller (once its slot is free)

@@ -52,7 +52,8 @@ int c2_kind() {
     if (v && !strcmp(v, "ws")) return (int)C2_WS;
     return (int)C2_ST;
 }
-const void* c2_kernel(int kind, bool inv) {
+const void* c2_kernel(int kind, bool inv, int64_t n = 65536) {
+    if (n == 32768) return inv ? (const void*)k_ab_st<true, 2, 3, 32768> : (const void*)k_ab_st<false, 2, 3, 32768>;
     if (kind == C2_ST) return inv ? (const void*)k_ab_st<true, 2, 3> : (const void*)k_ab_st<false, 2, 3>;
     return inv ? (const void*)k_ab_ws<true> : (const void*)k_ab_ws<false>;
 }
@@ -135,10 +136,13 @@ namespace {
 
 void ab_persist_limit(int dev, size_t ring_bytes) { l2_persist_request(dev, ring_bytes); }
 
-// caller-provided scratch: the Y ring (ring x 512 KiB), then the counters
-size_t ab_ws_bytes(int64_t ring, int64_t batch) {
-    return (size_t)ring * 65536 * sizeof(float2) + (size_t)2 * batch * sizeof(int) + 16;
+// caller-provided scratch: the Y ring (ring x L x 8 B), then the counters
+size_t ab_ws_bytes(int64_t ring, int64_t batch, int64_t n = 65536) {
+    return (size_t)ring * n * sizeof(float2) + (size_t)2 * batch * sizeof(int) + 16;
 }
+// the N = 32768 form has half the tasks per transform and half-size slots:
+// twice the dependency distance and ring slots for the same positions / bytes
+int64_t ab_scale(int64_t n) { return n == 32768 ? 2 : 1; }
 
 // Grid of one launch.  A CTA's A task at local index k is signalled
 // (done_a) only once its producer has issued its loads up to local index
@@ -179,7 +183,7 @@ int ab_opts(int kind) {
     return (w && w[0] == '1' && x) ? atoi(x) : 0;
 }
 
-template <bool INV>
+template <bool INV, int64_t L = 65536>
 cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
                       void* ws, size_t ws_bytes, cudaStream_t st) {
     int dev = 0;
@@ -189,16 +193,19 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     e = ab_geom(dev, &g);
     if (e != cudaSuccess) return e;
     if (batch <= 0) return cudaSuccess;
-    if (!ws || ws_bytes < ab_ws_bytes(g.ring, batch)) return cudaErrorInvalidValue;
+    constexpr int64_t N1 = L / 256;  // columns of the [256][N1] view (n = n1 + N1 n2)
+    const int64_t D = g.D * ab_scale(L), R = g.ring * ab_scale(L);
+    if (!ws || ws_bytes < ab_ws_bytes(R, batch, L)) return cudaErrorInvalidValue;
     if ((e = w256_upload()) != cudaSuccess) return e;
     void* ring = ws;
-    const size_t rb = (size_t)g.ring * 65536 * sizeof(float2);
+    const size_t rb = (size_t)R * L * sizeof(float2);
     int* ctl = reinterpret_cast<int*>((char*)ws + rb);
-    const int kind = c2_kind();
+    const int kind = L == 65536 ? c2_kind() : (int)C2_ST;
     CUtensorMap m_x, m_out, m_yst, m_yld;
-    if (!encode3(&m_x, const_cast<void*>(in), 256, 256, (uint64_t)batch, 16, 256, 0) ||
+    if (!encode3(&m_x, const_cast<void*>(in), N1, 256, (uint64_t)batch, 16, 256, 0) ||
         !encode3(&m_out, out, 256, 256, (uint64_t)batch, 16, 256, 128) ||
-        !encode3(&m_yst, ring, 256, 256, g.ring, 16, 256, 0) || !encode3(&m_yld, ring, 256, 256, g.ring, 256, 16, 0))
+        !encode3(&m_yst, ring, 256, 256, R, 16, 256, 0) ||
+        !encode3(&m_yld, ring, N1, 256, R, (uint32_t)N1, (uint32_t)(4096 / N1), 0))
         return cudaErrorInvalidValue;
     // counters: done_a[batch], done_b[batch], then the 8-B task counter
     // (8-B aligned: 2 batch ints after the 512 KiB-aligned ring, padded)
@@ -206,7 +213,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
         reinterpret_cast<unsigned long long*>((char*)ctl + ((sizeof(int) * 2 * batch + 7) & ~(size_t)7));
     e = cudaMemsetAsync(ctl, 0, ((sizeof(int) * 2 * batch + 7) & ~(size_t)7) + 8, st);
     if (e != cudaSuccess) return e;
-    AbCtl c{ctl, ctl + batch, next, g.D, g.ring};
+    AbCtl c{ctl, ctl + batch, next, (int)D, (int)R};
     float a_scale = (float)scale;
     const float2* a_tw4 = reinterpret_cast<const float2*>(tw4);
     const float2* a_tw = reinterpret_cast<const float2*>(tw) + tw_base(256);
@@ -216,14 +223,23 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     float2* a_out = reinterpret_cast<float2*>(out);
     void* args_ws[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
     void* args_st[] = {&m_x, &m_yld, &a_ring, &a_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
-    const int grid = g.grid[kind][INV ? 1 : 0];
+    int grid = g.grid[kind][INV ? 1 : 0];
+    if (L != 65536) {  // the 32768-point instantiation: its own occupancy (same resources)
+        const void* k = c2_kernel(C2_ST, INV, L);
+        int occ = 0, sms = 0;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2_smem(C2_ST));
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c2_threads(C2_ST), c2_smem(C2_ST));
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        grid = sms * (occ > 0 ? occ : 1);
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     // k_ab_st signals an A task as soon as its own stores are done (no
     // signal waits for a later load): no small-batch grid cap
-    const int64_t tasks = 32 * batch;
+    const int64_t tasks = 2 * (N1 / 16) * batch;
     cfg.gridDim = dim3((unsigned)(kind == C2_WS ? ab_launch_grid(grid, batch, g.D, AbWsCfg::NS)
                                                 : (tasks < grid ? tasks : grid)),
                        1, 1);
@@ -250,7 +266,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
         attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.numAttrs = 2;
     }
-    return cudaLaunchKernelExC(&cfg, c2_kernel(kind, INV), kind == C2_WS ? args_ws : args_st);
+    return cudaLaunchKernelExC(&cfg, c2_kernel(kind, INV, L), kind == C2_WS ? args_ws : args_st);
 }
 
 // k_ab_pair (fft_c2pair.cuh): one 2-CTA cluster per transform, Y in TMEM;
@@ -319,8 +335,10 @@ bool c2_pair_selected() {
 }  // namespace
 
 bool c2_supported(int prec, int64_t n, int* n1, int* n2) {
-    if (prec != 0 || n != 65536) return false;
-    *n1 = 256;
+    if (prec != 0 || (n != 65536 && n != 32768)) return false;
+    const char* v = getenv("B200FFT_NO_AB32K");  // "1": 32768-point rows by the Stockham passes instead
+    if (n == 32768 && v && v[0] == '1') return false;
+    *n1 = (int)(n / 256);
     *n2 = 256;
     return true;
 }
@@ -347,16 +365,19 @@ void c2_plan_release(int dev) {
     c.limit = 0;
 }
 
-size_t c2_workspace_bytes(int64_t batch) {
+size_t c2_workspace_bytes(int64_t batch, int64_t n) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
     AbGeom g;
     if (ab_geom(dev, &g) != cudaSuccess) return 0;
-    return ab_ws_bytes(g.ring, batch);
+    return ab_ws_bytes(g.ring * ab_scale(n), batch, n);
 }
 
-cudaError_t launch_c2(bool inv, const void* in, void* out, int64_t batch, double scale, const void* tw4,
+cudaError_t launch_c2(bool inv, int64_t n, const void* in, void* out, int64_t batch, double scale, const void* tw4,
                       const void* tw, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (n == 32768)
+        return inv ? ab_launch<true, 32768>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st)
+                   : ab_launch<false, 32768>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
     if (c2_pair_selected())
         return inv ? pair_launch<true>(in, out, batch, scale, tw4, tw, st)
                    : pair_launch<false>(in, out, batch, scale, tw4, tw, st);

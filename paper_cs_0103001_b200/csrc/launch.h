@@ -178,12 +178,12 @@ cudaError_t launch_big(bool inv, const void* in, void* mid, void* out, double sc
 // occupancy at `threads` threads and `smem` bytes).  (kernels_misc.cu)
 cudaError_t kernel_setup(const void* kern, int threads, size_t smem, int* grid_max);
 
-// One-pass 65536-point complex64 transform (fft_c2.cuh, C2): n = 256 * 256
-// four-step through an L2-resident ring.  tw4: W_n^{n1 k2} laid out
-// [k2][n1]; caller-provided scratch of c2_workspace_bytes (the ring and the
-// task counters).
+// One-pass 65536- and 32768-point complex64 transforms (fft_c2.cuh, C2):
+// n = N1 * 256 (N1 = 256, 128) four-step through an L2-resident ring.  tw4:
+// W_n^{n1 k2} laid out [k2][n1]; caller-provided scratch of
+// c2_workspace_bytes (the ring and the task counters).
 bool c2_supported(int prec, int64_t n, int* n1, int* n2);
-size_t c2_workspace_bytes(int64_t batch);
+size_t c2_workspace_bytes(int64_t batch, int64_t n);
 // plan lifetime bookkeeping: the device's persisting-L2 set-aside for the
 // ring is released with its last 65536-point plan
 void c2_plan_acquire(int dev);
@@ -191,7 +191,7 @@ void c2_plan_release(int dev);
 // the device's persisting-L2 set-aside for an L2 ring of ring_bytes (the
 // largest requested; released with the last acquiring plan)
 void l2_persist_request(int dev, size_t ring_bytes);
-cudaError_t launch_c2(bool inv, const void* in, void* out, int64_t batch, double scale, const void* tw4,
+cudaError_t launch_c2(bool inv, int64_t n, const void* in, void* out, int64_t batch, double scale, const void* tw4,
                       const void* tw, void* ws, size_t ws_bytes, cudaStream_t st);
 
 // the constant step-twiddle tables of the task-pipeline modules (one copy per

@@ -264,7 +264,7 @@ size_t workspace_need(const fft_plan_s* p) {
     if (p->dist()) return 2 * (size_t)p->elems() * p->elem_bytes();  // send + recv slabs
     if (p->rank == 2)  // the transposed grid of the Gaussian pipeline (allocated on first use)
         return (size_t)p->n0 * p->n1 * p->elem_bytes();
-    if (p->rank == 1 && p->tw4) return c2_workspace_bytes(p->batch);
+    if (p->rank == 1 && p->tw4) return c2_workspace_bytes(p->batch, p->n0);
     if (p->rank == 1 && !p->radices.empty()) {
         size_t one = (size_t)p->elems() * p->elem_bytes();
         if (big_supported(p->prec, p->n0) && p->batch == 1 && !p->dist())
@@ -346,7 +346,7 @@ fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream
         // it writes it, so out == in is safe
         fft_status s = ensure_workspace(p);  // the Y ring and the task counters
         if (s != FFT_OK) return s;
-        e = launch_c2(inv, in, out, p->batch, scale, p->tw4, p->tw, p->ws, p->ws_bytes, st);
+        e = launch_c2(inv, p->n0, in, out, p->batch, scale, p->tw4, p->tw, p->ws, p->ws_bytes, st);
         p->last_launches = 1;
         if (e != cudaSuccess) return cuda_fail(e, "k_ab_ws launch");
         return FFT_OK;

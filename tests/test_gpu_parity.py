@@ -447,6 +447,30 @@ def test_c2_kernel_batches_and_inplace(fft, batch, kernel, monkeypatch):
     p.destroy()
 
 
+@pytest.mark.parametrize("batch", [1, 2, 5, 17, 56, 300])
+def test_ab_32768_batches_and_inplace(fft, batch):
+    """32768-point rows through the same one-pass task pipeline (k_ab_st<L =
+    32768>: n = n1 + 128 n2, 8 A tasks of 16 columns, 8 B tasks of 32 Y rows
+    with 128-point DFTs), forward and in-place inverse against the oracle --
+    also the sub-FFT length of the distributed 2^30 four-step."""
+    import paper_cs_0103001_b200 as b
+
+    n = 32768
+    x = fixtures.complex_input(batch * n, fixtures.NORMAL, seed=1900 + batch).reshape(batch, n)
+    p = b.Plan((n,), batch=batch)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    p.forward(xd, yd)
+    zd = yd.clone()
+    p.inverse(zd, zd)  # in place
+    torch.cuda.synchronize()
+    y = yd.cpu().numpy()
+    assert oracle.rel_l2(y, oracle.fft_batch(x)) <= 1e-5
+    assert oracle.rel_l2(zd.cpu().numpy(), oracle.fft_batch(y, inverse=True)) <= 1e-5
+    assert p.last_launch_count() == 1
+    p.destroy()
+
+
 def test_c2_two_plans_two_streams(fft):
     """Two plans (each with its own Y-ring workspace) running concurrently on
     two streams, forward on one and inverse on the other."""
