@@ -31,6 +31,17 @@ struct AbCtl {
     int D, ring;                    // dependency distance (transforms), ring slots
 };
 
+// optional outer four-step twiddle fused into the 32768-point B epilogue
+// (the distributed 2^30 four-step's step (T), else k_twiddle4): output k of
+// transform b times W_n^{(row0 + b) k}, W_n^x = a[x >> sh] * b[x & mask]
+// (fp64-generated tables, x < n: no wrap); a == nullptr: none
+struct OuterTw {
+    const float2* a;
+    const float2* b;
+    int sh;
+    int64_t row0;
+};
+
 // ---- mbarrier / bulk-copy / TMA primitives (sm_90+ PTX) ------------------
 __device__ __forceinline__ void bk_mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
@@ -460,8 +471,9 @@ __device__ __forceinline__ void st_task_b(float2* st, int lo, int hi, int bar, u
 // step 0 radix 16 over r (8 lanes j per line), the XOR-layout exchange,
 // step 1 radix 8 over j with W_128^{q j} (q = lt + 8 b, line-fastest):
 // X[k2 + 256 k1], k1 = q + 16 m -- a warp stores 32 consecutive k2 (256 B).
-template <bool INV>
-__device__ __forceinline__ void st_task_b128(float2* st, int tid, int bar, uint32_t empty, float2* x0) {
+template <bool INV, bool OTW>
+__device__ __forceinline__ void st_task_b128(float2* st, int tid, int bar, uint32_t empty, float2* x0, OuterTw ow,
+                                             int64_t tb, int k2base) {
     const int L0 = tid >> 3, j = tid & 7;
     float2 v[16];
     const float2* src = st + L0 * 128;
@@ -480,12 +492,39 @@ __device__ __forceinline__ void st_task_b128(float2* st, int tid, int bar, uint3
         for (int r = 0; r < 8; ++r) v[b * 8 + r] = st[big_bx(q + 16 * r, line)];
     }
     bk_arrive(empty);
+    // outer twiddle W^{R k}, k = k2 + 256 (q + 16 m): per b the value at m = 0
+    // and the step W^{4096 R} (loaded here: their latency overlaps step 1)
+    float2 ha[2], la[2], hs = make_float2(0.f, 0.f), ls = hs;
+    const int64_t R = ow.row0 + tb, msk = ((int64_t)1 << ow.sh) - 1;
+    if constexpr (OTW) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int64_t x = R * (int64_t)(k2base + line + 256 * (lt + 8 * b));
+            ha[b] = __ldg(ow.a + (x >> ow.sh));
+            la[b] = __ldg(ow.b + (x & msk));
+        }
+        const int64_t xs = R * 4096;
+        hs = __ldg(ow.a + (xs >> ow.sh));
+        ls = __ldg(ow.b + (xs & msk));
+    }
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
         const int q = lt + 8 * b;
 #pragma unroll
         for (int r = 1; r < 8; ++r) v[b * 8 + r] = cmul_dir<INV>(v[b * 8 + r], c_w256[(2 * q * r) & 255]);
         dft<8, INV>(v + b * 8);
+    }
+    if constexpr (OTW) {
+        const float2 ws = cmul(hs, ls);
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            float2 w = cmul(ha[b], la[b]);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                v[b * 8 + m] = cmul_dir<INV>(v[b * 8 + m], w);
+                if (m < 7) w = cmul(w, ws);
+            }
+        }
     }
     float2* x = x0 + line;
 #pragma unroll
@@ -495,12 +534,13 @@ __device__ __forceinline__ void st_task_b128(float2* st, int tid, int bar, uint3
 }
 
 // L = 65536 (C2: N1 = N2 = 256, 16 A + 16 B tasks per transform) or 32768
-// (N1 = 128, N2 = 256: 8 A tasks of 16 columns, 8 B tasks of 32 Y rows)
-template <bool INV, int NS, int MINB, int L = 65536>
+// (N1 = 128, N2 = 256: 8 A tasks of 16 columns, 8 B tasks of 32 Y rows;
+// OTW: with the outer four-step twiddle `ow` in the B epilogue)
+template <bool INV, int NS, int MINB, int L = 65536, bool OTW = false>
 __global__ void __launch_bounds__(320, MINB)
     k_ab_st(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_yld,
             float2* __restrict__ ring, float2* __restrict__ out, int64_t batch, float scale,
-            const float2* __restrict__ tw4, const float2* __restrict__ tw256, AbCtl ctl, int opts) {
+            const float2* __restrict__ tw4, const float2* __restrict__ tw256, AbCtl ctl, int opts, OuterTw ow) {
     using G = AbStCfg<NS>;
     constexpr int N1 = L / 256, T = N1 / 16, ROWS = 4096 / N1;  // B task: ROWS Y rows of N1
     constexpr int NSIG = G::NSIG;
@@ -623,7 +663,7 @@ __global__ void __launch_bounds__(320, MINB)
             if constexpr (L == 65536)
                 st_task_b<INV>(st, lo, hi, 1, empty0 + 8 * s, out + b * 65536 + part * 16, tw256, opts);
             else
-                st_task_b128<INV>(st, tid, 1, empty0 + 8 * s, out + b * L + part * ROWS);
+                st_task_b128<INV, OTW>(st, tid, 1, empty0 + 8 * s, out + b * L + part * ROWS, ow, b, part * ROWS);
         }
     }
     // done: tell the signaller (once its slot is free)

@@ -52,7 +52,9 @@ int c2_kind() {
     if (v && !strcmp(v, "ws")) return (int)C2_WS;
     return (int)C2_ST;
 }
-const void* c2_kernel(int kind, bool inv, int64_t n = 65536) {
+const void* c2_kernel(int kind, bool inv, int64_t n = 65536, bool otw = false) {
+    if (n == 32768 && otw)
+        return inv ? (const void*)k_ab_st<true, 2, 3, 32768, true> : (const void*)k_ab_st<false, 2, 3, 32768, true>;
     if (n == 32768) return inv ? (const void*)k_ab_st<true, 2, 3, 32768> : (const void*)k_ab_st<false, 2, 3, 32768>;
     if (kind == C2_ST) return inv ? (const void*)k_ab_st<true, 2, 3> : (const void*)k_ab_st<false, 2, 3>;
     return inv ? (const void*)k_ab_ws<true> : (const void*)k_ab_ws<false>;
@@ -185,7 +187,7 @@ int ab_opts(int kind) {
 
 template <bool INV, int64_t L = 65536>
 cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, const void* tw4, const void* tw,
-                      void* ws, size_t ws_bytes, cudaStream_t st) {
+                      void* ws, size_t ws_bytes, cudaStream_t st, OuterTw ow = OuterTw{}) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -222,10 +224,11 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     float2* a_ring = reinterpret_cast<float2*>(ring);
     float2* a_out = reinterpret_cast<float2*>(out);
     void* args_ws[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
-    void* args_st[] = {&m_x, &m_yld, &a_ring, &a_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
+    OuterTw a_ow = ow;
+    void* args_st[] = {&m_x, &m_yld, &a_ring, &a_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts, &a_ow};
     int grid = g.grid[kind][INV ? 1 : 0];
     if (L != 65536) {  // the 32768-point instantiation: its own occupancy (same resources)
-        const void* k = c2_kernel(C2_ST, INV, L);
+        const void* k = c2_kernel(C2_ST, INV, L, ow.a != nullptr);
         int occ = 0, sms = 0;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2_smem(C2_ST));
         if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c2_threads(C2_ST), c2_smem(C2_ST));
@@ -266,7 +269,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
         attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.numAttrs = 2;
     }
-    return cudaLaunchKernelExC(&cfg, c2_kernel(kind, INV, L), kind == C2_WS ? args_ws : args_st);
+    return cudaLaunchKernelExC(&cfg, c2_kernel(kind, INV, L, ow.a != nullptr), kind == C2_WS ? args_ws : args_st);
 }
 
 // k_ab_pair (fft_c2pair.cuh): one 2-CTA cluster per transform, Y in TMEM;
@@ -374,10 +377,15 @@ size_t c2_workspace_bytes(int64_t batch, int64_t n) {
 }
 
 cudaError_t launch_c2(bool inv, int64_t n, const void* in, void* out, int64_t batch, double scale, const void* tw4,
-                      const void* tw, void* ws, size_t ws_bytes, cudaStream_t st) {
-    if (n == 32768)
-        return inv ? ab_launch<true, 32768>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st)
-                   : ab_launch<false, 32768>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st);
+                      const void* tw, void* ws, size_t ws_bytes, cudaStream_t st, const void* ow_a, const void* ow_b,
+                      int ow_sh, int64_t ow_row0) {
+    if (n == 32768) {
+        const OuterTw ow{reinterpret_cast<const float2*>(ow_a), reinterpret_cast<const float2*>(ow_b), ow_sh,
+                         ow_row0};
+        return inv ? ab_launch<true, 32768>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st, ow)
+                   : ab_launch<false, 32768>(in, out, batch, scale, tw4, tw, ws, ws_bytes, st, ow);
+    }
+    if (ow_a) return cudaErrorInvalidValue;  // the outer twiddle is fused for 32768-point rows only
     if (c2_pair_selected())
         return inv ? pair_launch<true>(in, out, batch, scale, tw4, tw, st)
                    : pair_launch<false>(in, out, batch, scale, tw4, tw, st);

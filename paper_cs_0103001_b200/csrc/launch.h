@@ -191,8 +191,11 @@ void c2_plan_release(int dev);
 // the device's persisting-L2 set-aside for an L2 ring of ring_bytes (the
 // largest requested; released with the last acquiring plan)
 void l2_persist_request(int dev, size_t ring_bytes);
+// ow_a / ow_b / ow_sh / ow_row0: optional outer four-step twiddle W_n^{(row0
+// + b) k} on output k of transform b (n = 32768 only; ow_a = nullptr: none)
 cudaError_t launch_c2(bool inv, int64_t n, const void* in, void* out, int64_t batch, double scale, const void* tw4,
-                      const void* tw, void* ws, size_t ws_bytes, cudaStream_t st);
+                      const void* tw, void* ws, size_t ws_bytes, cudaStream_t st, const void* ow_a = nullptr,
+                      const void* ow_b = nullptr, int ow_sh = 0, int64_t ow_row0 = 0);
 
 // the constant step-twiddle tables of the task-pipeline modules (one copy per
 // module, fft_engine.cuh c_w256), uploaded for the current device

@@ -191,6 +191,13 @@ struct fft_plan_s {
     void* ftb = nullptr;          // W_n^{i}
     int fsh = 0;
     double scale_override = 0.0;  // sub-plans: scale of the last pass (0 = the default)
+    // sub-plans: the outer four-step twiddle fused into the one-pass 32768-
+    // point kernel (run_1d sets otw_done when it applied it)
+    const void* otw_a = nullptr;
+    const void* otw_b = nullptr;
+    int otw_sh = 0;
+    int64_t otw_row0 = 0;
+    bool otw_done = false;
     // two-pass 2^30 (fft_big.cuh): W_32768^x, W_n^{i 32768}, W_n^i (i < 32768)
     void* big_twl = nullptr;
     void* big_hi = nullptr;
@@ -346,7 +353,10 @@ fft_status run_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaStream
         // it writes it, so out == in is safe
         fft_status s = ensure_workspace(p);  // the Y ring and the task counters
         if (s != FFT_OK) return s;
-        e = launch_c2(inv, p->n0, in, out, p->batch, scale, p->tw4, p->tw, p->ws, p->ws_bytes, st);
+        const bool fuse = p->otw_a && p->n0 == 32768;
+        e = launch_c2(inv, p->n0, in, out, p->batch, scale, p->tw4, p->tw, p->ws, p->ws_bytes, st,
+                      fuse ? p->otw_a : nullptr, p->otw_b, p->otw_sh, p->otw_row0);
+        p->otw_done = fuse && e == cudaSuccess;
         p->last_launches = 1;
         if (e != cudaSuccess) return cuda_fail(e, "k_ab_ws launch");
         return FFT_OK;
@@ -1400,6 +1410,34 @@ fft_status run_paper_tree(fft_plan_s* p, const void* in, void* out, cudaStream_t
 #endif
 }
 
+// Steps (A) + (T) of the distributed four-step on one local slab [S1][N2],
+// in place: the sub-FFTs over n2, then W_n^{(row0 + i) k2} -- fused into the
+// epilogue of the one-pass 32768-point kernel when that kernel runs them
+// (complex64, N2 = 32768; B200FFT_NO_TWFUSE=1: not fused), else the separate
+// k_twiddle4 pass.
+fft_status run_1d_twiddled(fft_plan_s* p, void* a, bool inv, int64_t row0, cudaStream_t st, int* launches) {
+    fft_plan_s* sa = p->sub_a;
+    const char* nf = getenv("B200FFT_NO_TWFUSE");
+    if (p->prec == 0 && sa->tw4 && sa->n0 == 32768 && !(nf && nf[0] == '1')) {
+        sa->otw_a = p->fta;
+        sa->otw_b = p->ftb;
+        sa->otw_sh = p->fsh;
+        sa->otw_row0 = row0;
+    }
+    fft_status s = run_1d(sa, a, a, inv, st);
+    const bool fused = sa->otw_done;
+    sa->otw_a = sa->otw_b = nullptr;
+    sa->otw_done = false;
+    if (s != FFT_OK) return s;
+    *launches += sa->last_launches;
+    if (!fused) {
+        cudaError_t e = launch_twiddle4(p->prec, inv, a, sa->batch, p->fs2, row0, p->fta, p->ftb, p->fsh, st);
+        if (e != cudaSuccess) return cuda_fail(e, "twiddle");
+        ++*launches;
+    }
+    return FFT_OK;
+}
+
 // Fused form of the schedule below: each pack -> all-to-all -> unpack is ONE
 // distributed-transpose launch (k_dist_transpose) whose stores go straight
 // into the other ranks' receive slabs (peer memory) -- the last one pulls
@@ -1472,12 +1510,8 @@ fft_status run_dist_1d_fused(fft_plan_s* p, const void* in, void* out, bool inv,
     // 2. (A) FFT over n2 (unnormalised) and (T) the four-step twiddle
     for (int l = 0; l < nloc; ++l) {
         char* a = buf(0, r0 + l);
-        s = run_1d(p->sub_a, a, a, inv, st);
+        s = run_1d_twiddled(p, a, inv, (int64_t)(r0 + l) * S1, st, &launches);
         if (s != FFT_OK) return s;
-        launches += p->sub_a->last_launches;
-        e = launch_twiddle4(p->prec, inv, a, S1, N2, (int64_t)(r0 + l) * S1, p->fta, p->ftb, p->fsh, st);
-        if (e != cudaSuccess) return cuda_fail(e, "twiddle");
-        ++launches;
     }
     prof_mark(p, st, "FFT over n2 + twiddle");
     // 3. phase A [N1][N2] (rows n1) -> phase B [N2][N1] slabs of S2 rows; push
@@ -1555,12 +1589,8 @@ fft_status run_dist_1d(fft_plan_s* p, const void* in, void* out, bool inv, cudaS
     }
     // 3. (A) FFT over n2 (unnormalised) and (T) the four-step twiddle
     for (int l = 0; l < nloc; ++l) {
-        s = run_1d(p->sub_a, slab(w0, l), slab(w0, l), inv, st);
+        s = run_1d_twiddled(p, slab(w0, l), inv, (int64_t)(r0 + l) * S1, st, &launches);
         if (s != FFT_OK) return s;
-        launches += p->sub_a->last_launches;
-        e = launch_twiddle4(p->prec, inv, slab(w0, l), S1, N2, (int64_t)(r0 + l) * S1, p->fta, p->ftb, p->fsh, st);
-        if (e != cudaSuccess) return cuda_fail(e, "twiddle");
-        ++launches;
     }
     // 4. pack [S1][N2] -> [N2][S1] (block q = rows k2 of rank q), exchange, unpack to [S2][N1]
     e = launch_transpose(p->prec, w0, w1, S1, N2, nloc, st);
