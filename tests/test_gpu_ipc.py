@@ -73,6 +73,26 @@ def _worker(rank, world, port, case, q):
             torch.cuda.synchronize()
             res["fwd"], res["inv"] = F.cpu().numpy(), G.cpu().numpy()
             res["launches"] = p.last_launch_count()
+        elif case[0] == "c5":
+            # BASELINE configs[4]: 2^30 over the processes (32768 x 32768
+            # four-step, 32768-point sub-FFTs with the fused outer twiddle);
+            # each rank returns the sampled bins it owns
+            _, bins_f, bins_i = case
+            n = 1 << 30
+            loc = n // world
+            x = np.empty(loc, np.complex64)
+            p = b.Plan((n,), batch=1)
+            p.set_host_collectives(world, rank, allgather, dist.barrier)
+            for name, seed, bins, fwd in (("fwd", 5, bins_f, True), ("inv", 105, bins_i, False)):
+                fixtures.complex_input(loc, fixtures.NORMAL, seed=seed, offset=rank * loc, out=x)
+                xd = torch.from_numpy(x).cuda()
+                yd = torch.empty_like(xd)
+                (p.forward if fwd else p.inverse)(xd, yd)
+                torch.cuda.synchronize()
+                mine = [int(k) for k in bins if rank * loc <= k < (rank + 1) * loc]
+                idx = torch.tensor([k - rank * loc for k in mine], dtype=torch.int64, device="cuda")
+                res[name] = dict(zip(mine, yd[idx].cpu().numpy().tolist()))
+                del xd, yd
         else:
             _, m = case
             n = 1 << m
@@ -144,3 +164,23 @@ def test_processes_fused_four_step_1d(world, m):
     inv = np.concatenate([res[r]["inv"] for r in range(world)])
     assert oracle.rel_l2(fwd, oracle.fft(x)) <= 1e-5
     assert oracle.rel_l2(inv, oracle.ifft(x)) <= 1e-5
+
+
+def test_processes_c5_shape():
+    """C5's shape (n = 2^30) over 2 processes: forward on seed 5 and inverse
+    on seed 105, 64 bins each against the oracle's direct sums (SURVEY 8(c)
+    O7) -- the distributed four-step with the 32768-point one-pass sub-FFTs
+    and the cross-process transposes."""
+    n = 1 << 30
+    rng_f, rng_i = np.random.default_rng(5), np.random.default_rng(105)
+    bins_f = np.concatenate([[0, 1, n // 2, n - 1], rng_f.integers(0, n, 60)]).astype(np.int64)
+    bins_i = np.concatenate([[0, 1, n // 2, n - 1], rng_i.integers(0, n, 60)]).astype(np.int64)
+    res = _run(2, ("c5", bins_f.tolist(), bins_i.tolist()))
+    x = np.empty(n, np.complex64)
+    for name, seed, bins, inv in (("fwd", 5, bins_f, False), ("inv", 105, bins_i, True)):
+        got = {}
+        for r in range(2):
+            got.update(res[r][name])
+        fixtures.complex_input(n, fixtures.NORMAL, seed=seed, out=x)
+        ref = oracle.dft_bins(x, bins, inverse=inv)
+        assert oracle.rel_l2(np.array([got[int(k)] for k in bins]), ref) <= 1e-5
