@@ -269,16 +269,18 @@ __global__ void __launch_bounds__(NG*(R / E), 1)
 // transposed into `out` (PAIR2 = 2: complex (a, 0), (b, 0); 1: real pairs).
 // One launch instead of two saves the second launch's ramp and tail (the
 // C3 breakdown: ~15 us of the 40 were launch + first-load latency).
-// Grid barrier (self-resetting, so a launch needs no host-side state and a
-// CUDA-graph replay of it is correct): gbar[0] counts arrivals, gbar[1] is
-// the generation.  Thread 0 of every CTA reads the generation (it cannot
-// advance before this CTA arrives), releases the CTA's pass-1 stores at gpu
-// scope (bar.sync + fence.acq_rel.gpu: cumulative) and arrives; the last
-// arrival resets the count and advances the generation (release); the
-// others wait for the generation to change (acquire).  Then a proxy fence
-// orders the generic-proxy stores before the TMA (async proxy) reads of
-// pass 2.  All CTAs are co-resident (cooperative launch); launches of one
-// plan are stream-ordered, so they never share the counter at once.
+// Grid barrier without host-side state (so a CUDA-graph replay of a launch
+// is correct): *gbar counts arrivals and only grows; thread 0 of every CTA
+// reads it at kernel start -- before its own arrival, so between k grid and
+// k grid + grid - 1 when k launches (of this plan, same grid) completed --
+// and waits for target = (k + 1) grid.  At the barrier it releases the
+// CTA's pass-1 stores at gpu scope (bar.sync + fence.acq_rel.gpu:
+// cumulative), arrives, and polls (acquire); then a proxy fence orders the
+// generic-proxy stores before the TMA (async proxy) reads of pass 2.  All
+// CTAs are co-resident (cooperative launch); launches of one plan are
+// stream-ordered, so they never share the counter at once.  (A host-passed
+// target -- the earlier form -- is frozen by graph capture: a replay would
+// pass the barrier early.)
 // ---------------------------------------------------------------------------
 template <int R, int E, int W, int STAGES, int PAIR2, int MLX = 0>
 __global__ void __launch_bounds__(W*(R / E), 1)
@@ -289,7 +291,11 @@ __global__ void __launch_bounds__(W*(R / E), 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t bar0 = smem_addr_u32(smem_raw + STAGES * G::STAGE_BYTES);
     const uint32_t bar1 = bar0 + 8 * STAGES;
+    unsigned long long target = 0;  // thread 0: this launch's barrier count
     if (threadIdx.x == 0) {
+        unsigned long long c0;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(c0) : "l"(gbar) : "memory");
+        target = (c0 / gridDim.x + 1) * (unsigned long long)gridDim.x;
         for (int s = 0; s < 2 * STAGES; ++s) mbar_init(bar0 + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         rows_tma_issue_first<float, R, E, W, false, STAGES>(in_, lines, smem_raw, bar0);
@@ -299,19 +305,13 @@ __global__ void __launch_bounds__(W*(R / E), 1)
                                                                            smem_raw, bar0);
     // ---- grid barrier (the loop ended with a __syncthreads) ----
     if (threadIdx.x == 0) {
-        unsigned long long g0, v, old;
-        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(g0) : "l"(gbar + 1) : "memory");
         asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;\n" : "=l"(old) : "l"(gbar) : "memory");
-        if (old == (unsigned long long)gridDim.x - 1) {
-            asm volatile("st.relaxed.gpu.global.u64 [%0], 0;\n" ::"l"(gbar) : "memory");
-            asm volatile("red.release.gpu.global.add.u64 [%0], 1;\n" ::"l"(gbar + 1) : "memory");
-        } else {
-            for (;;) {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(gbar + 1) : "memory");
-                if (v != g0) break;
-                __nanosleep(64);
-            }
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;\n" ::"l"(gbar) : "memory");
+        unsigned long long v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(gbar) : "memory");
+            if (v >= target) break;
+            __nanosleep(64);
         }
         asm volatile("fence.proxy.async.global;\n" ::: "memory");
         rows_tma_issue_first<float, R, E, W, false, STAGES>(mid, lines, smem_raw, bar1);

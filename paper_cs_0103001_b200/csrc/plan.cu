@@ -202,9 +202,9 @@ struct fft_plan_s {
     void* big_twl = nullptr;
     void* big_hi = nullptr;
     void* big_lo = nullptr;
-    // grid-barrier state of the fused two-pass pipeline (k_rows_tma2): the
-    // arrival count and the generation (plan-owned, zeroed once; the barrier
-    // resets the count itself, so graph replays need no host-side state)
+    // grid-barrier arrival count of the fused two-pass pipeline (k_rows_tma2;
+    // plan-owned, zeroed once, only grows; each launch derives its target
+    // from it on the device, so graph replays need no host-side state)
     unsigned long long* gbar = nullptr;
     // k_colfilt's task counters (plan-owned, grown on demand)
     void* cws = nullptr;
@@ -634,7 +634,7 @@ cudaError_t colfilt(fft_plan_s* p, void* grid, int64_t SM, int64_t nimg, double 
     return launch_colfilt(grid, SM, nimg, scale, p->tw, p->twl, p->gu, gv, col_off, p->cws, p->cws_bytes, st);
 }
 
-// the fused pipeline's grid-barrier state (zeroed once; self-resetting)
+// the fused pipeline's grid-barrier count (zeroed once; only grows)
 cudaError_t ensure_gbar(fft_plan_s* p, cudaStream_t st) {
     if (p->gbar) return cudaSuccess;
     cudaError_t e = cudaMalloc(&p->gbar, 256);
