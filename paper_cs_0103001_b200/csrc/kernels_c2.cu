@@ -69,6 +69,7 @@ size_t c2_smem(int kind) { return kind == C2_WS ? AbWsCfg::SMEM : AbStCfg<2>::SM
 // threads / devices may launch concurrently.
 struct AbGeom {
     int grid[C2_NKIND][2] = {};  // [kind][inverse]
+    int grid32[2][2] = {};       // k_ab_st<32768>: [outer twiddle][inverse]
     int D = 0, ring = 0;
     bool limit_set = false;
     size_t limit = 0;  // the persisting set-aside requested so far (the largest ring)
@@ -93,6 +94,15 @@ cudaError_t ab_geom(int dev, AbGeom* g) {
                     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c2_threads(kind), c2_smem(kind));
                 t.grid[kind][d] = sms * (occ > 0 ? occ : 1);
                 gmax = t.grid[kind][d] > gmax ? t.grid[kind][d] : gmax;
+            }
+        for (int o = 0; o < 2 && e == cudaSuccess; ++o)
+            for (int d = 0; d < 2 && e == cudaSuccess; ++d) {
+                const void* k = c2_kernel(C2_ST, d != 0, 32768, o != 0);
+                int occ = 0;
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2_smem(C2_ST));
+                if (e == cudaSuccess)
+                    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c2_threads(C2_ST), c2_smem(C2_ST));
+                t.grid32[o][d] = sms * (occ > 0 ? occ : 1);
             }
         if (e != cudaSuccess) return e;
         // every wait must point at least (tasks in flight per CTA) x grid
@@ -226,16 +236,7 @@ cudaError_t ab_launch(const void* in, void* out, int64_t batch, double scale, co
     void* args_ws[] = {&m_x, &m_yst, &m_yld, &m_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts};
     OuterTw a_ow = ow;
     void* args_st[] = {&m_x, &m_yld, &a_ring, &a_out, &a_batch, &a_scale, &a_tw4, &a_tw, &c, &a_opts, &a_ow};
-    int grid = g.grid[kind][INV ? 1 : 0];
-    if (L != 65536) {  // the 32768-point instantiation: its own occupancy (same resources)
-        const void* k = c2_kernel(C2_ST, INV, L, ow.a != nullptr);
-        int occ = 0, sms = 0;
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2_smem(C2_ST));
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, c2_threads(C2_ST), c2_smem(C2_ST));
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e != cudaSuccess) return e;
-        grid = sms * (occ > 0 ? occ : 1);
-    }
+    const int grid = L == 65536 ? g.grid[kind][INV ? 1 : 0] : g.grid32[ow.a != nullptr][INV ? 1 : 0];
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
