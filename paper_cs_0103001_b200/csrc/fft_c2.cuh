@@ -409,7 +409,11 @@ __device__ __forceinline__ void st_task_a(float2* st, int lo, int hi, int bar, u
     }
     // Y[k2][n1] = v[q] * W_N^{n1 k2} * scale, k2 = hi + 16 q
     float2 wm = cscale(wm0, scale);
-    float2* y = y0 + (int64_t)hi * N1 + n1;
+    // N1 = 128: Y rows stored with column n1 ^ 8 (k2 mod 4) (k2 mod 4 = hi mod
+    // 4 here) so that st_task_b128's step-0 reads of 4 rows per warp hit
+    // distinct banks (1 KiB rows alone put them on the same 16 banks)
+    const int yc = N1 == 128 ? (n1 ^ (8 * (hi & 3))) : n1;
+    float2* y = y0 + (int64_t)hi * N1 + yc;
     const uint64_t keep = tmaops::policy_evict_last();
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
@@ -474,11 +478,11 @@ __device__ __forceinline__ void st_task_b(float2* st, int lo, int hi, int bar, u
 template <bool INV, bool OTW>
 __device__ __forceinline__ void st_task_b128(float2* st, int tid, int bar, uint32_t empty, float2* x0, OuterTw ow,
                                              int64_t tb, int k2base) {
-    const int L0 = tid >> 3, j = tid & 7;
+    const int L0 = tid >> 3, j = tid & 7, sw = L0 & 3;  // row L0 stored with column ^ 8 (L0 mod 4)
     float2 v[16];
-    const float2* src = st + L0 * 128;
+    const float2* src = st + L0 * 128 + j;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = src[j + 8 * r];
+    for (int r = 0; r < 16; ++r) v[r] = src[8 * (r ^ sw)];
     dft<16, INV>(v);
     grp_sync(bar);
 #pragma unroll

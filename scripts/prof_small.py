@@ -20,6 +20,15 @@ if which in ("all", "c2"):
     torch.cuda.synchronize()
     p.forward(x, y)
     torch.cuda.synchronize()
+if which in ("all", "r32k"):  # 32768-point rows (k_ab_st<32768>), 32768 rows
+    x = torch.from_numpy(fixtures.complex_input(32768 * 32768, 1, seed=7).reshape(32768, 32768)).to(dev)
+    y = torch.empty_like(x)
+    p = b.Plan((32768,), batch=32768)
+    p.forward(x, y)
+    torch.cuda.synchronize()
+    p.forward(x, y)
+    torch.cuda.synchronize()
+    del x, y
 if which in ("all", "c3"):
     img = torch.from_numpy(fixtures.sky_image(2048, 2048, seed=3)).to(dev)
     out = torch.empty((2048, 2048), dtype=torch.complex64, device=dev)
