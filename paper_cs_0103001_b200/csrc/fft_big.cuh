@@ -190,8 +190,10 @@ __global__ void __launch_bounds__(320, 3)
             bk_arrive(empty0 + 8 * s);
             if (PASS == 2) wm = cscale(wm, scale);
             // pass 1: ring[kc][a][16 n1]; pass 2: ring[kc][r][128 a]
+            // (pass 2: line (kc, r) stored with element a at a ^ 8 (r mod 4), so
+            // the B task's step-0 reads of 4 lines per warp hit distinct banks)
             float2* y = PASS == 1 ? slot + (int64_t)hi * 2048 + a * 16 + lo
-                                  : slot + (int64_t)hi * 2048 + (part >> 3) * 128 + a;
+                                  : slot + (int64_t)hi * 2048 + (part >> 3) * 128 + (a ^ (8 * ((part >> 3) & 3)));
 #pragma unroll
             for (int m = 0; m < 16; ++m) {
                 st_pol(y + m * 16 * 2048, cmul_dir<INV>(v[FA::pos_out(m)], wm), keep);
@@ -248,9 +250,10 @@ __global__ void __launch_bounds__(320, 3)
                 // [2 kc][16 r][128 a]: lines contiguous.  Step 0 (radix 16,
                 // span 1): line L = tid / 8, lane j = tid % 8, elements j + 8 r
                 const int L0 = tid >> 3, j = tid & 7;
-                const float2* src = st + L0 * 128;
+                const float2* src = st + L0 * 128 + j;
+                const int sw = L0 & 3;  // line stored with element a at a ^ 8 sw
 #pragma unroll
-                for (int r = 0; r < 16; ++r) v[r] = src[j + 8 * r];
+                for (int r = 0; r < 16; ++r) v[r] = src[8 * (r ^ sw)];
                 dft<16, INV>(v);
                 grp_sync(1);
                 // b[16 j + q] of line L0 -> XOR layout
