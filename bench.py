@@ -72,7 +72,9 @@ def roofline(alg_bytes, ms, kernel, tkey):
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": tb,
             "traffic_ratio": round(tb / alg_bytes, 3) if tb else None,
-            "alg_bytes": alg_bytes, "kernel": kernel, "peak_source": kind}
+            "alg_bytes": alg_bytes, "kernel": kernel, "peak_source": kind,
+            # also against the nominal 8 TB/s HBM3e figure
+            "frac_of_nominal_8000": round(achieved / 8000.0, 4)}
 
 
 # ------------------------------------------------------------------ clocks
