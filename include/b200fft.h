@@ -32,6 +32,13 @@
  *    returned synchronously; asynchronous CUDA faults surface on a later
  *    call.  After an error the output is undefined ("no partial result").
  *  - A plan is not thread-safe; distinct plans may be used concurrently.
+ *  - CUDA graphs: a single-GPU call may be captured on the plan's stream
+ *    after one warm-up call of the same kind (first calls allocate, set
+ *    kernel attributes and upload tables), and replayed with new data in
+ *    the captured buffers (per-launch state lives on the device).  Calls on
+ *    distributed plans are not capturable: their barriers synchronise on the
+ *    host or through the plan's NCCL communicator, and their receive slabs
+ *    alternate between two phases on the host.
  *  - Nothing throws across this ABI; every call returns an fft_status, and
  *    fft_last_error() gives a thread-local detail string for the last
  *    failure.
