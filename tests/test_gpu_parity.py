@@ -89,10 +89,11 @@ def test_1d_65536_multipass_fallback(fft, dtype, monkeypatch):
     assert oracle.rel_l2(run_1d(fft, x, inverse=True), oracle.fft_batch(x, inverse=True)) <= TOL[dtype]
 
 
-@pytest.mark.parametrize("case", ["1d-8", "1d-2048", "1d-8192", "1d-65536", "1d-2^17", "1d-2^21",
+@pytest.mark.parametrize("case", ["1d-8", "1d-2048", "1d-8192", "1d-32768", "1d-65536", "1d-65536pair",
+                                  "1d-2^17", "1d-2^21",
                                   "2d-256x512", "pipe-2048-real", "pipe-8192x16", "pipe-literal",
                                   "dist2d-4", "dist1d-4"])
-def test_no_writes_outside_the_buffers(fft, case):
+def test_no_writes_outside_the_buffers(fft, case, monkeypatch):
     """Canary bounds check (compute-sanitizer is not available on this pool):
     every call runs on the interior of a buffer whose 64 KiB guard zones on
     both sides hold a sentinel, for output and input; the guards must come
@@ -111,7 +112,11 @@ def test_no_writes_outside_the_buffers(fft, case):
         assert bool((buf[:G].cpu() == ref).all()) and bool((buf[G + n:].cpu() == ref).all())
 
     if kind == "1d":
-        n = {"8": 8, "2048": 2048, "8192": 8192, "65536": 65536, "2^17": 1 << 17, "2^21": 1 << 21}[rest]
+        if rest == "65536pair":  # k_ab_pair (C2 with Y in TMEM)
+            monkeypatch.setenv("B200FFT_C2", "pair")
+            rest = "65536"
+        n = {"8": 8, "2048": 2048, "8192": 8192, "32768": 32768, "65536": 65536, "2^17": 1 << 17,
+             "2^21": 1 << 21}[rest]
         batch = 3 if n <= 65536 else (2 if n < (1 << 21) else 1)
         p = b.Plan((n,), batch=batch)
         shapes = [(n * batch, lambda x, y: p.forward(x, y)), (n * batch, lambda x, y: p.inverse(x, y))]
