@@ -79,7 +79,9 @@ cudaError_t launch_colfilt(void* grid, int64_t M, int64_t nimg, double scale, co
     // phase distance: B(g) is 96 D positions after A(g), beyond the ~900
     // positions in flight; 2 D + ~10 groups (1 MiB each) live in L2
     const char* dv = getenv("B200FFT_COLS1_D");
-    ColPipeCtl c{ctr, ctr + groups, next, dv ? atoi(dv) : 32};
+    // (D = 24: C4 0.8095-0.8102 vs 0.8155-0.8167 ms at D = 32, same box,
+    // alternating; 16: 0.830, 40: 0.868)
+    ColPipeCtl c{ctr, ctr + groups, next, dv ? atoi(dv) : 24};
     float2* a_grid = reinterpret_cast<float2*>(grid);
     int64_t a_M = M, a_nimg = nimg;
     float a_scale = (float)scale;
